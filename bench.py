@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""bench.py -- ParaExp + Leapfrog (arXiv:1705.08019) on B200: FIT curl cell-updates/s and
+ParaExp wall time.
+
+One "step" = one full ParaExp solve (Algorithm 1, every SURVEY 8(a) row: particular leapfrog
+sweeps with the source, seed sync, Leja tails by Horner over the sub-interval propagators,
+NCCL reduce for N > 1, dt/2 reconstruction) of the default workload C3 (256^3 layered PEC
+cavity, fp64, n_t = 4096, p = 8) through the C ABI.  Inputs are resident in HBM when the timed
+region starts; the working set (815 MB per state vector) exceeds the 126 MB L2, so no L2
+flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c3-f32|c2|c1|c5-256]
+                  [--impl ours|reference] [--no-cpu-baseline]
+
+Under torchrun (N > 1) every rank runs one process per GPU; sub-intervals are sharded in
+contiguous blocks, tails summed with one ncclReduce (the library's own communicator).
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FIT curl cell-updates/s per GPU; ParaExp wall time & speedup at 1-8 B200"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+
+
+def workload(name):
+    from synth import config_c1, config_c2, config_c3, config_c5
+    if name == "c3":
+        return config_c3("f64", p=8, nsteps=4096)
+    if name == "c3-f32":
+        return config_c3("f32", p=8, nsteps=4096)
+    if name == "c3-p64":
+        return config_c3("f64", p=64, nsteps=4096)
+    if name == "c2":
+        return config_c2()
+    if name == "c1":
+        return config_c1()
+    if name.startswith("c5-"):
+        n = int(name.split("-")[1])
+        return config_c5(n=n, dtype="f64" if name.endswith("f64") else "f32")
+    raise SystemExit(f"unknown workload {name}")
+
+
+def hbm_peak():
+    try:
+        d = json.load(open(PEAKS_FILE))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region (200 ms)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+def cpu_baseline(w, budget_steps=None):
+    """The oracle as it stands, on the host cores, on a bounded sample of the workload:
+    leapfrog steps + one degree-8 Leja substep on the full grid (cell-updates/s)."""
+    from oracle import fit
+    g = fit.Grid.from_workload(w)
+    e, h = g.zeros()
+    nlf = budget_steps or (20 if w.cells <= 20_000_000 else 4)
+    t0 = time.perf_counter()
+    e, h = fit.leapfrog(g, e, h, nlf, w.sources, t0=0.0)
+    t1 = time.perf_counter()
+    plan = fit.make_plan("leja", 8, 1, 3 * g.dt, g.rho_cfl)
+    fit.expmv(g, plan, e + 1.0 * g.live_e, h, mode="pairs")
+    t2 = time.perf_counter()
+    cu = (nlf + 8) * w.cells
+    return {"value": cu / (t2 - t0), "unit": "cell-updates/s", "cores": fit.num_threads(),
+            "kind": "oracle",
+            "sample": f"{w.name} grid {w.nx}x{w.ny}x{w.nz} {w.dtype}: {nlf} leapfrog steps + one "
+                      f"degree-8 Leja substep (8 A-applications), plain C/OpenMP + numpy oracle",
+            "leapfrog_rate": nlf * w.cells / (t1 - t0), "expmv_rate": 8 * w.cells / (t2 - t1),
+            "seconds": t2 - t0}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (the only reference this paper-only tier has)."""
+    if rank != 0:
+        return
+    w = workload(args.workload)
+    steps = []
+    cb = None
+    for it in range(args.warmup + args.steps):
+        r = cpu_baseline(w, budget_steps=2)
+        if it >= args.warmup:
+            steps.append(r)
+        cb = r
+    value = statistics.median(s["value"] for s in steps)
+    ms = statistics.median(s["seconds"] for s in steps) * 1e3
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "cell-updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": w.dtype,
+        "data": "synthetic", "config": {"workload": w.name, "cells": w.cells, "nsteps": w.nsteps,
+                                        "p": w.p, "sample": cb["sample"]},
+        "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cb["cores"],
+                         "kind": "oracle", "sample": cb["sample"]},
+        "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernels", default="auto", choices=["auto", "unfused", "fused"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-serial", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1705_08019_b200 as pe
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workload(args.workload)
+    grid = pe.Grid.from_workload(w, device=local, kernels=args.kernels)
+    stream = torch.cuda.current_stream(local)
+    info = grid.info(compute_rho_pow=True, stream=stream.cuda_stream)
+    comm = pe.Comm(rank, world, local) if world > 1 else None
+    tdt = grid.torch_dtype()
+    e_out = torch.zeros(3 * grid.npts, dtype=tdt, device=f"cuda:{local}")
+    h_out = torch.zeros_like(e_out)
+    kw = dict(sources=w.sources, method=w.method, m=w.m, s=w.s, eps_A=w.eps_A, comm=comm)
+    u0 = None
+    if w.u0_seed is not None:
+        import numpy as np
+        e0, h0 = w.u0()
+        u0 = (torch.tensor(e0, dtype=tdt, device=f"cuda:{local}"),
+              torch.tensor(h0, dtype=tdt, device=f"cuda:{local}"))
+
+    def step():
+        return pe.solve(grid, w.nsteps, w.p, u0=u0, e_out=e_out, h_out=h_out, **kw)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events on the launching stream, max over ranks) ----
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    stats = [step() for _ in range(args.steps)]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms_local = ev0.elapsed_time(ev1)
+
+    cu_local = sum(s["cell_updates"] for s in stats)
+    launches_local = sum(s["kernel_launches"] for s in stats)
+    lf_ms = sum(s["ms_leapfrog_kernels"] for s in stats)
+    poly_ms = sum(s["ms_poly_kernels"] for s in stats)
+    lf_steps = sum(s["leapfrog_steps"] for s in stats)
+    a_apps = sum(s["a_applications"] for s in stats)
+    if world > 1:
+        t = torch.tensor([ms_local], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        c = torch.tensor([cu_local, launches_local], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(c)
+        cu, launches = float(c[0].item()), int(c[1].item())
+    else:
+        ms, cu, launches = ms_local, float(cu_local), launches_local
+    value = cu / (ms * 1e-3)
+
+    # ---- e2e through the public API with host buffers (pinned), D2H of the result ----
+    e_host = torch.empty(3 * grid.npts, dtype=tdt, pin_memory=True)
+    h_host = torch.empty_like(e_host)
+    u0_host = None
+    if u0 is not None:
+        u0_host = (u0[0].cpu().pin_memory(), u0[1].cpu().pin_memory())
+    barrier()
+    torch.cuda.synchronize()
+    e2e0 = torch.cuda.Event(enable_timing=True)
+    e2e1 = torch.cuda.Event(enable_timing=True)
+    e2e0.record(stream)
+    cu_e2e = 0
+    h2d = d2h = 0
+    q_bytes = w.nsteps * len(w.sources) * (8 if w.dtype == "f64" else 4)
+    for _ in range(args.steps):
+        ud = None
+        if u0_host is not None:
+            ud = (u0_host[0].to(f"cuda:{local}", non_blocking=True),
+                  u0_host[1].to(f"cuda:{local}", non_blocking=True))
+            h2d += 2 * u0_host[0].numel() * u0_host[0].element_size()
+        st = pe.solve(grid, w.nsteps, w.p, u0=ud, e_out=e_out, h_out=h_out, **kw)
+        h2d += q_bytes           # the library uploads the source amplitude table every call
+        cu_e2e += st["cell_updates"]
+        if rank == st["root"]:
+            e_host.copy_(e_out, non_blocking=True)
+            h_host.copy_(h_out, non_blocking=True)
+            d2h += 2 * e_out.numel() * e_out.element_size()
+    e2e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = e2e0.elapsed_time(e2e1)
+    if world > 1:
+        t = torch.tensor([ms_e2e, cu_e2e, h2d, d2h], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        s2 = t[1:].clone()
+        dist.all_reduce(s2)
+        ms_e2e, cu_e2e, h2d, d2h = float(t[0]), float(s2[0]), float(s2[1]), float(s2[2])
+
+    # ---- serial leapfrog over the same interval on 1 GPU (speedup denominator) ----
+    serial_ms = None
+    if not args.no_serial and rank == 0:
+        te = torch.zeros(3 * grid.npts, dtype=tdt, device=f"cuda:{local}")
+        th = torch.zeros_like(te)
+        if u0 is not None:
+            te.copy_(u0[0])
+            th.copy_(u0[1])
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        pe.leapfrog(grid, te, th, w.nsteps, w.sources)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        serial_ms = s0.elapsed_time(s1)
+    barrier()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel family (HBM bound) ----
+    es = 8 if w.dtype == "f64" else 4
+    per_cell = {0: 12, 1: 12, 2: 15}[info["material_mode"]]   # values per cell-update
+    peak, peak_kind = hbm_peak()
+    fam = []
+    if lf_ms > 0 and lf_steps > 0:
+        fam.append(("leapfrog", lf_ms, lf_steps))
+    if poly_ms > 0 and a_apps > 0:
+        fam.append(("expmv_pair", poly_ms, a_apps))
+    name, fam_ms, units = max(fam, key=lambda f: f[1])
+    bytes_per_unit = per_cell * es * w.cells
+    achieved = bytes_per_unit * units / (fam_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "kernel": name,
+                "peak_kind": peak_kind,
+                "algorithmic_bytes_per_cell_update": per_cell * es,
+                "share_of_step": fam_ms / ms_local if ms_local else None,
+                "leapfrog_ms": lf_ms, "expmv_ms": poly_ms}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": w.dtype,
+        "data": "synthetic",
+        "config": {"workload": w.name, "grid": [w.nx, w.ny, w.nz], "cells": w.cells,
+                   "nsteps": w.nsteps, "p": w.p, "method": w.method, "eps_A": w.eps_A,
+                   "rho": stats[-1]["rho"], "m": stats[-1]["m"], "s_per_subinterval": stats[-1]["s_first"],
+                   "material_mode": info["material_mode"], "kernels": args.kernels,
+                   "parallelism": f"paraexp time-parallel x{world}",
+                   "l2": "inputs larger than L2 (815 MB/state fp64), no flush"},
+        "per_gpu": value / world,
+        "paraexp": {"wall_ms": ms / args.steps, "serial_leapfrog_ms": serial_ms,
+                    "speedup_vs_serial_leapfrog": (serial_ms / (ms / args.steps)) if serial_ms else None,
+                    "leapfrog_steps_per_solve": stats[-1]["leapfrog_steps"],
+                    "a_applications_per_solve": stats[-1]["a_applications"]},
+        "roofline": roofline,
+        "e2e": {"value": cu_e2e / (ms_e2e * 1e-3), "unit": "cell-updates/s",
+                "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_baseline(w)
+    elif not args.no_cpu_baseline and rank == 0:
+        out["cpu_baseline"] = cpu_baseline(w)
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,276 @@
+/*
+ * paraexp.h -- C ABI of the B200-native ParaExp + Leapfrog library for FIT-discretised
+ * Maxwell equations (Merkel, Niyonzima, Schoeps, arXiv:1705.08019).
+ *
+ * Citations: PAPER:n = line n of the paper text; SPEC:n = line n of the
+ * CPU-program spec; "reading n" = DESIGN.md "Readings of the paper" item n.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  Grid       nx, ny, nz primal cells; (nx+1)(ny+1)(nz+1) = npts primal points.
+ *  Fields     "canonical layout" (PAPER:164-167 with n_dof = 3 npts, reading 3):
+ *             e = [e_x | e_y | e_z], h = [h_x | h_y | h_z], each component an array of
+ *             npts values indexed i + (nx+1)*(j + (ny+1)*k), x fastest.
+ *             e_x(i,j,k) is the primal edge (i,j,k)->(i+1,j,k); h_z(i,j,k) the dual edge
+ *             through the primal z-face spanned by e_x(i,j,k) and e_y(i,j,k).
+ *             Values are grid voltages: e in volts, h in amperes.
+ *             Element type = the grid dtype (double for PARAEXP_F64, float for F32).
+ *  Dead DOFs  PEC edges (tangential on the box, edges of PEC cells), virtual edges/faces
+ *             and boundary-normal faces are ZEROED by the library on input and are
+ *             always written as 0 (reading 5).
+ *  Pointers   Field pointers passed to leapfrog/expmv/solve are caller-owned DEVICE
+ *             pointers on the grid's device (e.g. torch tensors), unless stated.  The
+ *             library never frees them.  `stream` is a cudaStream_t (NULL = legacy
+ *             default stream); all device work is stream-ordered on it and the call
+ *             returns after enqueue unless it must read back a status flag (then it
+ *             synchronises that stream).
+ *  Errors     0 = PARAEXP_OK, negative = error (see codes), positive = warning bits.
+ *             paraexp_last_error() returns a thread-local message for the last failure.
+ *             On error the output buffers are unspecified.
+ *  Threads    A grid owns a device workspace: calls on one grid must not run
+ *             concurrently from several host threads.
+ */
+#ifndef PARAEXP_H
+#define PARAEXP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------------------ */
+#define PARAEXP_OK 0
+#define PARAEXP_EINVAL (-1)     /* invalid argument                                      */
+#define PARAEXP_ENOMEM (-2)     /* host or device allocation failed                     */
+#define PARAEXP_ECUDA (-3)      /* CUDA runtime / driver error                          */
+#define PARAEXP_ENCCL (-4)      /* NCCL error or NCCL library not loadable              */
+#define PARAEXP_EDIVERGED (-5)  /* non-finite field in leapfrog              */
+#define PARAEXP_EOVERFLOW (-6)  /* non-finite result of exp(tA)v             */
+#define PARAEXP_ENOTSUP (-7)    /* valid but unsupported request (e.g. host-only grid)  */
+#define PARAEXP_WCFL 1          /* warning bit: dt > dt_CFL (SPEC:189 warn, not forbid) */
+
+/* ---- enums ----------------------------------------------------------------------- */
+enum { PARAEXP_F64 = 0, PARAEXP_F32 = 1 };
+enum { PARAEXP_SRC_ZERO = 0, PARAEXP_SRC_GAUSS_PAPER = 1, PARAEXP_SRC_GAUSS_SINE = 2,
+       PARAEXP_SRC_SINE = 3 };
+enum { PARAEXP_TAYLOR = 0, PARAEXP_LEJA = 1 };
+enum { PARAEXP_TAIL_EXP = 0, PARAEXP_TAIL_LEAPFROG = 1 };
+enum { PARAEXP_MAT_SCALAR = 0, PARAEXP_MAT_ZTABLE = 1, PARAEXP_MAT_ARRAY = 2 };
+enum { PARAEXP_KERNELS_AUTO = 0, PARAEXP_KERNELS_UNFUSED = 1, PARAEXP_KERNELS_FUSED = 2 };
+
+#define PARAEXP_MAX_DEGREE 100
+#define PARAEXP_MAX_SOURCES 64
+
+/* ---- grid ------------------------------------------------------------------------ */
+/* Grid description (SPEC:30-35 grid, SPEC:63-67 materials).
+ *   nx, ny, nz  cells per axis, each >= 1 ("< 2 points" rejected)
+ *   dx, dy, dz  per-cell spacings in metres (length nx / ny / nz), or NULL => uniform d0
+ *   eps_r, mu_r per-cell relative permittivity / permeability, length nx*ny*nz, x fastest,
+ *               strictly positive and finite, or NULL => 1 (vacuum)
+ *   pec_cell    per-cell PEC flag (nonzero = PEC), or NULL => none (reading 5)
+ *   dtype       PARAEXP_F64 or PARAEXP_F32: storage and arithmetic type of every kernel
+ *   device      CUDA device ordinal, or -1 for a HOST-ONLY grid (coefficients, CFL and
+ *               plans only; every compute call on it returns PARAEXP_ENOTSUP)
+ *   dt, dt_frac exactly one > 0: explicit time step in seconds, or a fraction of the
+ *               eq:cfl bound dt_CFL.  dt is a grid property: it is baked
+ *               into cE = dt*M_eps^-1 and cH = dt*M_nu (reading 24)
+ *   kernels     PARAEXP_KERNELS_AUTO (fused z-marching kernels), _UNFUSED (one kernel
+ *               per curl half; debugging/parity baseline) or _FUSED
+ * All input arrays are host pointers, read during the call only. */
+typedef struct {
+    int32_t nx, ny, nz;
+    const double *dx, *dy, *dz;
+    double d0;
+    const double *eps_r, *mu_r;
+    const uint8_t *pec_cell;
+    int32_t dtype;
+    int32_t device;
+    double dt;
+    double dt_frac;
+    int32_t kernels;
+} paraexp_grid_desc;
+
+typedef struct paraexp_grid paraexp_grid;
+typedef struct paraexp_comm paraexp_comm;
+
+typedef struct {
+    int32_t nx, ny, nz, dtype;
+    int64_t npts;          /* (nx+1)(ny+1)(nz+1)                                        */
+    int64_t ndof_field;    /* 3*npts per field; the paper's n_dof counts e+h = 6*npts   */
+    int64_t cells;         /* nx*ny*nz                                                  */
+    double dt, dt_cfl;     /* seconds; dt_cfl per eq:cfl                                 */
+    double rho_cfl;        /* 2/dt_cfl, an upper bound of ||A||_2 (SURVEY finding 7)     */
+    double rho_pow;        /* Lanczos estimate of ||A||_2 (K5), 0 if not yet computed    */
+    int32_t material_mode; /* PARAEXP_MAT_*                                              */
+    int32_t kernels;       /* resolved kernel family                                     */
+    int64_t pitch_x;       /* device layout x pitch (elements)                           */
+    int64_t device_bytes;  /* bytes of device memory currently owned by the grid         */
+    int32_t device;
+    int32_t warnings;      /* PARAEXP_WCFL if dt > dt_cfl                                */
+} paraexp_grid_info_t;
+
+/* Create a grid: validates, assembles fp64 FIT coefficients on the host (standard FIT
+ * dual-facet averaging, reading 4), rounds them once to dtype and uploads them.
+ * *out receives a new grid owned by the caller (free with paraexp_grid_destroy).
+ * Returns PARAEXP_OK, PARAEXP_WCFL (created, dt > dt_CFL), or an error code. */
+int paraexp_grid_create(const paraexp_grid_desc *desc, paraexp_grid **out);
+void paraexp_grid_destroy(paraexp_grid *grid);
+/* Fill *out.  If compute_rho_pow != 0 and the grid is on a device, runs the Lanczos
+ * norm estimate K5 (40 steps, stream-synchronous on `stream`) and caches it. */
+int paraexp_grid_info(paraexp_grid *grid, int32_t compute_rho_pow, void *stream,
+                      paraexp_grid_info_t *out);
+/* Export the fp64 coefficients the library assembled, canonical layout, host pointers of
+ * 3*npts doubles each: cE = dt*M_eps^-1 (0 on dead edges), cH = dt*M_nu (0 on dead faces).
+ * Host-side; works on host-only grids.  (Used to check the host assembly.) */
+int paraexp_grid_coefficients(const paraexp_grid *grid, double *cE, double *cH);
+
+/* ---- sources ---------------------------------------------------------------------- */
+/* An edge current (eq:line_current; reading 6): primal edge (comp, i,j,k),
+ * comp 0/1/2 = x/y/z.  The edge must be live.  The injected current at global step m is
+ * jhat = weight * i(t0 + (m + 1/2) dt) amperes, subtracted in the e-update:
+ *   e_s <- e_s - fl_T(cE64_s * jhat)       (PAPER:232 '-j'; PAPER:647 g = -[0, j]).
+ * Waveforms i(t):
+ *   ZERO         0
+ *   GAUSS_PAPER  amp * exp(-4 ((t - t_param)/t_param)^2)                 (eq:line_current)
+ *   GAUSS_SINE   amp * sin(2 pi f0 (t - t_delay)) * exp(-((t - t_delay)/t_param)^2)
+ *   SINE         amp * sin(2 pi f0 t)                                                    */
+typedef struct {
+    int32_t comp, i, j, k;
+    int32_t kind;
+    double weight, amp, t_param, f0, t_delay;
+} paraexp_source;
+
+/* ---- statistics / SMVP ledger ------------------------------------ */
+typedef struct {
+    int64_t curl_applications; /* SMVPs: leapfrog counts 2 per step (eq:cost_LF), an
+                                  A-application counts 2 curl halves                    */
+    int64_t a_applications;    /* A-applications of exp(tA)v polynomials (n_Leja)       */
+    int64_t leapfrog_steps;
+    int64_t substeps;          /* polynomial substeps (sum of s)                         */
+    int64_t kernel_launches;   /* device kernels launched by the call                    */
+    int64_t cell_updates;      /* (leapfrog steps + A-applications) * cells              */
+    double rho;                /* spectral bound used by the plans                        */
+    int32_t method, m, s_first, s_last, m_half, s_half; /* plans used (solve: E_1 / E_p)  */
+    int32_t root;              /* solve: rank owning sub-interval p (holds the output)    */
+    int32_t first_interval, last_interval; /* solve: block owned by this rank (1-based)   */
+    int32_t fail_interval;     /* solve: sub-interval index of a divergence, else 0       */
+    double ms_particular, ms_tails, ms_reduce, ms_finish, ms_total; /* device-event times */
+    double ms_leapfrog_kernels;  /* device time of the leapfrog kernel sequences (a2/a3)      */
+    double ms_poly_kernels;      /* device time of the polynomial substep kernels (a6)         */
+} paraexp_stats;
+
+/* ---- leapfrog (a2, a3) ----------------------------------------------------------- */
+/* nsteps leapfrog steps (with C on e in the h-update: reading 1):
+ *   e <- e + cE.*(C^T h) - q(m);   h <- h - cH.*(C e)      m = 0..nsteps-1
+ * In/out (e, h) = (e^(0), h^(1/2)) -> (e^(n), h^(n+1/2)), device pointers, canonical
+ * layout, 3*npts elements each of the grid dtype.  Source times t0 + (m + 1/2) dt.
+ * Returns after enqueue; the non-finite check (EDIVERGED) is performed only if
+ * check_finite != 0 (then the call synchronises `stream`).
+ * Errors: EINVAL (nsteps < 0, nsrc out of range, dead/out-of-range source edge),
+ *         ENOTSUP (host-only grid), EDIVERGED, ECUDA. */
+int paraexp_leapfrog(paraexp_grid *grid, const paraexp_source *src, int32_t nsrc, double t0,
+                     int64_t nsteps, void *e, void *h, int32_t check_finite, void *stream,
+                     paraexp_stats *stats);
+
+/* ---- exp(tau A) v (a5, a6) -------------------------------------------------------- */
+/* Options:
+ *   method   PARAEXP_LEJA (Newton form on Leja points of i[-a,a], a = 1.05 h rho,
+ *            reading 14) or PARAEXP_TAYLOR (truncated Taylor)
+ *   m, s     fixed degree (1 or even, <= 100) and substep count; m = 0 => choose (m, s)
+ *            minimising m*s subject to the per-substep criterion of reading 16 at eps_A;
+ *            m > 0 with s = 0 => s from the criterion at that m
+ *   eps_A    relative backward-error tolerance in (1e-14, 1)
+ *   rho      spectral bound of A; 0 => min(rho_cfl, 1.05*rho_pow) (reading 17)
+ *   early_term  must be 0 (reserved)                                                   */
+typedef struct {
+    int32_t method;
+    int32_t m, s;
+    double eps_A;
+    double rho;
+    int32_t early_term;
+} paraexp_expmv_opts;
+
+/* Plan export (reading 25: parity is defined at a fixed plan). */
+typedef struct {
+    int32_t method, m, s, n_ops;
+    double tau, rho, a, gamma;
+    double sigma;              /* (tau/s) / (gamma dt): scale of cE, cH in X = h/gamma A  */
+    double xi[PARAEXP_MAX_DEGREE + 1];    /* Leja sequence on [-1,1] (k <= m)             */
+    double d_re[PARAEXP_MAX_DEGREE + 1];  /* d-hat_k = gamma^k exp[z_0..z_k], fp64       */
+    double d_im[PARAEXP_MAX_DEGREE + 1];
+} paraexp_plan_info;
+
+/* In place (h, e) <- exp(tau A_orig)(h, e), A_orig = [[0, -M_nu C], [M_eps^-1 C^T, 0]]
+ * (original variables; PAPER:204-215 via SURVEY finding 1), same time level.
+ * e, h: device pointers, canonical layout.  tau >= 0 seconds.
+ * Errors: EINVAL (tau < 0, bad opts), ENOTSUP, EOVERFLOW (non-finite, synchronises). */
+int paraexp_expmv(paraexp_grid *grid, double tau, const paraexp_expmv_opts *opts, void *e,
+                  void *h, void *stream, paraexp_stats *stats);
+/* Compute the plan paraexp_expmv would use (host only; no device work unless rho = 0
+ * requires the K5 estimate). */
+int paraexp_expmv_plan(paraexp_grid *grid, double tau, const paraexp_expmv_opts *opts,
+                       paraexp_plan_info *out);
+
+/* ---- communicator (a8) ------------------------------------------------------------ */
+/* NCCL is loaded at run time (dlopen "libnccl.so.2"); the library owns the ncclComm_t.
+ * The caller broadcasts the 128-byte id (e.g. with torch.distributed) and every rank
+ * calls paraexp_comm_create with the same id.  Errors: ENCCL. */
+int paraexp_comm_unique_id(uint8_t id[128]);
+int paraexp_comm_create(const uint8_t id[128], int32_t rank, int32_t world, int32_t device,
+                        paraexp_comm **out);
+void paraexp_comm_destroy(paraexp_comm *comm);
+
+/* ---- ParaExp solve (a4, a7, a8, a9; Algorithm 1) -------------------- */
+/* COLLECTIVE over `comm` (NULL => single GPU, world 1): every rank calls with identical
+ * arguments.  Time interval (t0, t0 + nsteps dt] is split into p sub-intervals of
+ * nsteps/p steps, residual steps to the last.  Sub-intervals are assigned
+ * to ranks in contiguous blocks (rank r gets an equal share, earlier ranks get the
+ * remainder); a rank computes, for each owned j, the particular solution v_j by
+ * leapfrog from zero with global source times, the seed s_j = (e_j, h_j + cH/2 C e_j)
+ * (reading 9) and accumulates its tails to T_p by Horner over the per-sub-interval
+ * propagators E_i (SURVEY finding 9):  W <- E_i W + s_i.  The rank owning sub-interval
+ * 1 also carries u0 (reading 12).  W is summed with ncclReduce onto the root = owner of
+ * sub-interval p, which reconstructs (eq:averaging1/2, reading 10):
+ *      e_out = e_p + W_e,   h_out = h_p + [exp(dt/2 A) W]_h.
+ * tail_mode PARAEXP_TAIL_LEAPFROG propagates the staggered seeds with leapfrog instead
+ * (debug identity: equals serial leapfrog).
+ *   e0, h0   same-time initial value u0 at t0 (device, canonical) or NULL => 0
+ *   e_out, h_out  device, canonical; written on the root, or on every rank when
+ *            broadcast_out != 0 (one ncclBroadcast).  Output convention equals
+ *            paraexp_leapfrog from (e0, h0 - cH/2 C e0): (e^(n), h^(n+1/2)).
+ * Errors: EINVAL (p < 1, nsteps < p), ENOTSUP, EDIVERGED / EOVERFLOW (stats.fail_interval),
+ *         ENCCL, ECUDA.  Synchronises `stream` before returning. */
+int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
+                  int32_t nsrc, double t0, int64_t nsteps, int32_t p,
+                  const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
+                  const void *e0, const void *h0, void *e_out, void *h_out, void *stream,
+                  paraexp_stats *stats);
+
+/* ---- host-only helpers (no GPU needed) -------------------------------------------- */
+/* Partition of nsteps into p sub-intervals: bounds[0..p], bounds[0] = 0, bounds[p] = nsteps
+ * (SPEC:345-353).  EINVAL if p < 1 or nsteps < p. */
+int paraexp_partition(int64_t nsteps, int32_t p, int64_t *bounds);
+/* Contiguous block [first, last] (1-based sub-interval indices) owned by `rank` of `world`
+ * for p sub-intervals; first = last + 1 = 0 if the rank owns none.  root = owner of p. */
+int paraexp_schedule(int32_t p, int32_t world, int32_t rank, int32_t *first, int32_t *last,
+                     int32_t *root);
+/* Symmetrised Leja sequence xi'_0..xi'_{count-1} on [-1,1] (reading 14). */
+int paraexp_leja_points(int32_t count, double *xi);
+/* Plan without a grid: tau and rho given, dt used only for sigma (may be 1). */
+int paraexp_plan_host(int32_t method, int32_t m, int32_t s, double eps_A, double tau,
+                      double rho, double dt, paraexp_plan_info *out);
+/* theta_m(eps_A): largest theta with max_{|x|<=theta} |p(ix) - e^{ix}| <= eps_A theta
+ * (reading 16), method TAYLOR or LEJA.  Cached. */
+double paraexp_theta(int32_t method, int32_t m, double eps_A);
+
+const char *paraexp_strerror(int code);
+const char *paraexp_last_error(void);
+/* library version string, e.g. "paraexp-b200 0.1 (sm_100a)" */
+const char *paraexp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARAEXP_H */

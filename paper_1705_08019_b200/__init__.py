@@ -1,0 +1,284 @@
+"""paraexp-b200: B200-native ParaExp + Leapfrog for FIT-discretised Maxwell equations
+(arXiv:1705.08019).  Python binding of the C ABI in include/paraexp.h.
+
+The functions below only marshal arguments (torch tensors -> device pointers, streams,
+ctypes structs); every step of the hot path runs in libparaexp.so.  Names follow the C ABI
+(``paraexp_<name>`` -> ``<name>``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+from . import abi
+from .abi import (EDIVERGED, EINVAL, ENOTSUP, EOVERFLOW, F32, F64, KERNELS_AUTO, KERNELS_FUSED,  # noqa
+                  KERNELS_UNFUSED, LEJA, TAIL_EXP, TAIL_LEAPFROG, TAYLOR, ParaexpError, check)
+
+__all__ = ["Grid", "Comm", "leapfrog", "expmv", "expmv_plan", "solve", "partition", "schedule",
+           "leja_points", "plan_host", "theta", "version", "make_sources", "ParaexpError"]
+
+_DT = {"f64": F64, "f32": F32}
+_KER = {"auto": KERNELS_AUTO, "unfused": KERNELS_UNFUSED, "fused": KERNELS_FUSED}
+_SRC_KIND = {"zero": 0, "gauss_paper": 1, "gauss_sine": 2, "sine": 3}
+_METHOD = {"taylor": TAYLOR, "leja": LEJA}
+
+
+def version() -> str:
+    return abi.lib.paraexp_version().decode()
+
+
+def _arr(a, dtype):
+    if a is None:
+        return None, None
+    x = np.ascontiguousarray(a, dtype=dtype)
+    return x, x.ctypes.data_as(C.POINTER(C.c_double if dtype == np.float64 else C.c_uint8))
+
+
+class Grid:
+    """paraexp_grid_create / _destroy / _info / _coefficients.
+
+    device=-1 builds a host-only grid (coefficients, CFL and plans; no compute)."""
+
+    def __init__(self, nx, ny, nz, d0=None, dx=None, dy=None, dz=None, eps_r=None, mu_r=None,
+                 pec_cell=None, dtype="f64", device=0, dt=None, dt_frac=None, kernels="auto"):
+        keep = []
+        d = abi.paraexp_grid_desc()
+        d.nx, d.ny, d.nz = int(nx), int(ny), int(nz)
+        for name, v in (("dx", dx), ("dy", dy), ("dz", dz), ("eps_r", eps_r), ("mu_r", mu_r)):
+            arr, ptr = _arr(v, np.float64)
+            keep.append(arr)
+            setattr(d, name, ptr)
+        arr, ptr = _arr(pec_cell, np.uint8)
+        keep.append(arr)
+        d.pec_cell = ptr
+        d.d0 = float(d0 or 0.0)
+        d.dtype = _DT[dtype]
+        d.device = int(device)
+        d.dt = float(dt or 0.0)
+        d.dt_frac = float(dt_frac or 0.0)
+        d.kernels = _KER[kernels]
+        h = C.c_void_p()
+        rc = abi.lib.paraexp_grid_create(C.byref(d), C.byref(h))
+        check(rc, "paraexp_grid_create")
+        self.warnings = rc
+        self._h = h
+        self.dtype = dtype
+        self.device = int(device)
+        self.nx, self.ny, self.nz = d.nx, d.ny, d.nz
+        self.npts = (self.nx + 1) * (self.ny + 1) * (self.nz + 1)
+        inf = self.info()
+        self.dt, self.dt_cfl, self.rho_cfl = inf["dt"], inf["dt_cfl"], inf["rho_cfl"]
+
+    @classmethod
+    def from_workload(cls, w, device=0, dtype=None, kernels="auto"):
+        return cls(w.nx, w.ny, w.nz, d0=w.d0, eps_r=w.eps_r, pec_cell=w.pec_cell,
+                   dtype=dtype or w.dtype, device=device, dt_frac=w.dt_frac, kernels=kernels)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self, compute_rho_pow=False, stream=None):
+        o = abi.paraexp_grid_info_t()
+        check(abi.lib.paraexp_grid_info(self._h, int(bool(compute_rho_pow)), _stream(stream, self),
+                                        C.byref(o)), "paraexp_grid_info")
+        return {f[0]: getattr(o, f[0]) for f in o._fields_}
+
+    def coefficients(self):
+        cE = np.empty(3 * self.npts)
+        cH = np.empty(3 * self.npts)
+        check(abi.lib.paraexp_grid_coefficients(self._h, cE.ctypes.data_as(abi._dp),
+                                                cH.ctypes.data_as(abi._dp)),
+              "paraexp_grid_coefficients")
+        return cE, cH
+
+    def torch_dtype(self):
+        import torch
+        return torch.float64 if self.dtype == "f64" else torch.float32
+
+    def close(self):
+        if getattr(self, "_h", None):
+            abi.lib.paraexp_grid_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _stream(stream, grid):
+    if stream is not None:
+        return C.c_void_p(int(stream))
+    if grid is None or grid.device < 0:
+        return C.c_void_p(0)
+    import torch
+    return C.c_void_p(torch.cuda.current_stream(grid.device).cuda_stream)
+
+
+def _field(t, grid, name, writable=True):
+    """Validate a canonical-layout field tensor and return its device pointer."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor")
+    if t.device.type != "cuda" or t.device.index != grid.device:
+        raise ValueError(f"{name} must live on cuda:{grid.device}")
+    if t.dtype != grid.torch_dtype() or not t.is_contiguous() or t.numel() != 3 * grid.npts:
+        raise ValueError(f"{name} must be a contiguous {grid.torch_dtype()} tensor of 3*npts elements")
+    return C.c_void_p(t.data_ptr())
+
+
+def make_sources(sources: Optional[Iterable]) -> tuple:
+    """Sources as any objects with comp, i, j, k, kind, weight, amp, t_param, f0, t_delay."""
+    srcs = list(sources or [])
+    arr = (abi.paraexp_source * max(1, len(srcs)))()
+    for q, s in enumerate(srcs):
+        a = arr[q]
+        a.comp, a.i, a.j, a.k = int(s.comp), int(s.i), int(s.j), int(s.k)
+        a.kind = _SRC_KIND[s.kind] if isinstance(s.kind, str) else int(s.kind)
+        a.weight = float(getattr(s, "weight", 1.0))
+        a.amp = float(s.amp)
+        a.t_param = float(s.t_param)
+        a.f0 = float(s.f0)
+        a.t_delay = float(s.t_delay)
+    return arr, len(srcs)
+
+
+def _opts(method="leja", m=0, s=0, eps_A=1e-12, rho=0.0):
+    o = abi.paraexp_expmv_opts()
+    o.method = _METHOD[method] if isinstance(method, str) else int(method)
+    o.m, o.s, o.eps_A, o.rho, o.early_term = int(m), int(s), float(eps_A), float(rho or 0.0), 0
+    return o
+
+
+def leapfrog(grid: Grid, e, h, nsteps: int, sources=None, t0: float = 0.0,
+             check_finite: bool = False, stream=None) -> dict:
+    """paraexp_leapfrog: (e^(0), h^(1/2)) -> (e^(n), h^(n+1/2)) in place on the tensors."""
+    arr, n = make_sources(sources)
+    st = abi.paraexp_stats()
+    check(abi.lib.paraexp_leapfrog(grid.handle, arr, n, float(t0), int(nsteps), _field(e, grid, "e"),
+                                   _field(h, grid, "h"), int(bool(check_finite)),
+                                   _stream(stream, grid), C.byref(st)), "paraexp_leapfrog")
+    return st.as_dict()
+
+
+def expmv(grid: Grid, tau: float, e, h, method="leja", m=0, s=0, eps_A=1e-12, rho=0.0,
+          stream=None) -> dict:
+    """paraexp_expmv: (h, e) <- exp(tau A_orig)(h, e) in place."""
+    o = _opts(method, m, s, eps_A, rho)
+    st = abi.paraexp_stats()
+    check(abi.lib.paraexp_expmv(grid.handle, float(tau), C.byref(o), _field(e, grid, "e"),
+                                _field(h, grid, "h"), _stream(stream, grid), C.byref(st)),
+          "paraexp_expmv")
+    return st.as_dict()
+
+
+def _plan_dict(p):
+    m = p.m
+    return {"method": "leja" if p.method == LEJA else "taylor", "m": m, "s": p.s, "tau": p.tau,
+            "rho": p.rho, "a": p.a, "gamma": p.gamma, "sigma": p.sigma, "n_ops": p.n_ops,
+            "xi": list(p.xi[:m + 1]), "d": [complex(p.d_re[k], p.d_im[k]) for k in range(m + 1)]}
+
+
+def expmv_plan(grid: Grid, tau: float, method="leja", m=0, s=0, eps_A=1e-12, rho=0.0) -> dict:
+    o = _opts(method, m, s, eps_A, rho)
+    p = abi.paraexp_plan_info()
+    check(abi.lib.paraexp_expmv_plan(grid.handle, float(tau), C.byref(o), C.byref(p)),
+          "paraexp_expmv_plan")
+    return _plan_dict(p)
+
+
+def plan_host(method, m, s, eps_A, tau, rho, dt=1.0) -> dict:
+    p = abi.paraexp_plan_info()
+    check(abi.lib.paraexp_plan_host(_METHOD[method], int(m), int(s), float(eps_A), float(tau),
+                                    float(rho), float(dt), C.byref(p)), "paraexp_plan_host")
+    return _plan_dict(p)
+
+
+def theta(method, m, eps_A) -> float:
+    return abi.lib.paraexp_theta(_METHOD[method], int(m), float(eps_A))
+
+
+def leja_points(count: int) -> list:
+    out = (C.c_double * count)()
+    check(abi.lib.paraexp_leja_points(int(count), out), "paraexp_leja_points")
+    return list(out)
+
+
+def partition(nsteps: int, p: int) -> list:
+    out = (C.c_int64 * (p + 1))()
+    check(abi.lib.paraexp_partition(int(nsteps), int(p), out), "paraexp_partition")
+    return list(out)
+
+
+def schedule(p: int, world: int, rank: int) -> tuple:
+    f, l, r = C.c_int32(), C.c_int32(), C.c_int32()
+    check(abi.lib.paraexp_schedule(int(p), int(world), int(rank), C.byref(f), C.byref(l),
+                                   C.byref(r)), "paraexp_schedule")
+    return f.value, l.value, r.value
+
+
+class Comm:
+    """paraexp_comm_*: the library's own NCCL communicator.  The 128-byte id is created on
+    rank 0 and broadcast with torch.distributed (plumbing only)."""
+
+    def __init__(self, rank: int, world: int, device: int, id_bytes: Optional[bytes] = None):
+        if id_bytes is None:
+            id_bytes = Comm.unique_id_via_torch(rank)
+        buf = (C.c_uint8 * 128).from_buffer_copy(id_bytes)
+        h = C.c_void_p()
+        check(abi.lib.paraexp_comm_create(buf, int(rank), int(world), int(device), C.byref(h)),
+              "paraexp_comm_create")
+        self._h = h
+        self.rank, self.world, self.device = rank, world, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(abi.lib.paraexp_comm_unique_id(buf), "paraexp_comm_unique_id")
+        return bytes(buf)
+
+    @staticmethod
+    def unique_id_via_torch(rank: int) -> bytes:
+        import torch
+        import torch.distributed as dist
+        t = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            t = torch.tensor(list(Comm.unique_id()), dtype=torch.uint8)
+        if dist.get_backend() == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, 0)
+        return bytes(t.cpu().tolist())
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            abi.lib.paraexp_comm_destroy(self._h)
+            self._h = None
+
+
+def solve(grid: Grid, nsteps: int, p: int, sources=None, t0: float = 0.0, method="leja", m=0,
+          s=0, eps_A=1e-12, rho=0.0, tail_mode=TAIL_EXP, u0=None, e_out=None, h_out=None,
+          comm: Optional[Comm] = None, broadcast_out=False, stream=None) -> dict:
+    """paraexp_solve (Algorithm 1): returns the stats dict; output in e_out/h_out."""
+    arr, n = make_sources(sources)
+    o = _opts(method, m, s, eps_A, rho)
+    st = abi.paraexp_stats()
+    e0 = h0 = C.c_void_p(0)
+    if u0 is not None:
+        e0 = _field(u0[0], grid, "e0")
+        h0 = _field(u0[1], grid, "h0")
+    eo = _field(e_out, grid, "e_out") if e_out is not None else C.c_void_p(0)
+    ho = _field(h_out, grid, "h_out") if h_out is not None else C.c_void_p(0)
+    tm = tail_mode if isinstance(tail_mode, int) else {"exp": TAIL_EXP, "leapfrog": TAIL_LEAPFROG}[tail_mode]
+    check(abi.lib.paraexp_solve(grid.handle, comm.handle if comm else C.c_void_p(0), arr, n,
+                                float(t0), int(nsteps), int(p), C.byref(o), tm,
+                                int(bool(broadcast_out)), e0, h0, eo, ho, _stream(stream, grid),
+                                C.byref(st)), "paraexp_solve")
+    return st.as_dict()

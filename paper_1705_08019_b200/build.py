@@ -1,0 +1,57 @@
+"""Build the in-tree C-ABI library libparaexp.so for sm_100a (nvcc cross-compiles without
+a GPU).  Usage: python -m paper_1705_08019_b200.build [--force] [--verbose]"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build")
+LIB = os.path.join(HERE, "libparaexp.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CUFLAGS = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2",
+                  "--expt-relaxed-constexpr", "-Xptxas", "-v" if os.environ.get("PARAEXP_PTXAS_V") else "-O3",
+                  "-I" + os.path.join(HERE, "..", "include")]
+CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-I/usr/local/cuda/include",
+            "-I" + os.path.join(HERE, "..", "include")]
+SOURCES = ["kernels.cu", "fused.cu", "grid.cpp", "plan.cpp", "api.cpp"]
+HEADERS = ["internal.h", "kernels_common.cuh", "../../include/paraexp.h"]
+
+
+def _newer(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS]
+    objs = []
+    for src in SOURCES:
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(OBJ, src + ".o")
+        objs.append(obj)
+        if not force and not _newer(obj, [path] + hdrs):
+            continue
+        if src.endswith(".cu"):
+            cmd = [NVCC] + CUFLAGS + ["-c", path, "-o", obj]
+        else:
+            cmd = ["g++"] + CXXFLAGS + ["-c", path, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    if force or _newer(LIB, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-ldl", "-lpthread"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

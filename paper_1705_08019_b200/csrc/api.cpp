@@ -1,0 +1,719 @@
+// api.cpp -- C ABI entry points: leapfrog (a2/a3), expmv (a5/a6), ParaExp solve (a4, a7-a9),
+// K5 norm estimate, communicator (a8), host helpers and error handling.
+// See include/paraexp.h for the contract of every function.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace pe {
+
+// ---- errors ------------------------------------------------------------------------------
+static thread_local std::string t_last_error;
+void set_error(const std::string &msg) { t_last_error = msg; }
+int fail(int code, const std::string &msg) {
+    set_error(msg);
+    return code;
+}
+
+// ---- workspace ---------------------------------------------------------------------------
+static int ensure_ws(Grid &G, int n) {
+    const size_t bytes = (size_t)G.L.state_elems() * G.esize();
+    while ((int)G.ws.size() < n) {
+        void *p = nullptr;
+        int rc = dev_alloc(&p, bytes);
+        if (rc) return rc;
+        G.ws.push_back(p);
+        G.device_bytes += bytes;
+        G.ws_bytes += bytes;
+    }
+    return PARAEXP_OK;
+}
+
+// ---- sources (reading 6, 24) ---------------------------------------------------------------
+static double waveform(const paraexp_source &s, double t) {
+    switch (s.kind) {
+        case PARAEXP_SRC_ZERO: return 0.0;
+        case PARAEXP_SRC_GAUSS_PAPER: {
+            const double x = (t - s.t_param) / s.t_param;
+            return s.amp * std::exp(-4.0 * x * x);
+        }
+        case PARAEXP_SRC_GAUSS_SINE: {
+            const double x = t - s.t_delay;
+            const double r = x / s.t_param;
+            return s.amp * std::sin(2.0 * M_PI * s.f0 * x) * std::exp(-(r * r));
+        }
+        case PARAEXP_SRC_SINE: return s.amp * std::sin(2.0 * M_PI * s.f0 * t);
+    }
+    return 0.0;
+}
+
+// validate sources and upload descriptors + the amplitude table q[m][s] for global steps
+// m0 .. m0+nsteps-1:  q = fl_T(cE64_s * weight_s * i_s(t0 + (m + 1/2) dt)).
+static int prepare_sources(Grid &G, const paraexp_source *src, int nsrc, double t0, int64_t m0,
+                           int64_t nsteps, void *stream, std::vector<SrcDev> &sd) {
+    if (nsrc < 0 || nsrc > PARAEXP_MAX_SOURCES) return fail(PARAEXP_EINVAL, "nsrc out of range");
+    if (nsrc > 0 && !src) return fail(PARAEXP_EINVAL, "null sources");
+    sd.resize(nsrc);
+    std::vector<double> ce(nsrc);
+    const int64_t NX = G.nx + 1, NY = G.ny + 1;
+    for (int s = 0; s < nsrc; ++s) {
+        const paraexp_source &S = src[s];
+        if (S.comp < 0 || S.comp > 2 || S.i < 0 || S.j < 0 || S.k < 0 || S.i > G.nx || S.j > G.ny || S.k > G.nz)
+            return fail(PARAEXP_EINVAL, "source edge out of range");
+        if (S.kind < 0 || S.kind > 3) return fail(PARAEXP_EINVAL, "bad source kind");
+        if ((S.kind == PARAEXP_SRC_GAUSS_PAPER || S.kind == PARAEXP_SRC_GAUSS_SINE) && !(S.t_param > 0))
+            return fail(PARAEXP_EINVAL, "source t_param must be > 0");
+        const double c = G.cE64[S.comp * G.npts + S.i + NX * (S.j + NY * (int64_t)S.k)];
+        if (c == 0.0) return fail(PARAEXP_EINVAL, "source on a dead (PEC/virtual) edge");
+        ce[s] = c;
+        sd[s].comp = S.comp;
+        sd[s].i = S.i;
+        sd[s].j = S.j;
+        sd[s].k = S.k;
+        sd[s].off = S.comp * G.L.cs + S.i + G.L.px * (S.j + (int64_t)G.ny * S.k);
+    }
+    if (nsrc == 0 || nsteps <= 0) return PARAEXP_OK;
+    const size_t es = G.esize();
+    const int64_t n = nsteps * nsrc;
+    std::vector<char> host(n * es);
+    for (int64_t m = 0; m < nsteps; ++m)
+        for (int s = 0; s < nsrc; ++s) {
+            const double t = t0 + ((double)(m0 + m) + 0.5) * G.dt;
+            const double q = ce[s] * (src[s].weight * waveform(src[s], t));
+            if (G.dtype == PARAEXP_F64)
+                reinterpret_cast<double *>(host.data())[m * nsrc + s] = q;
+            else
+                reinterpret_cast<float *>(host.data())[m * nsrc + s] = (float)q;
+        }
+    if ((int64_t)(n * es) > G.d_q_cap) {
+        dev_free(G.d_q);
+        G.d_q = nullptr;
+        int rc = dev_alloc(&G.d_q, n * es);
+        if (rc) return rc;
+        G.device_bytes += n * es - G.d_q_cap;
+        G.d_q_cap = n * es;
+    }
+    int rc = dev_memcpy_h2d_async(G.d_q, host.data(), n * es, stream);
+    if (rc) return rc;
+    rc = dev_memcpy_h2d_async(G.d_src, sd.data(), sizeof(SrcDev) * nsrc, stream);
+    if (rc) return rc;
+    return dev_sync(stream);   // host staging buffers go out of scope
+}
+
+// ---- K5: Lanczos estimate of ||A||_2 -----------------------------------------------------
+// Lanczos on B = -(dt A_orig)^2, self-adjoint and PSD in the energy inner product
+// <x,y>_M (A = T A_orig T^-1 normal with imaginary spectrum), 60 steps
+// without reorthogonalisation; rho_pow = sqrt(largest Ritz value) / dt.
+static double tridiag_max_eig(const std::vector<double> &a, const std::vector<double> &b) {
+    const int n = (int)a.size();
+    double lo = 1e300, hi = -1e300;
+    for (int i = 0; i < n; ++i) {
+        const double r = (i > 0 ? std::fabs(b[i - 1]) : 0) + (i + 1 < n ? std::fabs(b[i]) : 0);
+        lo = std::min(lo, a[i] - r);
+        hi = std::max(hi, a[i] + r);
+    }
+    auto count_below = [&](double x) {   // Sturm count of eigenvalues < x
+        int c = 0;
+        double d = 1;
+        for (int i = 0; i < n; ++i) {
+            d = a[i] - x - (i > 0 ? b[i - 1] * b[i - 1] / d : 0);
+            if (d == 0) d = 1e-300;
+            if (d < 0) ++c;
+        }
+        return c;
+    };
+    for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (count_below(mid) >= n) hi = mid; else lo = mid;
+    }
+    return hi;
+}
+
+static int compute_rho_pow(Grid &G, void *stream, int64_t *launches) {
+    int rc = ensure_ws(G, 4);
+    if (rc) return rc;
+    KernelArgs ka{&G, stream, launches};
+    void *q = G.ws[0], *qp = G.ws[1], *t = G.ws[2], *w = G.ws[3];
+    if ((rc = k_fill_random(ka, q, 0x5eed1234ull))) return rc;
+    if ((rc = dev_memset_async(qp, 0, G.L.state_elems() * G.esize(), stream))) return rc;
+    double nn;
+    if ((rc = k_dot_M(ka, q, q, &nn))) return rc;
+    if (!(nn > 0)) {
+        G.rho_pow = 0;
+        return PARAEXP_OK;
+    }
+    if ((rc = k_lincomb(ka, q, q, q, 1.0 / std::sqrt(nn), 0.0, 0.0))) return rc;
+    std::vector<double> al, be;
+    double beta_prev = 0;
+    const int K = 60;
+    for (int it = 0; it < K; ++it) {
+        if ((rc = k_apply_A(ka, q, t, 1.0))) return rc;   // t = dt A q
+        if ((rc = k_apply_A(ka, t, w, 1.0))) return rc;   // w = (dt A)^2 q
+        double alpha;
+        if ((rc = k_dot_M(ka, q, w, &alpha))) return rc;
+        alpha = -alpha;                                  // <q, B q>, B = -(dt A)^2
+        // w <- -w - alpha q - beta_prev qp
+        if ((rc = k_lincomb(ka, w, q, qp, -alpha, -beta_prev, -1.0))) return rc;
+        double bb;
+        if ((rc = k_dot_M(ka, w, w, &bb))) return rc;
+        al.push_back(alpha);
+        const double beta = std::sqrt(std::max(bb, 0.0));
+        if (!(beta > 1e-14 * std::fabs(alpha)) || it == K - 1) break;
+        be.push_back(beta);
+        std::swap(q, qp);                                // qp <- q
+        if ((rc = k_lincomb(ka, q, w, w, 1.0 / beta, 0.0, 0.0))) return rc;   // q <- w / beta
+        beta_prev = beta;
+    }
+    be.resize(al.size() > 0 ? al.size() - 1 : 0);
+    const double lmax = tridiag_max_eig(al, be);
+    G.rho_pow = std::sqrt(std::max(lmax, 0.0)) / G.dt;
+    return PARAEXP_OK;
+}
+
+static double default_rho(Grid &G, const paraexp_expmv_opts *o, void *stream, int64_t *launches,
+                          int *rc) {
+    *rc = PARAEXP_OK;
+    if (o && o->rho > 0) return o->rho;
+    if (G.device < 0) return G.rho_cfl;
+    if (G.rho_pow == 0) {
+        *rc = compute_rho_pow(G, stream, launches);
+        if (*rc) return 0;
+    }
+    return G.rho_pow > 0 ? std::min(G.rho_cfl, 1.05 * G.rho_pow) : G.rho_cfl;
+}
+
+// ---- dispatch fused / unfused -------------------------------------------------------------
+int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev *src_dev,
+                     int nsrc, const void *q_dev);
+int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]);
+bool fused_supported(const Grid &g);
+
+int k_leapfrog(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev *src_dev,
+               int nsrc, const void *q_dev) {
+    if (ka.g->kernels == PARAEXP_KERNELS_FUSED && fused_supported(*ka.g))
+        return k_leapfrog_fused(ka, bufs, nsteps, src_dev, nsrc, q_dev);
+    return k_leapfrog_unfused(ka, bufs[0], nsteps, src_dev, nsrc, q_dev);
+}
+int k_poly_substep(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
+    if (ka.g->kernels == PARAEXP_KERNELS_FUSED && fused_supported(*ka.g))
+        return k_poly_substep_fused(ka, plan, bufs);
+    return k_poly_substep_unfused(ka, plan, bufs);
+}
+
+struct Events {
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+    cudaStream_t s;
+    explicit Events(void *stream) : s((cudaStream_t)stream) {}
+    int open(int phase) {
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+        ev.push_back({phase, {a, b}});
+        return (int)ev.size() - 1;
+    }
+    void close(int id) { cudaEventRecord(ev[id].second.second, s); }
+    void sum(double out[7]) {
+        for (auto &e : ev) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e.second.first, e.second.second);
+            out[e.first] += ms;
+        }
+    }
+    ~Events() {
+        for (auto &e : ev) {
+            cudaEventDestroy(e.second.first);
+            cudaEventDestroy(e.second.second);
+        }
+    }
+};
+
+// apply the propagator p(X)^s in place: bufs[0] in/out.  Kernel time is attributed to
+// phase 6 (ms_poly_kernels) when an Events recorder is given.
+static int run_plan(const KernelArgs &ka, const Plan &plan, void *bufs[4], paraexp_stats *st,
+                    Events *ev = nullptr) {
+    const int id = ev && plan.s > 0 ? ev->open(6) : -1;
+    for (int q = 0; q < plan.s; ++q) {
+        int rc = k_poly_substep(ka, plan, bufs);
+        if (rc) return rc;
+    }
+    if (id >= 0) ev->close(id);
+    if (st) {
+        st->a_applications += (int64_t)plan.s * plan.m;
+        st->substeps += plan.s;
+    }
+    return PARAEXP_OK;
+}
+
+static int opts_plan(Grid &G, double tau, const paraexp_expmv_opts *o, double rho, Plan &plan) {
+    paraexp_expmv_opts def{PARAEXP_LEJA, 0, 0, 1e-12, 0.0, 0};
+    if (!o) o = &def;
+    if (o->early_term) return fail(PARAEXP_EINVAL, "early_term is reserved (must be 0)");
+    return make_plan(o->method, o->m, o->s, o->eps_A, tau, rho, G.dt, plan);
+}
+
+}  // namespace pe
+
+// =====================================================================================
+// NCCL (a8), loaded at run time
+// =====================================================================================
+namespace {
+typedef struct ncclComm *ncclComm_t;
+typedef struct {
+    char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Reduce)(const void *, void *, size_t, int, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+const int kNcclSum = 0, kNcclF32 = 7, kNcclF64 = 8;
+
+int load_nccl() {
+    if (g_nccl.ok) return PARAEXP_OK;
+    void *h = nullptr;
+    const char *env = getenv("PARAEXP_NCCL_LIBRARY");
+    if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return pe::fail(PARAEXP_ENCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
+    g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+    g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.Reduce = (decltype(g_nccl.Reduce))dlsym(h, "ncclReduce");
+    g_nccl.Broadcast = (decltype(g_nccl.Broadcast))dlsym(h, "ncclBroadcast");
+    g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.CommDestroy || !g_nccl.Reduce ||
+        !g_nccl.Broadcast || !g_nccl.GetErrorString)
+        return pe::fail(PARAEXP_ENCCL, "libnccl.so.2 lacks required symbols");
+    g_nccl.ok = true;
+    return PARAEXP_OK;
+}
+int nccl_check(ncclResult_t r, const char *what) {
+    if (r == 0) return PARAEXP_OK;
+    return pe::fail(PARAEXP_ENCCL, std::string(what) + ": " + g_nccl.GetErrorString(r));
+}
+}  // namespace
+
+struct paraexp_comm {
+    ncclComm_t comm;
+    int rank, world, device;
+};
+
+extern "C" {
+
+const char *paraexp_version(void) { return "paraexp-b200 0.1 (sm_100a)"; }
+
+const char *paraexp_strerror(int code) {
+    switch (code) {
+        case PARAEXP_OK: return "ok";
+        case PARAEXP_EINVAL: return "invalid argument";
+        case PARAEXP_ENOMEM: return "out of memory";
+        case PARAEXP_ECUDA: return "CUDA error";
+        case PARAEXP_ENCCL: return "NCCL error";
+        case PARAEXP_EDIVERGED: return "integration diverged (non-finite field)";
+        case PARAEXP_EOVERFLOW: return "exp(tA)v overflow (non-finite result; use more substeps)";
+        case PARAEXP_ENOTSUP: return "not supported";
+        case PARAEXP_WCFL: return "warning: dt exceeds the CFL bound";
+    }
+    return "unknown status";
+}
+
+const char *paraexp_last_error(void) { return pe::t_last_error.c_str(); }
+
+int paraexp_partition(int64_t nsteps, int32_t p, int64_t *bounds) {
+    if (p < 1 || nsteps < p || !bounds) return pe::fail(PARAEXP_EINVAL, "need p >= 1 and nsteps >= p");
+    const int64_t M = nsteps / p;
+    for (int j = 0; j < p; ++j) bounds[j] = j * M;
+    bounds[p] = nsteps;
+    return PARAEXP_OK;
+}
+
+int paraexp_schedule(int32_t p, int32_t world, int32_t rank, int32_t *first, int32_t *last,
+                     int32_t *root) {
+    if (p < 1 || world < 1 || rank < 0 || rank >= world) return pe::fail(PARAEXP_EINVAL, "bad schedule arguments");
+    // contiguous blocks; ranks with longer tails (earlier blocks) get the smaller share
+    const int active = std::min(p, world);
+    const int base = p / active, rem = p % active;
+    int f = 0, l = -1;
+    if (rank < active) {
+        // ranks active-rem .. active-1 get base+1
+        int start = 1;
+        for (int r = 0; r < rank; ++r) start += base + (r >= active - rem ? 1 : 0);
+        f = start;
+        l = start + base + (rank >= active - rem ? 1 : 0) - 1;
+    }
+    if (first) *first = f;
+    if (last) *last = l;
+    if (root) *root = active - 1;
+    return PARAEXP_OK;
+}
+
+int paraexp_grid_info(paraexp_grid *grid, int32_t compute_rho_pow, void *stream,
+                      paraexp_grid_info_t *o) {
+    if (!grid || !o) return pe::fail(PARAEXP_EINVAL, "null argument");
+    pe::Grid &G = grid->g;
+    if (compute_rho_pow && G.device >= 0 && G.rho_pow == 0) {
+        int64_t launches = 0;
+        pe::dev_set_device(G.device);
+        int rc = pe::compute_rho_pow(G, stream, &launches);
+        if (rc) return rc;
+    }
+    *o = paraexp_grid_info_t();
+    o->nx = G.nx;
+    o->ny = G.ny;
+    o->nz = G.nz;
+    o->dtype = G.dtype;
+    o->npts = G.npts;
+    o->ndof_field = 3 * G.npts;
+    o->cells = (int64_t)G.nx * G.ny * G.nz;
+    o->dt = G.dt;
+    o->dt_cfl = G.dt_cfl;
+    o->rho_cfl = G.rho_cfl;
+    o->rho_pow = G.rho_pow;
+    o->material_mode = G.mat_mode;
+    o->kernels = G.kernels;
+    o->pitch_x = G.L.px;
+    o->device_bytes = G.device_bytes;
+    o->device = G.device;
+    o->warnings = G.warnings;
+    return PARAEXP_OK;
+}
+
+int paraexp_leapfrog(paraexp_grid *grid, const paraexp_source *src, int32_t nsrc, double t0,
+                     int64_t nsteps, void *e, void *h, int32_t check_finite, void *stream,
+                     paraexp_stats *st) {
+    using namespace pe;
+    if (!grid) return fail(PARAEXP_EINVAL, "null grid");
+    Grid &G = grid->g;
+    if (G.device < 0) return fail(PARAEXP_ENOTSUP, "host-only grid");
+    if (nsteps < 0) return fail(PARAEXP_EINVAL, "nsteps < 0");
+    if (!e || !h) return fail(PARAEXP_EINVAL, "null field pointer");
+    paraexp_stats local{};
+    paraexp_stats &S = st ? *st : local;
+    S = paraexp_stats();
+    int rc = dev_set_device(G.device);
+    if (rc) return rc;
+    std::vector<SrcDev> sd;
+    if ((rc = prepare_sources(G, src, nsrc, t0, 0, nsteps, stream, sd))) return rc;
+    if ((rc = ensure_ws(G, 2))) return rc;
+    KernelArgs ka{&G, stream, &S.kernel_launches};
+    Events ev(stream);
+    const int id = ev.open(4);
+    void *bufs[2] = {G.ws[0], G.ws[1]};
+    if ((rc = k_pack(ka, e, h, bufs[0]))) return rc;
+    const int id5 = ev.open(5);
+    if ((rc = k_leapfrog(ka, bufs, nsteps, (const SrcDev *)G.d_src, nsrc, G.d_q))) return rc;
+    ev.close(id5);
+    if ((rc = k_unpack(ka, bufs[0], e, h))) return rc;
+    ev.close(id);
+    S.leapfrog_steps = nsteps;
+    S.curl_applications = 2 * nsteps;
+    S.cell_updates = nsteps * (int64_t)G.nx * G.ny * G.nz;
+    if (check_finite) {
+        int flag = 0;
+        if ((rc = k_check_finite(ka, bufs[0], &flag))) return rc;
+        if (flag) return fail(PARAEXP_EDIVERGED, "leapfrog produced non-finite values");
+    }
+    if (st) {
+        dev_sync(stream);
+        double ms[7] = {0, 0, 0, 0, 0, 0, 0};
+        ev.sum(ms);
+        S.ms_total = ms[4];
+        S.ms_leapfrog_kernels = ms[5];
+    }
+    return PARAEXP_OK;
+}
+
+int paraexp_expmv_plan(paraexp_grid *grid, double tau, const paraexp_expmv_opts *opts,
+                       paraexp_plan_info *out) {
+    using namespace pe;
+    if (!grid || !out) return fail(PARAEXP_EINVAL, "null argument");
+    Grid &G = grid->g;
+    int rc;
+    int64_t launches = 0;
+    if (G.device >= 0) dev_set_device(G.device);
+    const double rho = default_rho(G, opts, nullptr, &launches, &rc);
+    if (rc) return rc;
+    Plan plan;
+    if ((rc = opts_plan(G, tau, opts, rho, plan))) return rc;
+    plan_to_info(plan, out);
+    return PARAEXP_OK;
+}
+
+int paraexp_expmv(paraexp_grid *grid, double tau, const paraexp_expmv_opts *opts, void *e,
+                  void *h, void *stream, paraexp_stats *st) {
+    using namespace pe;
+    if (!grid) return fail(PARAEXP_EINVAL, "null grid");
+    Grid &G = grid->g;
+    if (G.device < 0) return fail(PARAEXP_ENOTSUP, "host-only grid");
+    if (!e || !h) return fail(PARAEXP_EINVAL, "null field pointer");
+    if (!(tau >= 0) || !std::isfinite(tau)) return fail(PARAEXP_EINVAL, "tau must be >= 0");
+    paraexp_stats local{};
+    paraexp_stats &S = st ? *st : local;
+    S = paraexp_stats();
+    int rc = dev_set_device(G.device);
+    if (rc) return rc;
+    const double rho = default_rho(G, opts, stream, &S.kernel_launches, &rc);
+    if (rc) return rc;
+    Plan plan;
+    if ((rc = opts_plan(G, tau, opts, rho, plan))) return rc;
+    if ((rc = ensure_ws(G, 4))) return rc;
+    KernelArgs ka{&G, stream, &S.kernel_launches};
+    Events ev(stream);
+    const int id = ev.open(4);
+    void *bufs[4] = {G.ws[0], G.ws[1], G.ws[2], G.ws[3]};
+    if ((rc = k_pack(ka, e, h, bufs[0]))) return rc;
+    if ((rc = run_plan(ka, plan, bufs, &S, &ev))) return rc;
+    if ((rc = k_unpack(ka, bufs[0], e, h))) return rc;
+    ev.close(id);
+    S.rho = rho;
+    S.method = plan.method;
+    S.m = plan.m;
+    S.s_first = S.s_last = plan.s;
+    S.curl_applications = 2 * S.a_applications;
+    S.cell_updates = S.a_applications * (int64_t)G.nx * G.ny * G.nz;
+    int flag = 0;
+    if ((rc = k_check_finite(ka, bufs[0], &flag))) return rc;
+    if (flag) return fail(PARAEXP_EOVERFLOW, "exp(tA)v produced non-finite values (use larger s)");
+    double ms[7] = {0, 0, 0, 0, 0, 0, 0};
+    ev.sum(ms);
+    S.ms_total = ms[4];
+    S.ms_poly_kernels = ms[6];
+    return PARAEXP_OK;
+}
+
+int paraexp_comm_unique_id(uint8_t id[128]) {
+    int rc = load_nccl();
+    if (rc) return rc;
+    ncclUniqueId u;
+    if ((rc = nccl_check(g_nccl.GetUniqueId(&u), "ncclGetUniqueId"))) return rc;
+    std::memcpy(id, u.internal, 128);
+    return PARAEXP_OK;
+}
+
+int paraexp_comm_create(const uint8_t id[128], int32_t rank, int32_t world, int32_t device,
+                        paraexp_comm **out) {
+    if (!id || !out || world < 1 || rank < 0 || rank >= world) return pe::fail(PARAEXP_EINVAL, "bad comm arguments");
+    int rc = load_nccl();
+    if (rc) return rc;
+    if ((rc = pe::dev_set_device(device))) return rc;
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, 128);
+    ncclComm_t c;
+    if ((rc = nccl_check(g_nccl.CommInitRank(&c, world, u, rank), "ncclCommInitRank"))) return rc;
+    *out = new paraexp_comm{c, rank, world, device};
+    return PARAEXP_OK;
+}
+
+void paraexp_comm_destroy(paraexp_comm *comm) {
+    if (!comm) return;
+    if (g_nccl.ok) g_nccl.CommDestroy(comm->comm);
+    delete comm;
+}
+
+int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
+                  int32_t nsrc, double t0, int64_t nsteps, int32_t p,
+                  const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
+                  const void *e0, const void *h0, void *e_out, void *h_out, void *stream,
+                  paraexp_stats *st) {
+    using namespace pe;
+    if (!grid) return fail(PARAEXP_EINVAL, "null grid");
+    Grid &G = grid->g;
+    if (G.device < 0) return fail(PARAEXP_ENOTSUP, "host-only grid");
+    if (p < 1 || nsteps < p) return fail(PARAEXP_EINVAL, "need p >= 1 and nsteps >= p");
+    if (p > 1000) return fail(PARAEXP_EINVAL, "p > 1000 not supported");
+    if (tail_mode != PARAEXP_TAIL_EXP && tail_mode != PARAEXP_TAIL_LEAPFROG) return fail(PARAEXP_EINVAL, "bad tail mode");
+    if ((e0 == nullptr) != (h0 == nullptr)) return fail(PARAEXP_EINVAL, "e0 and h0 must both be given or both NULL");
+    const int rank = comm ? comm->rank : 0, world = comm ? comm->world : 1;
+    paraexp_stats local{};
+    paraexp_stats &S = st ? *st : local;
+    S = paraexp_stats();
+    int rc = dev_set_device(G.device);
+    if (rc) return rc;
+    std::vector<int64_t> B(p + 1);
+    paraexp_partition(nsteps, p, B.data());
+    int first, last, root;
+    paraexp_schedule(p, world, rank, &first, &last, &root);
+    S.first_interval = first;
+    S.last_interval = last;
+    S.root = root;
+    const bool has_u0 = e0 != nullptr;
+
+    const double rho = default_rho(G, opts, stream, &S.kernel_launches, &rc);
+    if (rc) return rc;
+    S.rho = rho;
+    // one plan per distinct sub-interval length, plus the dt/2 shift plan
+    std::map<int64_t, Plan> plans;
+    for (int i = 1; i <= p; ++i) {
+        const int64_t M = B[i] - B[i - 1];
+        if (!plans.count(M)) {
+            Plan pl;
+            if ((rc = opts_plan(G, M * G.dt, opts, rho, pl))) return rc;
+            plans[M] = pl;
+        }
+    }
+    Plan half;
+    {
+        const double theta = rho * G.dt * 0.5;
+        const int sh = std::max(1, (int)std::ceil(theta));
+        if ((rc = make_plan(PARAEXP_TAYLOR, 24, sh, 0.0, 0.5 * G.dt, rho, G.dt, half))) return rc;
+    }
+    const Plan &P1 = plans[B[1] - B[0]];
+    const Plan &Pp = plans[B[p] - B[p - 1]];
+    S.method = P1.method;
+    S.m = P1.m;
+    S.s_first = P1.s;
+    S.s_last = Pp.s;
+    S.m_half = half.m;
+    S.s_half = half.s;
+
+    std::vector<SrcDev> sd;
+    if ((rc = prepare_sources(G, src, nsrc, t0, 0, nsteps, stream, sd))) return rc;
+    if ((rc = ensure_ws(G, 5))) return rc;
+    KernelArgs ka{&G, stream, &S.kernel_launches};
+    const size_t sbytes = (size_t)G.L.state_elems() * G.esize();
+    const int64_t cells = (int64_t)G.nx * G.ny * G.nz;
+    Events ev(stream);
+    const int idt = ev.open(4);
+
+    void *P = G.ws[0];          // particular state of the current sub-interval
+    void *W = G.ws[1];          // Horner accumulator of the tails
+    void *X[3] = {G.ws[2], G.ws[3], G.ws[4]};
+    bool W_valid = false;
+    int *dflag = (int *)G.d_flag;
+    if ((rc = dev_memset_async(dflag, 0, sizeof(int) * (p + 2), stream))) return rc;
+
+    auto propagate = [&](int i) -> int {   // W <- E_i W
+        const int64_t M = B[i] - B[i - 1];
+        if (tail_mode == PARAEXP_TAIL_EXP) {
+            void *bufs[4] = {W, X[0], X[1], X[2]};
+            int r = run_plan(ka, plans[M], bufs, &S, &ev);
+            W = bufs[0];
+            X[0] = bufs[1];
+            X[1] = bufs[2];
+            X[2] = bufs[3];
+            return r;
+        }
+        void *bufs[2] = {W, X[0]};
+        const int id5 = ev.open(5);
+        int r = k_leapfrog(ka, bufs, M, nullptr, 0, nullptr);
+        ev.close(id5);
+        if (bufs[0] != W) std::swap(W, X[0]);
+        S.leapfrog_steps += M;
+        S.curl_applications += 2 * M;
+        return r;
+    };
+
+    if (first >= 1) {
+        if (first == 1 && has_u0) {
+            if ((rc = k_pack(ka, e0, h0, W))) return rc;
+            if (tail_mode == PARAEXP_TAIL_LEAPFROG && (rc = k_half_start(ka, W))) return rc;
+            W_valid = true;
+        }
+        for (int i = first; i <= last; ++i) {
+            const int64_t M = B[i] - B[i - 1];
+            int id = ev.open(0);
+            if ((rc = dev_memset_async(P, 0, sbytes, stream))) return rc;
+            void *bufs[2] = {P, X[0]};
+            const size_t qoff = (size_t)B[i - 1] * nsrc * G.esize();
+            const int id5 = ev.open(5);
+            if ((rc = k_leapfrog(ka, bufs, M, (const SrcDev *)G.d_src, nsrc, (const char *)G.d_q + qoff))) return rc;
+            ev.close(id5);
+            if (bufs[0] != P) std::swap(P, X[0]);
+            S.leapfrog_steps += M;
+            S.curl_applications += 2 * M;
+            if ((rc = k_check_finite_async(ka, P, dflag + i))) return rc;
+            ev.close(id);
+            id = ev.open(1);
+            if (W_valid && (rc = propagate(i))) return rc;
+            if (i < p) {
+                if (tail_mode == PARAEXP_TAIL_EXP && (rc = k_sync(ka, P))) return rc;
+                if (W_valid) {
+                    if ((rc = k_axpy(ka, W, P, 1.0))) return rc;
+                } else {
+                    if ((rc = dev_memcpy_d2d_async(W, P, sbytes, stream))) return rc;
+                    W_valid = true;
+                }
+            }
+            ev.close(id);
+        }
+        const int id = ev.open(1);
+        for (int i = last + 1; i <= p; ++i)
+            if (W_valid && (rc = propagate(i))) return rc;
+        ev.close(id);
+    }
+    if (!W_valid && (rc = dev_memset_async(W, 0, sbytes, stream))) return rc;
+    if ((rc = k_check_finite_async(ka, W, dflag + p + 1))) return rc;
+
+    // a8: sum the tails onto the root
+    if (world > 1) {
+        const int id = ev.open(2);
+        const int dt = G.dtype == PARAEXP_F64 ? kNcclF64 : kNcclF32;
+        if ((rc = nccl_check(g_nccl.Reduce(W, W, (size_t)G.L.state_elems(), dt, kNcclSum, root,
+                                          comm->comm, (cudaStream_t)stream), "ncclReduce"))) return rc;
+        ev.close(id);
+    }
+    // a9: reconstruction on the root (eq:averaging1/2, reading 10)
+    const int idf = ev.open(3);
+    if (rank == root) {
+        if (tail_mode == PARAEXP_TAIL_EXP) {
+            if ((rc = k_axpy_comps(ka, P, W, 1.0, 0, 3))) return rc;       // e_out = e_p + W_e
+            void *bufs[4] = {W, X[0], X[1], X[2]};
+            if ((rc = run_plan(ka, half, bufs, nullptr))) return rc;       // exp(dt/2 A) W
+            S.a_applications += (int64_t)half.s * half.m;
+            if ((rc = k_axpy_comps(ka, P, bufs[0], 1.0, 3, 6))) return rc;  // h_out = h_p + [.]_h
+        } else {
+            if ((rc = k_axpy(ka, P, W, 1.0))) return rc;
+        }
+    }
+    if (broadcast_out && world > 1) {
+        const int dt = G.dtype == PARAEXP_F64 ? kNcclF64 : kNcclF32;
+        if ((rc = nccl_check(g_nccl.Broadcast(P, P, (size_t)G.L.state_elems(), dt, root, comm->comm,
+                                             (cudaStream_t)stream), "ncclBroadcast"))) return rc;
+    }
+    if ((rank == root || broadcast_out) && e_out && h_out) {
+        if ((rc = k_unpack(ka, P, e_out, h_out))) return rc;
+    }
+    ev.close(idf);
+    ev.close(idt);
+    S.curl_applications = 2 * (S.leapfrog_steps + S.a_applications);
+    S.cell_updates = (S.leapfrog_steps + S.a_applications) * cells;
+    std::vector<int> flags(p + 2, 0);
+    if ((rc = dev_memcpy_d2h(flags.data(), dflag, sizeof(int) * (p + 2), stream))) return rc;
+    double ms[7] = {0, 0, 0, 0, 0, 0, 0};
+    ev.sum(ms);
+    S.ms_particular = ms[0];
+    S.ms_tails = ms[1];
+    S.ms_reduce = ms[2];
+    S.ms_finish = ms[3];
+    S.ms_total = ms[4];
+    S.ms_leapfrog_kernels = ms[5];
+    S.ms_poly_kernels = ms[6];
+    for (int i = 1; i <= p; ++i)
+        if (flags[i]) {
+            S.fail_interval = i;
+            return fail(PARAEXP_EDIVERGED, "leapfrog diverged in sub-interval " + std::to_string(i));
+        }
+    if (flags[p + 1]) {
+        S.fail_interval = first;
+        return fail(PARAEXP_EOVERFLOW, "exp(tA)v tails produced non-finite values");
+    }
+    return PARAEXP_OK;
+}
+
+}  // extern "C"

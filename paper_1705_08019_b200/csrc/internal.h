@@ -1,0 +1,145 @@
+// internal.h -- shared declarations of the paraexp-b200 library (not part of the ABI).
+//
+// Device layout:
+//   Every live DOF of the canonical layout lies in i < nx, j < ny, k < nz (each component's
+//   live range per axis is [0,n) or [1,n)), so the device stores exactly one cell-indexed
+//   array per component:  idx(i,j,k) = i + px*(j + ny*k),  px = nx rounded up to 128 B.
+//   A state vector is 6 components [ex, ey, ez, hx, hy, hz], component stride `cs`.
+//   Entries with i >= nx (x padding) and every dead DOF are kept at exactly 0.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "../../include/paraexp.h"
+
+typedef struct CUstream_st *cudaStream_t_;
+
+namespace pe {
+
+struct Layout {
+    int nx, ny, nz;
+    int64_t px;     // x pitch in elements
+    int64_t plane;  // px*ny
+    int64_t cs;     // component stride = plane*nz
+    int64_t state_elems() const { return 6 * cs; }
+};
+
+struct Grid {
+    int nx, ny, nz;
+    int dtype;          // PARAEXP_F64 / F32
+    int device;         // -1 host only
+    int kernels;        // resolved PARAEXP_KERNELS_*
+    int mat_mode;       // PARAEXP_MAT_*
+    bool h_array;       // per-face cH array
+    double dt, dt_cfl, rho_cfl, rho_pow;
+    int warnings;
+    Layout L;
+    int64_t npts;
+    // host fp64 coefficients, canonical layout (3*npts each)
+    std::vector<double> cE64, cH64;
+    // compact host tables (fp64): scalar per comp, or per (comp, k)
+    double cE_scalar[3], cH_scalar[3];
+    std::vector<double> cE_ztab;   // 3*nz
+    // device buffers
+    void *d_cE_tab = nullptr;   // 3*nz of T (ztable)
+    void *d_cE_arr = nullptr;   // 3*cs of T (array)
+    void *d_cH_arr = nullptr;   // 3*cs of T (array-H)
+    // workspace (state vectors)
+    std::vector<void *> ws;     // each 6*cs elements of T
+    int64_t ws_bytes = 0;
+    void *d_flag = nullptr;     // int device flag (non-finite)
+    void *d_red = nullptr;      // double reduction scratch
+    void *d_src = nullptr;      // source descriptors
+    void *d_q = nullptr;        // source amplitude table
+    int64_t d_q_cap = 0;
+    int64_t device_bytes = 0;
+    size_t esize() const { return dtype == PARAEXP_F64 ? 8 : 4; }
+};
+
+// ---- errors ----
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+void grid_free_device(Grid &G);
+int grid_create(const paraexp_grid_desc *d, paraexp_grid **out);
+
+// ---- plan ----
+struct Op {           // one step of the real conjugate-pair schedule (DESIGN a6)
+    int kind;         // 0 pair, 1 half pair, 2 zero node (with w update), 3 zero node last
+    double a, b, e2;  // pair/half: y += a w + b u ; w = X u + e2 w.   zero: y += a w
+};
+struct Plan {
+    int method, m, s;
+    double tau, rho, a, gamma, sigma;
+    std::vector<double> xi;        // Leja sequence on [-1,1]
+    std::vector<double> node_im;   // Im of capacity-scaled nodes 2*xi (Leja), empty (Taylor)
+    std::vector<double> d_re, d_im;
+    std::vector<Op> ops;
+};
+int make_plan(int method, int m, int s, double eps_A, double tau, double rho, double dt,
+              Plan &out);
+void leja_sequence(int count, std::vector<double> &xi);
+double theta_m(int method, int m, double tol);
+void plan_to_info(const Plan &p, paraexp_plan_info *out);
+
+// ---- device entry points (kernels.cu) ----
+struct SrcDev {       // one source edge in device layout
+    int64_t off;      // element offset into the state vector (component + idx)
+    int32_t comp, i, j, k;
+};
+int dev_alloc(void **p, size_t bytes);
+void dev_free(void *p);
+int dev_memset_async(void *p, int v, size_t bytes, void *stream);
+int dev_memcpy_h2d_async(void *dst, const void *src, size_t bytes, void *stream);
+int dev_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream);
+int dev_memcpy_d2d_async(void *dst, const void *src, size_t bytes, void *stream);
+int dev_set_device(int device);
+int dev_sync(void *stream);
+int check_cuda(const char *what);
+
+struct KernelArgs {
+    const Grid *g;
+    void *stream;
+    int64_t *launches;
+};
+
+// pack canonical (e, h) -> device state (zeroing dead DOFs); unpack the reverse.
+int k_pack(const KernelArgs &ka, const void *e, const void *h, void *state);
+int k_unpack(const KernelArgs &ka, const void *state, void *e, void *h);
+// leapfrog: `nsteps` steps; bufs[0] = state in/out, bufs[1] = spare (fused kernels
+// ping-pong; on return bufs[0] names the buffer holding the result).  q_dev points at the
+// amplitude row of the first step (nsrc values per step).
+int k_leapfrog(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev *src_dev,
+               int nsrc, const void *q_dev);
+int k_leapfrog_unfused(const KernelArgs &ka, void *state, int64_t nsteps, const SrcDev *src_dev,
+                       int nsrc, const void *q_dev);
+// h <- h + 0.5 cH (C e)  (seed sync, a4)
+int k_sync(const KernelArgs &ka, void *state);
+// h <- h - 0.5 cH (C e)  (staggered start, reading 11)
+int k_half_start(const KernelArgs &ka, void *state);
+// one substep of the polynomial: b <- p(X) b.  bufs[0] = b in/out, bufs[1..3] scratch; on
+// return bufs[0] names the result and bufs[1..3] the free buffers.
+int k_poly_substep(const KernelArgs &ka, const Plan &plan, void *bufs[4]);
+int k_poly_substep_unfused(const KernelArgs &ka, const Plan &plan, void *bufs[4]);
+// x <- x + alpha y (state-sized), or over components [c0, c1)
+int k_axpy(const KernelArgs &ka, void *x, const void *y, double alpha);
+int k_axpy_comps(const KernelArgs &ka, void *x, const void *y, double alpha, int c0, int c1);
+int k_check_finite_async(const KernelArgs &ka, const void *state, int *dflag);
+// non-finite check over the state; sets *flag (device int) if any
+int k_check_finite(const KernelArgs &ka, const void *state, int *host_flag);
+// energy-weighted dot products for K5 Lanczos: out[0] = <x,y>_M (host, synchronous)
+int k_dot_M(const KernelArgs &ka, const void *x, const void *y, double *out);
+// y <- sigma*dt*A_orig x  (one A-application, unfused)
+int k_apply_A(const KernelArgs &ka, const void *x, void *y, double sigma);
+// z <- alpha x + beta y + gamma z
+int k_lincomb(const KernelArgs &ka, void *z, const void *x, const void *y, double alpha,
+              double beta, double gamma);
+// fill a live-masked pseudo-random state (counter-based hash, seed)
+int k_fill_random(const KernelArgs &ka, void *state, uint64_t seed);
+
+}  // namespace pe
+
+struct paraexp_grid {
+    pe::Grid g;
+};

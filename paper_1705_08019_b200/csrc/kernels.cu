@@ -1,0 +1,528 @@
+// kernels.cu -- device kernels of the paraexp-b200 library (sm_100a).
+//
+// Rows a2/a3 (leapfrog halves), a4 (seed sync), a6 (polynomial recurrence, unfused form),
+// K0 pack/unpack, non-finite checks, energy-weighted dots (K5) and helpers.
+// The fused z-marching kernels live in fused.cu.
+//
+// Stencils (PAPER:153-157 eq:maxwell_grid1), device layout of internal.h:
+//  (C e)_x = ey + ez(j+1) - ey(k+1) - ez      (C^T h)_x = hz - hz(j-1) - hy + hy(k-1)
+//  (C e)_y = ez + ex(k+1) - ez(i+1) - ex      (C^T h)_y = hx - hx(k-1) - hz + hz(i-1)
+//  (C e)_z = ex + ey(i+1) - ex(j+1) - ey      (C^T h)_z = hy - hy(i-1) - hx + hx(j-1)
+// Neighbours outside [0,n) are dead/virtual DOFs and read as 0.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <type_traits>
+
+#include "internal.h"
+#include "kernels_common.cuh"
+
+namespace pe {
+
+// ---------------------------------------------------------------------------------------
+// runtime helpers
+// ---------------------------------------------------------------------------------------
+int check_cuda(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PARAEXP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return PARAEXP_OK;
+}
+int dev_alloc(void **p, size_t bytes) {
+    *p = nullptr;
+    if (bytes == 0) return PARAEXP_OK;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return fail(e == cudaErrorMemoryAllocation ? PARAEXP_ENOMEM : PARAEXP_ECUDA,
+                    std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    return PARAEXP_OK;
+}
+void dev_free(void *p) {
+    if (p) cudaFree(p);
+}
+int dev_memset_async(void *p, int v, size_t bytes, void *stream) {
+    if (cudaMemsetAsync(p, v, bytes, (cudaStream_t)stream) != cudaSuccess) return check_cuda("memset");
+    return PARAEXP_OK;
+}
+int dev_memcpy_h2d_async(void *dst, const void *src, size_t bytes, void *stream) {
+    if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
+        return check_cuda("memcpy h2d");
+    return PARAEXP_OK;
+}
+int dev_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream) {
+    if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream) != cudaSuccess)
+        return check_cuda("memcpy d2h");
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return check_cuda("sync");
+    return PARAEXP_OK;
+}
+int dev_memcpy_d2d_async(void *dst, const void *src, size_t bytes, void *stream) {
+    if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) != cudaSuccess)
+        return check_cuda("memcpy d2d");
+    return PARAEXP_OK;
+}
+int dev_set_device(int device) {
+    if (cudaSetDevice(device) != cudaSuccess) return check_cuda("cudaSetDevice");
+    return PARAEXP_OK;
+}
+int dev_sync(void *stream) {
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return check_cuda("sync");
+    return PARAEXP_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// K0: pack / unpack (canonical <-> device layout), zeroing dead DOFs (reading 5)
+// ---------------------------------------------------------------------------------------
+template <typename T, int EM, bool HA>
+__global__ void pack_kernel(Dev<T> D, Coef<T, EM, HA> cf, const T *__restrict__ e,
+                            const T *__restrict__ h, T *__restrict__ st) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    if (i >= D.px || j >= D.ny) return;
+    const int64_t idx = D.idx(i, j, k);
+    const int64_t NX = D.nx + 1, NY = D.ny + 1;
+    const int64_t np = NX * NY * (D.nz + 1);
+    const int64_t p = i + NX * (j + NY * (int64_t)k);
+    const bool in = i < D.nx;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        T ve = (in && D.e_live(c, i, j, k) && cf.e_alive(c, idx)) ? e[c * np + p] : T(0);
+        T vh = (in && D.h_live(c, i, j, k)) ? h[c * np + p] : T(0);
+        st[c * D.cs + idx] = ve;
+        st[(3 + c) * D.cs + idx] = vh;
+    }
+}
+
+template <typename T>
+__global__ void unpack_kernel(Dev<T> D, const T *__restrict__ st, T *__restrict__ e,
+                              T *__restrict__ h) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    if (i > D.nx || j > D.ny) return;
+    const int64_t NX = D.nx + 1, NY = D.ny + 1;
+    const int64_t np = NX * NY * (D.nz + 1);
+    const int64_t p = i + NX * (j + NY * (int64_t)k);
+    const bool in = i < D.nx && j < D.ny && k < D.nz;
+    const int64_t idx = in ? D.idx(i, j, k) : 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        e[c * np + p] = in ? st[c * D.cs + idx] : T(0);
+        h[c * np + p] = in ? st[(3 + c) * D.cs + idx] : T(0);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1u: unfused leapfrog halves (a2, a3) -- also the generic "X w" application
+// ---------------------------------------------------------------------------------------
+// e <- e + beta_E .* (C^T h)   (beta_E = cE * sigma, sigma = 1 for leapfrog)
+template <typename T, int EM, bool HA>
+__global__ void __launch_bounds__(256) e_half_kernel(Dev<T> D, Coef<T, EM, HA> cf,
+                                                     T *__restrict__ st) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    if (i >= D.nx || j >= D.ny) return;
+    const int64_t idx = D.idx(i, j, k);
+    T *ex = st, *ey = st + D.cs, *ez = st + 2 * D.cs;
+    const T *hx = st + 3 * D.cs, *hy = st + 4 * D.cs, *hz = st + 5 * D.cs;
+    T c0, c1, c2;
+    curlT_at(D, hx, hy, hz, i, j, k, idx, c0, c1, c2);
+    if (D.e_live(0, i, j, k)) ex[idx] = ex[idx] + cf.bE(0, k, idx) * c0;
+    if (D.e_live(1, i, j, k)) ey[idx] = ey[idx] + cf.bE(1, k, idx) * c1;
+    if (D.e_live(2, i, j, k)) ez[idx] = ez[idx] + cf.bE(2, k, idx) * c2;
+}
+
+// h <- h - coef * beta_H .* (C e)   (coef = 1 leapfrog, -1/2 seed sync, +1/2 half start)
+template <typename T, int EM, bool HA>
+__global__ void __launch_bounds__(256) h_half_kernel(Dev<T> D, Coef<T, EM, HA> cf,
+                                                     T *__restrict__ st, T coef) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    if (i >= D.nx || j >= D.ny) return;
+    const int64_t idx = D.idx(i, j, k);
+    const T *ex = st, *ey = st + D.cs, *ez = st + 2 * D.cs;
+    T *hx = st + 3 * D.cs, *hy = st + 4 * D.cs, *hz = st + 5 * D.cs;
+    T c0, c1, c2;
+    curl_at(D, ex, ey, ez, i, j, k, idx, c0, c1, c2);
+    if (D.h_live(0, i, j, k)) hx[idx] = hx[idx] - (coef * cf.bH(0, idx)) * c0;
+    if (D.h_live(1, i, j, k)) hy[idx] = hy[idx] - (coef * cf.bH(1, idx)) * c1;
+    if (D.h_live(2, i, j, k)) hz[idx] = hz[idx] - (coef * cf.bH(2, idx)) * c2;
+}
+
+// e_s <- e_s - q[m][s], sequentially in s (deterministic for coincident edges)
+template <typename T>
+__global__ void inject_kernel(T *__restrict__ st, const SrcDev *__restrict__ src, int nsrc,
+                              const T *__restrict__ q) {
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < nsrc; ++s) st[src[s].off] = st[src[s].off] - q[s];
+}
+
+// ---------------------------------------------------------------------------------------
+// Polynomial recurrence, unfused (a6): u = X w ;  pair/half/zero updates
+// ---------------------------------------------------------------------------------------
+// out = X in:  out_h = -bH .* (C in_e),  out_e = bE .* (C^T in_h)
+template <typename T, int EM, bool HA>
+__global__ void __launch_bounds__(256) applyX_kernel(Dev<T> D, Coef<T, EM, HA> cf,
+                                                     const T *__restrict__ in,
+                                                     T *__restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    if (i >= D.nx || j >= D.ny) return;
+    const int64_t idx = D.idx(i, j, k);
+    T a0, a1, a2, b0, b1, b2;
+    curlT_at(D, in + 3 * D.cs, in + 4 * D.cs, in + 5 * D.cs, i, j, k, idx, a0, a1, a2);
+    curl_at(D, in, in + D.cs, in + 2 * D.cs, i, j, k, idx, b0, b1, b2);
+    out[idx] = D.e_live(0, i, j, k) ? cf.bE(0, k, idx) * a0 : T(0);
+    out[D.cs + idx] = D.e_live(1, i, j, k) ? cf.bE(1, k, idx) * a1 : T(0);
+    out[2 * D.cs + idx] = D.e_live(2, i, j, k) ? cf.bE(2, k, idx) * a2 : T(0);
+    out[3 * D.cs + idx] = D.h_live(0, i, j, k) ? -(cf.bH(0, idx) * b0) : T(0);
+    out[4 * D.cs + idx] = D.h_live(1, i, j, k) ? -(cf.bH(1, idx) * b1) : T(0);
+    out[5 * D.cs + idx] = D.h_live(2, i, j, k) ? -(cf.bH(2, idx) * b2) : T(0);
+}
+
+// y <- (init ? 0 : y) + a w + b u ;  if do_w:  w <- X u + e2 w   (in place on w)
+template <typename T, int EM, bool HA>
+__global__ void __launch_bounds__(256) pair_update_kernel(Dev<T> D, Coef<T, EM, HA> cf,
+                                                          T *__restrict__ w,
+                                                          const T *__restrict__ u,
+                                                          T *__restrict__ y, T a, T b, T e2,
+                                                          int init, int do_w) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    if (i >= D.nx || j >= D.ny) return;
+    const int64_t idx = D.idx(i, j, k);
+    T xu[6];
+    if (do_w) {
+        T a0, a1, a2, b0, b1, b2;
+        curlT_at(D, u + 3 * D.cs, u + 4 * D.cs, u + 5 * D.cs, i, j, k, idx, a0, a1, a2);
+        curl_at(D, u, u + D.cs, u + 2 * D.cs, i, j, k, idx, b0, b1, b2);
+        xu[0] = D.e_live(0, i, j, k) ? cf.bE(0, k, idx) * a0 : T(0);
+        xu[1] = D.e_live(1, i, j, k) ? cf.bE(1, k, idx) * a1 : T(0);
+        xu[2] = D.e_live(2, i, j, k) ? cf.bE(2, k, idx) * a2 : T(0);
+        xu[3] = D.h_live(0, i, j, k) ? -(cf.bH(0, idx) * b0) : T(0);
+        xu[4] = D.h_live(1, i, j, k) ? -(cf.bH(1, idx) * b1) : T(0);
+        xu[5] = D.h_live(2, i, j, k) ? -(cf.bH(2, idx) * b2) : T(0);
+    }
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        const int64_t q = c * D.cs + idx;
+        const T wv = w[q];
+        const T uv = u[q];
+        const T y0 = init ? T(0) : y[q];
+        y[q] = (y0 + a * wv) + b * uv;
+        if (do_w) w[q] = xu[c] + e2 * wv;
+    }
+}
+
+// zero node: y <- (init ? 0 : y) + c w ; if do_w: wn <- X w
+template <typename T, int EM, bool HA>
+__global__ void __launch_bounds__(256) zero_node_kernel(Dev<T> D, Coef<T, EM, HA> cf,
+                                                        const T *__restrict__ w,
+                                                        T *__restrict__ wn,
+                                                        T *__restrict__ y, T cc, int init,
+                                                        int do_w) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    if (i >= D.nx || j >= D.ny) return;
+    const int64_t idx = D.idx(i, j, k);
+    if (do_w) {
+        T a0, a1, a2, b0, b1, b2;
+        curlT_at(D, w + 3 * D.cs, w + 4 * D.cs, w + 5 * D.cs, i, j, k, idx, a0, a1, a2);
+        curl_at(D, w, w + D.cs, w + 2 * D.cs, i, j, k, idx, b0, b1, b2);
+        wn[idx] = D.e_live(0, i, j, k) ? cf.bE(0, k, idx) * a0 : T(0);
+        wn[D.cs + idx] = D.e_live(1, i, j, k) ? cf.bE(1, k, idx) * a1 : T(0);
+        wn[2 * D.cs + idx] = D.e_live(2, i, j, k) ? cf.bE(2, k, idx) * a2 : T(0);
+        wn[3 * D.cs + idx] = D.h_live(0, i, j, k) ? -(cf.bH(0, idx) * b0) : T(0);
+        wn[4 * D.cs + idx] = D.h_live(1, i, j, k) ? -(cf.bH(1, idx) * b1) : T(0);
+        wn[5 * D.cs + idx] = D.h_live(2, i, j, k) ? -(cf.bH(2, idx) * b2) : T(0);
+    }
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        const int64_t q = c * D.cs + idx;
+        const T y0 = init ? T(0) : y[q];
+        y[q] = y0 + cc * w[q];
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// vector helpers
+// ---------------------------------------------------------------------------------------
+template <typename T>
+__global__ void axpy_kernel(T *__restrict__ x, const T *__restrict__ y, T alpha, int64_t n) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x)
+        x[q] = x[q] + alpha * y[q];
+}
+template <typename T>
+__global__ void lincomb_kernel(T *__restrict__ z, const T *__restrict__ x,
+                               const T *__restrict__ y, T al, T be, T ga, int64_t n) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x)
+        z[q] = al * x[q] + be * y[q] + ga * z[q];
+}
+template <typename T>
+__global__ void finite_kernel(const T *__restrict__ x, int64_t n, int *flag) {
+    int bad = 0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite((double)x[q]);
+    bad = __syncthreads_or(bad);
+    if (bad && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+// <x, y>_M / dt = sum_e x y / cE + sum_h x y / cH over live DOFs (energy inner product)
+template <typename T, int EM, bool HA>
+__global__ void __launch_bounds__(256) dotM_kernel(Dev<T> D, Coef<T, EM, HA> cf,
+                                                   const T *__restrict__ x,
+                                                   const T *__restrict__ y, double *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    double acc = 0.0;
+    if (i < D.nx && j < D.ny) {
+        const int64_t idx = D.idx(i, j, k);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double ce = (double)cf.bE(c, k, idx);
+            if (D.e_live(c, i, j, k) && ce != 0.0)
+                acc += (double)x[c * D.cs + idx] * (double)y[c * D.cs + idx] / ce;
+            const double ch = (double)cf.bH(c, idx);
+            if (D.h_live(c, i, j, k) && ch != 0.0)
+                acc += (double)x[(3 + c) * D.cs + idx] * (double)y[(3 + c) * D.cs + idx] / ch;
+        }
+    }
+    acc = block_sum(acc);
+    if (threadIdx.x == 0 && threadIdx.y == 0) atomicAdd(out, acc);
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+template <typename T, int EM, bool HA>
+__global__ void fill_random_kernel(Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ st,
+                                   uint64_t seed) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    if (i >= D.px || j >= D.ny) return;
+    const int64_t idx = D.idx(i, j, k);
+    const bool in = i < D.nx;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        const uint64_t r = splitmix64(seed ^ ((uint64_t)(c * D.cs + idx) * 0x2545F4914F6CDD1Dull));
+        const double u = (double)(r >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+        bool live = in && (c < 3 ? (D.e_live(c, i, j, k) && cf.e_alive(c, idx)) : D.h_live(c - 3, i, j, k));
+        st[c * D.cs + idx] = live ? T(u) : T(0);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------------
+static dim3 cell_grid(const Layout &L, bool pad) {
+    const int64_t nx = pad ? L.px : L.nx;
+    return dim3((unsigned)((nx + 31) / 32), (unsigned)((L.ny + 7) / 8), (unsigned)L.nz);
+}
+static const dim3 kBlock(32, 8, 1);
+
+int k_pack(const KernelArgs &ka, const void *e, const void *h, void *state) {
+    return with_types(*ka.g, 1.0, [&](auto tT, auto tEM, auto tHA) {
+        using T = decltype(tT);
+        constexpr int EM = decltype(tEM)::value;
+        constexpr bool HA = decltype(tHA)::value;
+        auto D = make_dev<T>(*ka.g);
+        auto cf = make_coef<T, EM, HA>(*ka.g, 1.0);
+        pack_kernel<T, EM, HA><<<cell_grid(ka.g->L, true), kBlock, 0, (cudaStream_t)ka.stream>>>(
+            D, cf, (const T *)e, (const T *)h, (T *)state);
+        ++*ka.launches;
+        return check_cuda("pack");
+    });
+}
+
+int k_unpack(const KernelArgs &ka, const void *state, void *e, void *h) {
+    const Grid &g = *ka.g;
+    dim3 grid((unsigned)((g.nx + 1 + 31) / 32), (unsigned)((g.ny + 1 + 7) / 8), (unsigned)(g.nz + 1));
+    if (g.dtype == PARAEXP_F64)
+        unpack_kernel<double><<<grid, kBlock, 0, (cudaStream_t)ka.stream>>>(make_dev<double>(g), (const double *)state, (double *)e, (double *)h);
+    else
+        unpack_kernel<float><<<grid, kBlock, 0, (cudaStream_t)ka.stream>>>(make_dev<float>(g), (const float *)state, (float *)e, (float *)h);
+    ++*ka.launches;
+    return check_cuda("unpack");
+}
+
+int k_leapfrog_unfused(const KernelArgs &ka, void *state, int64_t nsteps, const SrcDev *src_dev,
+                       int nsrc, const void *q_dev) {
+    return with_types(*ka.g, 1.0, [&](auto tT, auto tEM, auto tHA) {
+        using T = decltype(tT);
+        constexpr int EM = decltype(tEM)::value;
+        constexpr bool HA = decltype(tHA)::value;
+        auto D = make_dev<T>(*ka.g);
+        auto cf = make_coef<T, EM, HA>(*ka.g, 1.0);
+        const dim3 grid = cell_grid(ka.g->L, false);
+        cudaStream_t s = (cudaStream_t)ka.stream;
+        for (int64_t m = 0; m < nsteps; ++m) {
+            e_half_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, (T *)state);
+            if (nsrc > 0)
+                inject_kernel<T><<<1, 32, 0, s>>>((T *)state, src_dev, nsrc, (const T *)q_dev + m * nsrc);
+            h_half_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, (T *)state, T(1));
+            *ka.launches += 2 + (nsrc > 0);
+        }
+        return check_cuda("leapfrog");
+    });
+}
+
+static int h_shift(const KernelArgs &ka, void *state, double coef) {
+    return with_types(*ka.g, 1.0, [&](auto tT, auto tEM, auto tHA) {
+        using T = decltype(tT);
+        constexpr int EM = decltype(tEM)::value;
+        constexpr bool HA = decltype(tHA)::value;
+        h_half_kernel<T, EM, HA><<<cell_grid(ka.g->L, false), kBlock, 0, (cudaStream_t)ka.stream>>>(
+            make_dev<T>(*ka.g), make_coef<T, EM, HA>(*ka.g, 1.0), (T *)state, T(coef));
+        ++*ka.launches;
+        return check_cuda("h shift");
+    });
+}
+// h_sync = h + 1/2 cH (C e): h - (-1/2) cH (C e)
+int k_sync(const KernelArgs &ka, void *state) { return h_shift(ka, state, -0.5); }
+// h^(1/2) = h - 1/2 cH (C e)
+int k_half_start(const KernelArgs &ka, void *state) { return h_shift(ka, state, 0.5); }
+
+int k_poly_substep_unfused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
+    return with_types(*ka.g, plan.sigma, [&](auto tT, auto tEM, auto tHA) {
+        using T = decltype(tT);
+        constexpr int EM = decltype(tEM)::value;
+        constexpr bool HA = decltype(tHA)::value;
+        auto D = make_dev<T>(*ka.g);
+        auto cf = make_coef<T, EM, HA>(*ka.g, plan.sigma);
+        const dim3 grid = cell_grid(ka.g->L, false);
+        cudaStream_t s = (cudaStream_t)ka.stream;
+        T *w = (T *)bufs[0], *yy = (T *)bufs[1], *uu = (T *)bufs[2], *sp = (T *)bufs[3];
+        int init = 1;
+        for (const Op &op : plan.ops) {
+            if (op.kind == 0 || op.kind == 1) {
+                applyX_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, w, uu);
+                pair_update_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(
+                    D, cf, w, uu, yy, T(op.a), T(op.b), T(op.e2), init, op.kind == 0);
+                *ka.launches += 2;
+            } else {
+                const int do_w = op.kind == 2;
+                zero_node_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, w, sp, yy, T(op.a), init, do_w);
+                ++*ka.launches;
+                if (do_w) std::swap(w, sp);
+            }
+            init = 0;
+        }
+        bufs[0] = yy;
+        bufs[1] = w;
+        bufs[2] = uu;
+        bufs[3] = sp;
+        return check_cuda("poly substep");
+    });
+}
+
+int k_axpy(const KernelArgs &ka, void *x, const void *y, double alpha) {
+    const int64_t n = ka.g->L.state_elems();
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    if (ka.g->dtype == PARAEXP_F64)
+        axpy_kernel<double><<<blocks, 256, 0, (cudaStream_t)ka.stream>>>((double *)x, (const double *)y, alpha, n);
+    else
+        axpy_kernel<float><<<blocks, 256, 0, (cudaStream_t)ka.stream>>>((float *)x, (const float *)y, (float)alpha, n);
+    ++*ka.launches;
+    return check_cuda("axpy");
+}
+
+int k_axpy_comps(const KernelArgs &ka, void *x, const void *y, double alpha, int c0, int c1) {
+    const int64_t cs = ka.g->L.cs;
+    const int64_t n = (c1 - c0) * cs;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    if (ka.g->dtype == PARAEXP_F64)
+        axpy_kernel<double><<<blocks, 256, 0, (cudaStream_t)ka.stream>>>((double *)x + c0 * cs, (const double *)y + c0 * cs, alpha, n);
+    else
+        axpy_kernel<float><<<blocks, 256, 0, (cudaStream_t)ka.stream>>>((float *)x + c0 * cs, (const float *)y + c0 * cs, (float)alpha, n);
+    ++*ka.launches;
+    return check_cuda("axpy");
+}
+
+int k_lincomb(const KernelArgs &ka, void *z, const void *x, const void *y, double al, double be,
+              double ga) {
+    const int64_t n = ka.g->L.state_elems();
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    if (ka.g->dtype == PARAEXP_F64)
+        lincomb_kernel<double><<<blocks, 256, 0, (cudaStream_t)ka.stream>>>((double *)z, (const double *)x, (const double *)y, al, be, ga, n);
+    else
+        lincomb_kernel<float><<<blocks, 256, 0, (cudaStream_t)ka.stream>>>((float *)z, (const float *)x, (const float *)y, (float)al, (float)be, (float)ga, n);
+    ++*ka.launches;
+    return check_cuda("lincomb");
+}
+
+int k_check_finite_async(const KernelArgs &ka, const void *state, int *dflag) {
+    const int64_t n = ka.g->L.state_elems();
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    if (ka.g->dtype == PARAEXP_F64)
+        finite_kernel<double><<<blocks, 256, 0, (cudaStream_t)ka.stream>>>((const double *)state, n, dflag);
+    else
+        finite_kernel<float><<<blocks, 256, 0, (cudaStream_t)ka.stream>>>((const float *)state, n, dflag);
+    ++*ka.launches;
+    return check_cuda("finite");
+}
+
+int k_check_finite(const KernelArgs &ka, const void *state, int *host_flag) {
+    int *dflag = (int *)ka.g->d_flag;
+    int rc = dev_memset_async(dflag, 0, sizeof(int), ka.stream);
+    if (rc) return rc;
+    if ((rc = k_check_finite_async(ka, state, dflag))) return rc;
+    return dev_memcpy_d2h(host_flag, dflag, sizeof(int), ka.stream);
+}
+
+int k_dot_M(const KernelArgs &ka, const void *x, const void *y, double *out) {
+    double *dred = (double *)ka.g->d_red;
+    int rc = dev_memset_async(dred, 0, sizeof(double), ka.stream);
+    if (rc) return rc;
+    rc = with_types(*ka.g, 1.0, [&](auto tT, auto tEM, auto tHA) {
+        using T = decltype(tT);
+        constexpr int EM = decltype(tEM)::value;
+        constexpr bool HA = decltype(tHA)::value;
+        dotM_kernel<T, EM, HA><<<cell_grid(ka.g->L, false), kBlock, 0, (cudaStream_t)ka.stream>>>(
+            make_dev<T>(*ka.g), make_coef<T, EM, HA>(*ka.g, 1.0), (const T *)x, (const T *)y, dred);
+        ++*ka.launches;
+        return check_cuda("dotM");
+    });
+    if (rc) return rc;
+    return dev_memcpy_d2h(out, dred, sizeof(double), ka.stream);
+}
+
+int k_apply_A(const KernelArgs &ka, const void *x, void *y, double sigma) {
+    return with_types(*ka.g, sigma, [&](auto tT, auto tEM, auto tHA) {
+        using T = decltype(tT);
+        constexpr int EM = decltype(tEM)::value;
+        constexpr bool HA = decltype(tHA)::value;
+        applyX_kernel<T, EM, HA><<<cell_grid(ka.g->L, false), kBlock, 0, (cudaStream_t)ka.stream>>>(
+            make_dev<T>(*ka.g), make_coef<T, EM, HA>(*ka.g, sigma), (const T *)x, (T *)y);
+        ++*ka.launches;
+        return check_cuda("applyA");
+    });
+}
+
+int k_fill_random(const KernelArgs &ka, void *state, uint64_t seed) {
+    return with_types(*ka.g, 1.0, [&](auto tT, auto tEM, auto tHA) {
+        using T = decltype(tT);
+        constexpr int EM = decltype(tEM)::value;
+        constexpr bool HA = decltype(tHA)::value;
+        fill_random_kernel<T, EM, HA><<<cell_grid(ka.g->L, true), kBlock, 0, (cudaStream_t)ka.stream>>>(
+            make_dev<T>(*ka.g), make_coef<T, EM, HA>(*ka.g, 1.0), (T *)state, seed);
+        ++*ka.launches;
+        return check_cuda("fill random");
+    });
+}
+
+}  // namespace pe

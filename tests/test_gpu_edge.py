@@ -1,0 +1,90 @@
+"""GPU edge cases and error behaviour of the C ABI (degenerate grids, empty runs, invalid
+arguments, divergence detection)."""
+import numpy as np
+import pytest
+
+import paper_1705_08019_b200 as pe
+from gpu_util import inputs, lib_expmv, lib_leapfrog, lib_solve
+from oracle import fit
+from synth import Source, gauss_sine, random_fields
+
+pytestmark = pytest.mark.gpu
+
+
+def test_zero_steps_and_zero_tau_are_identity_on_live_dofs():
+    n = (9, 7, 5)
+    og = fit.Grid(*n, d0=1e-3, dt_frac=0.9)
+    lg = pe.Grid(*n, d0=1e-3, dt_frac=0.9)
+    e_raw, h_raw = random_fields(*n, seed=1)
+    e, h = inputs(og, e_raw, h_raw)
+    ge, gh, _ = lib_leapfrog(lg, e_raw, h_raw, 0, [])
+    assert np.array_equal(ge, e) and np.array_equal(gh, h)    # dead DOFs zeroed, rest kept
+    ge, gh, _ = lib_expmv(lg, 0.0, e_raw, h_raw, rho=og.rho_cfl, m=8, s=1)
+    assert np.array_equal(ge, e) and np.array_equal(gh, h)
+
+
+@pytest.mark.parametrize("n", [(1, 1, 1), (1, 4, 3), (2, 1, 5), (5, 3, 1), (33, 2, 2)])
+def test_degenerate_grids(n):
+    og = fit.Grid(*n, d0=1e-3, dt_frac=0.9)
+    lg = pe.Grid(*n, d0=1e-3, dt_frac=0.9)
+    e, h = inputs(og, *random_fields(*n, seed=2))
+    ref = fit.leapfrog(og, e, h, 25)
+    ge, gh, _ = lib_leapfrog(lg, e, h, 25, [])
+    np.testing.assert_allclose(ge, ref[0], rtol=0, atol=1e-12 * max(1.0, np.abs(ref[0]).max()))
+    np.testing.assert_allclose(gh, ref[1], rtol=0, atol=1e-12 * max(1e-3, np.abs(ref[1]).max()))
+
+
+def test_invalid_arguments():
+    with pytest.raises(pe.ParaexpError) as ei:
+        pe.Grid(0, 4, 4, d0=1e-3, dt_frac=0.9)
+    assert ei.value.code == pe.EINVAL
+    with pytest.raises(pe.ParaexpError):
+        pe.Grid(4, 4, 4, d0=1e-3, dt_frac=0.9, dt=1e-12)             # both dt and dt_frac
+    with pytest.raises(pe.ParaexpError):
+        pe.Grid(4, 4, 4, d0=1e-3, dt_frac=0.9, eps_r=-np.ones(64))
+    lg = pe.Grid(6, 6, 6, d0=1e-3, dt_frac=0.9)
+    og = fit.Grid(6, 6, 6, d0=1e-3, dt_frac=0.9)
+    e, h = og.zeros()
+    with pytest.raises(pe.ParaexpError) as ei:                       # source on a PEC wall edge
+        lib_leapfrog(lg, e, h, 3, [Source(0, 2, 0, 3, "gauss_paper", 1.0, 1e-12)])
+    assert ei.value.code == pe.EINVAL
+    with pytest.raises(pe.ParaexpError) as ei:                       # nsteps < p
+        lib_solve(lg, 3, 4, [])
+    assert ei.value.code == pe.EINVAL
+    with pytest.raises(pe.ParaexpError) as ei:                       # odd Leja degree > 1
+        lib_expmv(lg, 1e-12, e, h, m=3, s=1, rho=og.rho_cfl)
+    assert ei.value.code == pe.EINVAL
+
+
+def test_cfl_warning_and_divergence_detection():
+    lg = pe.Grid(8, 8, 8, d0=1e-3, dt_frac=1.5)
+    assert lg.warnings == pe.abi.WCFL                                 # warn, do not forbid
+    og = fit.Grid(8, 8, 8, d0=1e-3, dt_frac=1.5)
+    e, h = inputs(og, *random_fields(8, 8, 8, seed=3))
+    with pytest.raises(pe.ParaexpError) as ei:
+        lib_leapfrog(lg, e, h, 3000, [], check_finite=True)
+    assert ei.value.code == pe.EDIVERGED
+
+
+def test_host_only_grid_refuses_compute():
+    lg = pe.Grid(4, 4, 4, d0=1e-3, dt_frac=0.9, device=-1)
+    import torch
+    t = torch.zeros(3 * lg.npts, dtype=torch.float64, device="cuda:0")
+    with pytest.raises(Exception):
+        pe.leapfrog(lg, t, t.clone(), 1)
+
+
+def test_rho_pow_bounds():
+    """K5 Lanczos estimate: <= rho_CFL and close to the closed-form rho on a uniform grid;
+    on random eps (C2-like) clearly below rho_CFL (SURVEY finding 8)."""
+    import math
+    from oracle import dense
+    lg = pe.Grid(16, 16, 16, d0=1e-3, dt_frac=0.9)
+    inf = lg.info(compute_rho_pow=True)
+    c = 1 / math.sqrt(fit.EPS0 * fit.MU0)
+    rho = dense.cavity_frequencies(16, 16, 16, 1e-3, c).max()
+    assert rho * 0.97 <= inf["rho_pow"] <= rho * 1.0000001
+    eps = np.random.default_rng(2).uniform(1, 4, 32 ** 3)
+    lg2 = pe.Grid(32, 32, 32, d0=1e-3, eps_r=eps, dt_frac=0.95)
+    inf2 = lg2.info(compute_rho_pow=True)
+    assert 0.6 * inf2["rho_cfl"] < inf2["rho_pow"] < 0.85 * inf2["rho_cfl"]

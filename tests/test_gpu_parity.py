@@ -1,0 +1,200 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle on the same seeded inputs.
+
+Tolerances (north_star): rel-L2 <= 1e-10 (fp64), <= 1e-4 (fp32, oracle fed the fp32-rounded
+constants, DESIGN reading 24), separately for e (volts) and h (amperes)."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1705_08019_b200 as pe
+from gpu_util import (TOL, assert_parity, inputs, lib_expmv, lib_leapfrog, lib_solve, rel_l2)
+from oracle import fit
+from synth import (Source, config_c1, config_c2, config_c3, gauss_sine, layered_eps, random_fields,
+                   spiral_pec_cells)
+
+pytestmark = pytest.mark.gpu
+KERNELS = ["unfused", "fused"]
+
+
+def _material(kind, n, seed=3):
+    nx, ny, nz = n
+    if kind == "vacuum":
+        return None, None
+    if kind == "layered":
+        return layered_eps(nx, ny, nz, (1.0, 2.2, 4.4, 9.8)[:max(1, min(4, nz))]), None
+    rng = np.random.default_rng(seed)
+    eps = rng.uniform(1.0, 4.0, nx * ny * nz)
+    pec = (rng.uniform(size=nx * ny * nz) < 0.03).astype(np.uint8)
+    return eps, pec
+
+
+def _grids(n, kind, dtype, kernels, frac=0.95):
+    eps, pec = _material(kind, n)
+    og = fit.Grid(*n, d0=1e-3, eps_r=eps, pec_cell=pec, dt_frac=frac, dtype=dtype)
+    lg = pe.Grid(*n, d0=1e-3, eps_r=eps, pec_cell=pec, dt_frac=frac, dtype=dtype, kernels=kernels)
+    return og, lg
+
+
+def _sources(og, n):
+    nx, ny, nz = n
+    cands = [gauss_sine(2, nx // 2, ny // 3, nz // 2, f0=40e9, bw=40e9),
+             Source(0, nx // 3, ny // 2, max(1, nz // 3), "gauss_paper", 0.7, 6e-12),
+             Source(1, max(1, nx - 2), 1, max(1, nz - 2), "sine", 0.3, 0.0, 25e9, 0.0, 2.0)]
+    return [s for s in cands if og.cE[og.edge_dof(s.comp, s.i, s.j, s.k)] != 0]
+
+
+@pytest.mark.parametrize("kernels", KERNELS)
+def test_leapfrog_c1(kernels):
+    w = config_c1()
+    og = fit.Grid.from_workload(w)
+    lg = pe.Grid.from_workload(w, kernels=kernels)
+    assert lg.info()["material_mode"] == pe.abi.MAT_SCALAR
+    e, h = og.zeros()
+    ref = fit.leapfrog(og, e, h, w.nsteps, w.sources)
+    ge, gh, st = lib_leapfrog(lg, e, h, w.nsteps, w.sources)
+    assert_parity((ge, gh), ref, "f64", "C1 leapfrog")
+    assert st["curl_applications"] == 2 * w.nsteps          # eq:cost_LF
+    assert np.linalg.norm(ref[0]) > 0
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("kind", ["vacuum", "layered", "random"])
+@pytest.mark.parametrize("kernels", KERNELS)
+def test_leapfrog_ragged(dtype, kind, kernels):
+    n = (37, 23, 11)
+    og, lg = _grids(n, kind, dtype, kernels)
+    e, h = inputs(og, *random_fields(*n, seed=41))
+    src = _sources(og, n)
+    t0 = 3.5e-12
+    ref = fit.leapfrog(og, e, h, 300, src, t0=t0)
+    ge, gh, _ = lib_leapfrog(lg, e, h, 300, src, t0=t0)
+    assert_parity((ge, gh), ref, dtype, f"leapfrog {kind} {dtype}")
+    # dead DOFs stay exactly zero
+    assert not ge[~og.live_e].any() and not gh[~og.live_h].any()
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("method,m,s", [("leja", 40, 3), ("leja", 1, 7), ("leja", 2, 5),
+                                         ("leja", 64, 1), ("taylor", 16, 6)])
+@pytest.mark.parametrize("kind", ["vacuum", "layered", "random"])
+def test_expmv_fixed_plan(dtype, method, m, s, kind):
+    n = (21, 19, 13)
+    og, lg = _grids(n, kind, dtype, "auto")
+    e, h = inputs(og, *random_fields(*n, seed=7))
+    rho = og.rho_cfl
+    tau = 30 * og.dt if method == "leja" else 6 * og.dt
+    plan = fit.make_plan(method, m, s, tau, rho)
+    ref = fit.expmv(og, plan, e, h, mode="pairs", dtype=dtype)
+    ge, gh, st = lib_expmv(lg, tau, e, h, method=method, m=m, s=s, rho=rho)
+    assert_parity((ge, gh), ref, dtype, f"expmv {method} m={m} s={s} {kind}")
+    assert st["a_applications"] == m * s
+    # plan equality (reading 25): m, s, nodes exactly; d-hat to 1e-14
+    lp = pe.expmv_plan(lg, tau, method, m, s, rho=rho)
+    assert (lp["m"], lp["s"]) == (plan.m, plan.s)
+    assert abs(lp["gamma"] - plan.gamma) <= 1e-15 * plan.gamma
+    assert max(abs(a - b) for a, b in zip(lp["d"], plan.d)) <= 1e-14
+
+
+def test_expmv_vs_complex_newton_fp64():
+    n = (16, 16, 12)
+    og, lg = _grids(n, "random", "f64", "auto")
+    e, h = inputs(og, *random_fields(*n, seed=9))
+    plan = fit.make_plan("leja", 30, 4, 40 * og.dt, og.rho_cfl)
+    ref = fit.expmv(og, plan, e, h, mode="complex")
+    ge, gh, _ = lib_expmv(lg, 40 * og.dt, e, h, method="leja", m=30, s=4, rho=og.rho_cfl)
+    assert_parity((ge, gh), ref, "f64", "expmv vs complex Newton")
+
+
+def _fixed_s(method, m, tol, tau, rho):
+    return max(1, math.ceil(tau * rho / fit.theta_m(method, m, tol)))
+
+
+def test_solve_c1():
+    """C1: 8^3 vacuum, 2000 steps, p = 2, Leja fixed plan (m = 40 at eps_A 1e-12)."""
+    w = config_c1()
+    og = fit.Grid.from_workload(w)
+    lg = pe.Grid.from_workload(w)
+    rho = og.rho_cfl
+    S = fit.partition(w.nsteps, w.p)
+    s = _fixed_s("leja", 40, 1e-12, (S[1] - S[0]) * og.dt, rho)
+    ref = fit.paraexp(og, w.sources, 0.0, w.nsteps, w.p,
+                      lambda tau: fit.make_plan("leja", 40, s, tau, rho), rho=rho)
+    ge, gh, st = lib_solve(lg, w.nsteps, w.p, w.sources, method="leja", m=40, s=s, rho=rho)
+    assert_parity((ge, gh), ref, "f64", "C1 solve")
+    assert st["root"] == 0 and st["first_interval"] == 1 and st["last_interval"] == 2
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("p", [1, 3, 4])
+def test_solve_random_u0(dtype, p):
+    n = (19, 17, 9)
+    og, lg = _grids(n, "random", dtype, "auto")
+    u0 = inputs(og, *random_fields(*n, seed=77))
+    src = _sources(og, n)
+    nsteps = 61
+    rho = og.rho_cfl
+    s = 6
+    ref = fit.paraexp(og, src, 1e-12, nsteps, p, lambda tau: fit.make_plan("leja", 24, s, tau, rho),
+                      u0=u0, rho=rho, dtype=dtype)
+    ge, gh, _ = lib_solve(lg, nsteps, p, src, u0=u0, t0=1e-12, method="leja", m=24, s=s, rho=rho)
+    assert_parity((ge, gh), ref, dtype, f"solve p={p} {dtype}")
+
+
+def test_solve_leapfrog_tails_equal_serial():
+    """tail = LEAPFROG reproduces serial leapfrog on the GPU path."""
+    n = (19, 17, 9)
+    og, lg = _grids(n, "random", "f64", "auto")
+    u0 = inputs(og, *random_fields(*n, seed=5))
+    src = _sources(og, n)
+    ref = fit.leapfrog(og, u0[0], fit.half_step_start(og, *u0), 50, src)
+    ge, gh, _ = lib_solve(lg, 50, 4, src, u0=u0, tail_mode="leapfrog", rho=og.rho_cfl, m=8, s=1)
+    assert_parity((ge, gh), ref, "f64", "leapfrog tails")
+
+
+def test_solve_c2_reduced():
+    """C2 grid at full size (64^3, random eps), 400 of its 20000 steps, p = 8."""
+    w = config_c2(nsteps=400)
+    og = fit.Grid.from_workload(w)
+    lg = pe.Grid.from_workload(w)
+    assert lg.info()["material_mode"] == pe.abi.MAT_ARRAY
+    rho = og.rho_cfl
+    s = _fixed_s("leja", 40, 1e-10, 50 * og.dt, rho)
+    ref = fit.paraexp(og, w.sources, 0.0, w.nsteps, w.p,
+                      lambda tau: fit.make_plan("leja", 40, s, tau, rho), rho=rho)
+    ge, gh, _ = lib_solve(lg, w.nsteps, w.p, w.sources, method="leja", m=40, s=s, rho=rho)
+    assert_parity((ge, gh), ref, "f64", "C2 reduced solve")
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_c3_full_grid_short(dtype):
+    """C3 at full size (256^3, layered): 12 leapfrog steps from random fields with the C3
+    source, then exp(tau A) with a fixed degree-8 Leja plan."""
+    w = config_c3(dtype=dtype)
+    og = fit.Grid.from_workload(w)
+    lg = pe.Grid.from_workload(w)
+    assert lg.info()["material_mode"] == pe.abi.MAT_ZTABLE
+    e, h = inputs(og, *random_fields(w.nx, w.ny, w.nz, seed=3))
+    ref = fit.leapfrog(og, e, h, 12, w.sources, t0=100e-12)
+    ge, gh, _ = lib_leapfrog(lg, e, h, 12, w.sources, t0=100e-12)
+    assert_parity((ge, gh), ref, dtype, "C3 leapfrog")
+    plan = fit.make_plan("leja", 8, 1, 3 * og.dt, og.rho_cfl)
+    ref2 = fit.expmv(og, plan, *ref, mode="pairs", dtype=dtype)
+    ge2, gh2, _ = lib_expmv(lg, 3 * og.dt, *ref, method="leja", m=8, s=1, rho=og.rho_cfl)
+    assert_parity((ge2, gh2), ref2, dtype, "C3 expmv")
+
+
+def test_spiral_pec_small():
+    """C4-like structure on a small grid: PEC spiral + via + substrate, port sources."""
+    nx, ny, nz = 64, 64, 16
+    pec, port, _ = spiral_pec_cells(nx, ny, nz, k_trace=5, turns=3, width=2, gap=1, outer=40, k_sub=5)
+    eps = np.ones((nz, ny, nx))
+    eps[:5] = 11.9
+    og = fit.Grid(nx, ny, nz, d0=25e-6, eps_r=eps.reshape(-1), pec_cell=pec, dt_frac=0.95)
+    lg = pe.Grid(nx, ny, nz, d0=25e-6, eps_r=eps.reshape(-1), pec_cell=pec, dt_frac=0.95)
+    src = [gauss_sine(2, port[0], port[1], k, f0=5e9, bw=10e9) for k in range(5)]
+    e, h = og.zeros()
+    ref = fit.leapfrog(og, e, h, 400, src)
+    ge, gh, _ = lib_leapfrog(lg, e, h, 400, src)
+    assert_parity((ge, gh), ref, "f64", "spiral leapfrog")
+    assert np.linalg.norm(ref[0]) > 0

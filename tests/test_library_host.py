@@ -1,0 +1,141 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/paraexp.h declares,
+and its host-side logic (partition, schedule, Leja nodes, Newton coefficients, theta_m,
+coefficient assembly, CFL, material-mode detection, argument validation) agrees with the
+oracle / the paper's worked examples.  No GPU compute is called."""
+import json
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1705_08019_b200 as pe
+from paper_1705_08019_b200 import abi
+from oracle import fit
+from synth import config_c1, config_c2, config_c3, layered_eps
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_values.json")))
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "paraexp.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|void|double|const char \*)\s*\**(paraexp_\w+)\s*\(",
+                              hdr, flags=re.M))
+    assert len(declared) >= 19
+    for name in declared:
+        assert hasattr(abi.lib, name), name
+    assert declared == set(abi.EXPORTED)
+
+
+def test_partition_and_schedule():
+    ex = GOLD["partition_example"]
+    b = pe.partition(ex["nsteps"], ex["p"])
+    assert [y - x for x, y in zip(b[:-1], b[1:])] == ex["steps"]
+    with pytest.raises(pe.ParaexpError):
+        pe.partition(3, 4)
+    for p in [1, 2, 3, 8, 16, 64]:
+        for world in [1, 2, 3, 4, 8]:
+            owned = []
+            roots = set()
+            for r in range(world):
+                f, l, root = pe.schedule(p, world, r)
+                owned += list(range(f, l + 1)) if f >= 1 else []
+                roots.add(root)
+                if f >= 1 and l == p:
+                    assert root == r
+            assert sorted(owned) == list(range(1, p + 1))   # every sub-interval exactly once
+            assert len(roots) == 1
+
+
+def test_leja_points_match_oracle():
+    assert pe.leja_points(101) == list(fit.leja_points(101))
+
+
+@pytest.mark.parametrize("m,theta", [(8, 3.0), (40, 30.0), (64, 55.0), (100, 90.0)])
+def test_newton_coefficients_match_oracle(m, theta):
+    """d-hat_k by the bidiagonal exponential (library) == mpmath divided differences (oracle)."""
+    p = pe.plan_host("leja", m, 1, 1e-12, theta, 1.0)
+    o = fit.make_plan("leja", m, 1, theta, 1.0)
+    assert p["gamma"] == o.gamma and p["a"] == o.a
+    d = np.array(p["d"])
+    do = np.array(o.d)
+    assert np.abs(d - do).max() <= 1e-15 * max(1.0, np.abs(do).max())
+
+
+def test_taylor_coefficients():
+    p = pe.plan_host("taylor", 24, 2, 1e-12, 1.0, 1.0)
+    assert all(abs(p["d"][k] - 1.0 / math.factorial(k)) <= 2.3e-16 / math.factorial(k) for k in range(25))
+    assert p["gamma"] == 1.0
+
+
+@pytest.mark.parametrize("method,m,tol", [("leja", 32, 1e-8), ("leja", 64, 1e-13), ("taylor", 24, 1e-10)])
+def test_theta_matches_oracle(method, m, tol):
+    assert abs(pe.theta(method, m, tol) - fit.theta_m(method, m, tol)) <= 1e-9 * fit.theta_m(method, m, tol)
+
+
+def test_theta_reference_table():
+    """Regression against the theta table of SURVEY 8(c) (parity unpinned, ~1%)."""
+    ref = {(16, 1e-2): 11.9, (64, 1e-8): 41.3, (100, 1e-13): 61.1, (48, 1e-8): 27.9}
+    for (m, tol), v in ref.items():
+        assert abs(pe.theta("leja", m, tol) / v - 1) < 0.01
+
+
+def test_auto_plan_minimises_cost():
+    tau, rho, tol = 1.0, 300.0, 1e-10
+    p = pe.plan_host("leja", 0, 0, tol, tau, rho)
+    best = min((mm * max(1, math.ceil(tau * rho / pe.theta("leja", mm, tol))), mm)
+               for mm in [8, 12, 16, 20, 24, 32, 40, 48, 56, 64, 72, 80, 88, 100])
+    assert p["m"] * p["s"] == best[0]
+
+
+@pytest.mark.parametrize("wl", ["c1", "c3small", "random", "pec"])
+def test_host_grid_coefficients_match_oracle(wl):
+    n = (8, 8, 8)
+    eps = pec = None
+    if wl == "c3small":
+        n = (12, 10, 16)
+        eps = layered_eps(*n)
+    elif wl == "random":
+        n = (9, 7, 6)
+        eps = np.random.default_rng(1).uniform(1, 4, np.prod(n))
+    elif wl == "pec":
+        n = (9, 7, 6)
+        pec = (np.random.default_rng(2).uniform(size=np.prod(n)) < 0.1).astype(np.uint8)
+    lg = pe.Grid(*n, d0=1e-3, eps_r=eps, pec_cell=pec, dt_frac=0.95, device=-1)
+    og = fit.Grid(*n, d0=1e-3, eps_r=eps, pec_cell=pec, dt_frac=0.95)
+    cE, cH = lg.coefficients()
+    assert np.array_equal(cE != 0, og.cE != 0) and np.array_equal(cH != 0, og.cH != 0)
+    np.testing.assert_allclose(cE, og.cE, rtol=1e-14, atol=0)
+    np.testing.assert_allclose(cH, og.cH, rtol=1e-14, atol=0)
+    assert abs(lg.dt_cfl - og.dt_cfl) <= 1e-15 * og.dt_cfl
+    mode = lg.info()["material_mode"]
+    assert mode == {"c1": abi.MAT_SCALAR, "c3small": abi.MAT_ZTABLE, "random": abi.MAT_ARRAY,
+                    "pec": abi.MAT_ARRAY}[wl]
+
+
+def test_config_material_modes():
+    for w, mode in [(config_c1(), abi.MAT_SCALAR), (config_c2(nsteps=10), abi.MAT_ARRAY),
+                    (config_c3(n=32), abi.MAT_ZTABLE)]:
+        lg = pe.Grid.from_workload(w, device=-1)
+        assert lg.info()["material_mode"] == mode
+
+
+def test_grid_validation_host():
+    for kw in [dict(nx=0), dict(eps_r=np.zeros(64)), dict(dt=1e-12), dict(dt_frac=0.0)]:
+        args = dict(nx=4, ny=4, nz=4, d0=1e-3, dt_frac=0.9, device=-1)
+        args.update(kw)
+        with pytest.raises(pe.ParaexpError) as ei:
+            pe.Grid(**args)
+        assert ei.value.code == pe.EINVAL
+    g = pe.Grid(4, 4, 4, d0=1e-3, dt_frac=1.2, device=-1)
+    assert g.warnings == abi.WCFL
+
+
+def test_host_only_grid_has_no_compute():
+    g = pe.Grid(4, 4, 4, d0=1e-3, dt_frac=0.9, device=-1)
+    st = abi.paraexp_stats()
+    rc = abi.lib.paraexp_leapfrog(g.handle, None, 0, 0.0, 1, abi.C.c_void_p(8), abi.C.c_void_p(8),
+                                  0, None, abi.C.byref(st))
+    assert rc == pe.ENOTSUP
