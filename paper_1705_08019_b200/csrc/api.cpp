@@ -30,6 +30,8 @@ static int ensure_ws(Grid &G, int n) {
         void *p = nullptr;
         int rc = dev_alloc(&p, bytes);
         if (rc) return rc;
+        // padding entries (i >= nx) are never written by the kernels: start from zero
+        if ((rc = dev_memset_async(p, 0, bytes, nullptr)) || (rc = dev_sync(nullptr))) return rc;
         G.ws.push_back(p);
         G.device_bytes += bytes;
         G.ws_bytes += bytes;
@@ -105,6 +107,7 @@ static int prepare_sources(Grid &G, const paraexp_source *src, int nsrc, double 
     if (rc) return rc;
     rc = dev_memcpy_h2d_async(G.d_src, sd.data(), sizeof(SrcDev) * nsrc, stream);
     if (rc) return rc;
+    G.h_src = sd;
     return dev_sync(stream);   // host staging buffers go out of scope
 }
 

@@ -26,6 +26,11 @@ struct Layout {
     int64_t state_elems() const { return 6 * cs; }
 };
 
+struct SrcDev {       // one source edge in device layout
+    int64_t off;      // element offset into the state vector (component + idx)
+    int32_t comp, i, j, k;
+};
+
 struct Grid {
     int nx, ny, nz;
     int dtype;          // PARAEXP_F64 / F32
@@ -52,6 +57,7 @@ struct Grid {
     void *d_flag = nullptr;     // int device flag (non-finite)
     void *d_red = nullptr;      // double reduction scratch
     void *d_src = nullptr;      // source descriptors
+    std::vector<SrcDev> h_src;  // host copy of the current source descriptors
     void *d_q = nullptr;        // source amplitude table
     int64_t d_q_cap = 0;
     int64_t device_bytes = 0;
@@ -84,10 +90,6 @@ double theta_m(int method, int m, double tol);
 void plan_to_info(const Plan &p, paraexp_plan_info *out);
 
 // ---- device entry points (kernels.cu) ----
-struct SrcDev {       // one source edge in device layout
-    int64_t off;      // element offset into the state vector (component + idx)
-    int32_t comp, i, j, k;
-};
 int dev_alloc(void **p, size_t bytes);
 void dev_free(void *p);
 int dev_memset_async(void *p, int v, size_t bytes, void *stream);

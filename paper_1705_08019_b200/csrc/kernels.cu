@@ -430,6 +430,20 @@ int k_poly_substep_unfused(const KernelArgs &ka, const Plan &plan, void *bufs[4]
     });
 }
 
+int zero_node_launch(const KernelArgs &ka, const Plan &plan, const void *w, void *wn, void *y,
+                     double c, int init, int do_w) {
+    return with_types(*ka.g, plan.sigma, [&](auto tT, auto tEM, auto tHA) {
+        using T = decltype(tT);
+        constexpr int EM = decltype(tEM)::value;
+        constexpr bool HA = decltype(tHA)::value;
+        zero_node_kernel<T, EM, HA><<<cell_grid(ka.g->L, false), kBlock, 0, (cudaStream_t)ka.stream>>>(
+            make_dev<T>(*ka.g), make_coef<T, EM, HA>(*ka.g, plan.sigma), (const T *)w, (T *)wn, (T *)y,
+            T(c), init, do_w);
+        ++*ka.launches;
+        return check_cuda("zero node");
+    });
+}
+
 int k_axpy(const KernelArgs &ka, void *x, const void *y, double alpha) {
     const int64_t n = ka.g->L.state_elems();
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);

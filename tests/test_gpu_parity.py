@@ -78,9 +78,10 @@ def test_leapfrog_ragged(dtype, kind, kernels):
 @pytest.mark.parametrize("method,m,s", [("leja", 40, 3), ("leja", 1, 7), ("leja", 2, 5),
                                          ("leja", 64, 1), ("taylor", 16, 6)])
 @pytest.mark.parametrize("kind", ["vacuum", "layered", "random"])
-def test_expmv_fixed_plan(dtype, method, m, s, kind):
+@pytest.mark.parametrize("kernels", KERNELS)
+def test_expmv_fixed_plan(dtype, method, m, s, kind, kernels):
     n = (21, 19, 13)
-    og, lg = _grids(n, kind, dtype, "auto")
+    og, lg = _grids(n, kind, dtype, kernels)
     e, h = inputs(og, *random_fields(*n, seed=7))
     rho = og.rho_cfl
     tau = 30 * og.dt if method == "leja" else 6 * og.dt
@@ -127,9 +128,10 @@ def test_solve_c1():
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("p", [1, 3, 4])
-def test_solve_random_u0(dtype, p):
+@pytest.mark.parametrize("kernels", KERNELS)
+def test_solve_random_u0(dtype, p, kernels):
     n = (19, 17, 9)
-    og, lg = _grids(n, "random", dtype, "auto")
+    og, lg = _grids(n, "random", dtype, kernels)
     u0 = inputs(og, *random_fields(*n, seed=77))
     src = _sources(og, n)
     nsteps = 61
