@@ -574,6 +574,45 @@ def paraexp(g: Grid, sources, t0: float, nsteps: int, p: int, plan_for, u0=None,
     return e_p + We, h_p + Wh_half
 
 
+def paraexp_block(g: Grid, sources, t0: float, nsteps: int, p: int, plan_for, first: int,
+                  last: int, u0=None, mode: str = "pairs", dtype: Optional[str] = None):
+    """One worker's share of Algorithm 1's parfor for the contiguous block of
+    sub-intervals [first, last] (1-based; first = 0 => none): its tails carried to T_p,
+        W_r = sum_{j in block, j < p} E_p..E_{j+1} s_j  (+ E_p..E_1 u0 if first == 1),
+    and, if it owns p, the particular state (e_p, h_p).  The sum over workers of W_r is the
+    W of paraexp() (superposition; SURVEY finding 9)."""
+    dtype = dtype or g.dtype
+    S = partition(nsteps, p)
+    We = Wh = None
+    P = None
+    if first >= 1:
+        if first == 1 and u0 is not None:
+            We, Wh = g.clean(*u0)
+        for i in range(first, last + 1):
+            z_e, z_h = g.zeros()
+            ei, hi = leapfrog(g, z_e, z_h, S[i] - S[i - 1], sources, t0, S[i - 1])
+            if We is not None:
+                We, Wh = expmv(g, plan_for((S[i] - S[i - 1]) * g.dt), We, Wh, mode, dtype)
+            if i < p:
+                se, sh = ei, sync_h(g, ei, hi)
+                We, Wh = (se.copy(), sh.copy()) if We is None else (We + se, Wh + sh)
+            else:
+                P = (ei, hi)
+        for i in range(last + 1, p + 1):
+            if We is not None:
+                We, Wh = expmv(g, plan_for((S[i] - S[i - 1]) * g.dt), We, Wh, mode, dtype)
+    if We is None:
+        We, Wh = g.zeros()
+    return (We, Wh), P
+
+
+def paraexp_finish(g: Grid, P, W, rho, mode: str = "pairs", dtype: Optional[str] = None):
+    """Reconstruction on the owner of sub-interval p (eq:averaging1/2, reading 10)."""
+    dtype = dtype or g.dtype
+    _, Wh_half = expmv(g, half_step_plan(g, rho), W[0], W[1], mode, dtype)
+    return P[0] + W[0], P[1] + Wh_half
+
+
 def cost_proc(nt: int, p: int, n_leja: int) -> float:
     """eq:tot_cost, PAPER:474-477: C_proc = (2/p) n_t + n_Leja + 2."""
     return 2.0 * nt / p + n_leja + 2

@@ -73,7 +73,7 @@ __device__ __forceinline__ void fence_barrier_init() {
 template <typename T, int BX_, int BY_>
 struct Geo {
     static constexpr int BX = BX_, BY = BY_;
-    static constexpr int NT = BX * BY;
+    static constexpr int NT = BX * BY;                              // tile points (phase B)
     static constexpr int VEC = 16 / (int)sizeof(T);
     static constexpr int OX = VEC;                                  // tile origin inside the box (the TMA x start must be 16 B aligned)
     static constexpr int WX = ((OX + BX + 1 + VEC - 1) / VEC) * VEC; // TMA box width (16 B multiple)
@@ -81,6 +81,7 @@ struct Geo {
     static constexpr int PL = WX * HY;                              // one component of a stage
     static constexpr int EX = BX + 1, EY = BY + 1;                 // halo-extended ring plane
     static constexpr int RP = EX * EY;                              // one component of a ring plane
+    static constexpr int NTHR = ((RP + 31) / 32) * 32;               // threads: phase A in one pass
 };
 
 struct Sched {
@@ -162,7 +163,7 @@ __device__ __forceinline__ void curl_stage(const T *E0, const T *E1, int s, T &c
 // K1: fused leapfrog step
 // ---------------------------------------------------------------------------------------
 template <typename T, int EM, bool HA, int BX, int BY, int S>
-__global__ void __launch_bounds__(BX *BY) leapfrog_fused_kernel(
+__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ out,
     Sched sch, SrcList src, const T *__restrict__ q) {
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(BX *BY) leapfrog_fused_kernel(
             T *R1 = ring + ((k + 1) & 1) * 3 * G::RP;
             const int kk = k + 1;
             // ---- e'(k+1) on the tile and its +1 halo ----
-            for (int q2 = tid; q2 < G::RP; q2 += G::NT) {
+            for (int q2 = tid; q2 < G::RP; q2 += G::NTHR) {
                 const int ii = q2 % G::EX, jj = q2 / G::EX;
                 const int i = x0 + ii, j = y0 + jj;
                 const int s = (jj + 1) * G::WX + (ii + G::OX);
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(BX *BY) leapfrog_fused_kernel(
             }
             __syncthreads();
             // ---- h'(k) on the tile ----
-            if (k >= kb) {
+            if (k >= kb && tid < G::NT) {
                 const T *R0 = ring + (k & 1) * 3 * G::RP;
                 const int i = x0 + tx, j = y0 + ty;
                 const int r = ty * G::EX + tx;
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(BX *BY) leapfrog_fused_kernel(
 // K2: fused Newton pair  u = X w ; y <- (init?0:y) + a w + b u ; [w' = X u + e2 w]
 // ---------------------------------------------------------------------------------------
 template <typename T, int EM, bool HA, int BX, int BY, int S>
-__global__ void __launch_bounds__(BX *BY) pair_fused_kernel(
+__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
     T *__restrict__ y, Sched sch, T a, T b, T e2, int init, int do_w) {
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(BX *BY) pair_fused_kernel(
                                           &tm_cH, x0, y0, kb - 1 + p);
             }
         const int i_own = x0 + tx, j_own = y0 + ty;
-        const bool own_in = i_own < D.nx && j_own < D.ny;
+        const bool own_in = tid < G::NT && i_own < D.nx && j_own < D.ny;
         for (int p = 0; p + 1 < nplanes; ++p) {
             const int k = kb - 1 + p;
             const uint32_t L0 = lcount + p, L1 = L0 + 1;
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(BX *BY) pair_fused_kernel(
             T *UE1 = UE + ((k + 1) & 1) * 3 * G::RP;         // u_e(k+1)
             T *UH0 = UH + (k & 1) * 3 * G::RP;               // u_h(k)
             const int kk = k + 1;
-            for (int q2 = tid; q2 < G::RP; q2 += G::NT) {
+            for (int q2 = tid; q2 < G::RP; q2 += G::NTHR) {
                 const int ii = q2 % G::EX, jj = q2 / G::EX;
                 // u_e(k+1) at (x0+ii, y0+jj)
                 {
@@ -485,6 +486,7 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
             bc = ch;
         }
     }
+    if (const char *ev = getenv("PARAEXP_ZCHUNK")) bc = std::max(1, std::min(g.nz, atoi(ev)));
     s.chunk = bc;
     s.nchunks = (g.nz + bc - 1) / bc;
     s.units = s.ntiles * s.nchunks;
@@ -513,7 +515,7 @@ static int leapfrog_fused_T(const KernelArgs &ka, void *bufs[2], int64_t nsteps,
         attr_set = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BX * BY, Cfg::lf_smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::NTHR, Cfg::lf_smem);
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "fused leapfrog kernel does not fit on an SM");
     const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
     const int grid = std::min(sch.units, per_sm * num_sms());
@@ -536,7 +538,7 @@ static int leapfrog_fused_T(const KernelArgs &ka, void *bufs[2], int64_t nsteps,
     cudaStream_t s = (cudaStream_t)ka.stream;
     for (int64_t m = 0; m < nsteps; ++m) {
         const bool even = (m % 2) == 0;
-        kern<<<grid, BX * BY, Cfg::lf_smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf,
+        kern<<<grid, G::NTHR, Cfg::lf_smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf,
                                                  (T *)(even ? bufs[1] : bufs[0]), sch, sl,
                                                  nsrc ? (const T *)q_dev + m * nsrc : nullptr);
         ++*ka.launches;
@@ -573,7 +575,7 @@ static int poly_fused_T(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
         attr_set = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BX * BY, Cfg::pair_smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::NTHR, Cfg::pair_smem);
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "fused pair kernel does not fit on an SM");
     const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
     const int grid = std::min(sch.units, per_sm * num_sms());
@@ -591,7 +593,7 @@ static int poly_fused_T(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
             CUtensorMap tmW;
             if ((rc = make_map<T>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
             const int do_w = op.kind == 0;
-            kern<<<grid, BX * BY, Cfg::pair_smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, sch, T(op.a), T(op.b),
+            kern<<<grid, G::NTHR, Cfg::pair_smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, sch, T(op.a), T(op.b),
                                                        T(op.e2), init, do_w);
             ++*ka.launches;
             if (do_w) std::swap(w, sp);
