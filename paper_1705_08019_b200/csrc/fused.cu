@@ -162,19 +162,39 @@ __device__ __forceinline__ void curl_stage(const T *E0, const T *E1, int s, T &c
 // ---------------------------------------------------------------------------------------
 // K1: fused leapfrog step
 // ---------------------------------------------------------------------------------------
-template <typename T, int EM, bool HA, int BX, int BY, int S>
+// Per-CTA pipeline (S stages).  Iteration p works on planes k = kb-1+p and k+1:
+//   phase A: e'(k+1) on the tile + halo  -> ring slot (k+1) % NR (and global for tile points)
+//   barrier
+//   phase B: h'(k) on the tile           -> global
+//   [barrier]  refill
+// ONEBAR = false: two barriers per plane, ring depth 2, the slot of plane k is refilled at the
+//   end of iteration k.
+// ONEBAR = true: one barrier per plane, ring depth 3, the slot of plane k-1 is refilled right
+//   after the barrier of iteration k (every warp has then left phase B of iteration k-1).
+template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
 __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ out,
     Sched sch, SrcList src, const T *__restrict__ q) {
     using G = Geo<T, BX, BY>;
-    constexpr int NC = NComp<T, EM, HA>::value;
+    using SL = StageL<T, EM, HA, G>;
+    constexpr int NR = ONEBAR ? 3 : 2;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *stages = reinterpret_cast<T *>(smem_raw);
-    T *ring = stages + S * StageL<T, EM, HA, G>::SZ;                   // [2][3][EY][EX] e' planes
-    uint64_t *bars = reinterpret_cast<uint64_t *>(ring + 2 * 3 * G::RP);
+    T *ring = stages + S * SL::SZ;                       // [NR][3][EY][EX] e' planes
+    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(ring + NR * 3 * G::RP) + 15) & ~uintptr_t(15));
     const int tid = threadIdx.x;
+    // phase-A point (tile + halo) and phase-B point (tile) of this thread
+    const bool hasA = tid < G::RP;
+    const int ii = tid % G::EX, jj = tid / G::EX;
+    const int sA = (jj + 1) * G::WX + ii + G::OX;
+    const bool tileA = ii < BX && jj < BY;
+    const bool hasB = tid < G::NT;
     const int tx = tid % BX, ty = tid / BX;
+    const int rB = ty * G::EX + tx;
+    const int sB = (ty + 1) * G::WX + tx + G::OX;
+    T bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
+    const T bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_barrier_init();
@@ -186,87 +206,111 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
         const int nplanes = ke - kb + 2;                 // planes kb-1 .. ke
+        const int iA = x0 + ii, jA = y0 + jj;
+        const bool inA = hasA && iA < D.nx && jA < D.ny;
+        const bool lxA = inA && jA > 0, lyA = inA && iA > 0, lzA = inA && iA > 0 && jA > 0;
+        const bool wrA = inA && tileA;
+        uint32_t smask = 0;
+        for (int r = 0; r < src.n; ++r)
+            if (inA && src.i[r] == iA && src.j[r] == jA) smask |= 1u << r;
+        T *oA = out + D.idx(wrA ? iA : 0, wrA ? jA : 0, 0);
+        const int iB = x0 + tx, jB = y0 + ty;
+        const bool inB = hasB && iB < D.nx && jB < D.ny;
+        const bool lxB = iB > 0, lyB = jB > 0;
+        T *oB = out + D.idx(inB ? iB : 0, inB ? jB : 0, 0) + 3 * D.cs;
         if (tid == 0)
             for (int p = 0; p < min(S, nplanes); ++p) {
                 const uint32_t L = lcount + p;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * StageL<T, EM, HA, G>::SZ, &bars[L % S], &tm_state, &tm_cE,
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
                                           &tm_cH, x0, y0, kb - 1 + p);
             }
         for (int p = 0; p + 1 < nplanes; ++p) {         // iteration on planes k = kb-1+p, k+1
-            const int k = kb - 1 + p;
+            const int k = kb - 1 + p, kk = k + 1;
             const uint32_t L0 = lcount + p, L1 = L0 + 1;
             if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
             mbar_wait(&bars[L1 % S], (L1 / S) & 1);
-            const T *P0 = stages + (L0 % S) * StageL<T, EM, HA, G>::SZ;   // plane k
-            const T *P1 = stages + (L1 % S) * StageL<T, EM, HA, G>::SZ;   // plane k+1
-            T *R1 = ring + ((k + 1) & 1) * 3 * G::RP;
-            const int kk = k + 1;
-            // ---- e'(k+1) on the tile and its +1 halo ----
-            for (int q2 = tid; q2 < G::RP; q2 += G::NTHR) {
-                const int ii = q2 % G::EX, jj = q2 / G::EX;
-                const int i = x0 + ii, j = y0 + jj;
-                const int s = (jj + 1) * G::WX + (ii + G::OX);
+            const T *P0 = stages + (L0 % S) * SL::SZ;    // plane k
+            const T *P1 = stages + (L1 % S) * SL::SZ;    // plane k+1
+            T *R1 = ring + (kk % NR) * 3 * G::RP;
+            if (EM == 1 && kk < D.nz) {
+                bE0 = __ldg(cf.tab + kk) * cf.sig;
+                bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
+                bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
+            }
+            // ---- phase A: e'(k+1) on the tile and its +1 halo ----
+            if (hasA) {
                 T c0, c1, c2;
-                curlT_stage<T, G>(P1, P0, s, c0, c1, c2);
-                const bool valid = i < D.nx && j < D.ny && kk < D.nz && kk >= 0;
-                T en[3];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const T cc = c == 0 ? c0 : (c == 1 ? c1 : c2);
-                    en[c] = (valid && D.e_live(c, i, j, kk))
-                                ? P1[c * G::PL + s] + stage_bE<T, EM, HA, G>(cf, P1, c, kk, s) * cc
-                                : T(0);
+                curlT_stage<T, G>(P1, P0, sA, c0, c1, c2);
+                const bool vk = kk < D.nz, kp = kk > 0;
+                T e0, e1, e2;
+                if (EM == 2) {
+                    e0 = (lxA && vk && kp) ? P1[sA] + (P1[SL::ST + sA] * cf.sig) * c0 : T(0);
+                    e1 = (lyA && vk && kp) ? P1[G::PL + sA] + (P1[SL::ST + G::PL + sA] * cf.sig) * c1 : T(0);
+                    e2 = (lzA && vk) ? P1[2 * G::PL + sA] + (P1[SL::ST + 2 * G::PL + sA] * cf.sig) * c2 : T(0);
+                } else {
+                    e0 = (lxA && vk && kp) ? P1[sA] + bE0 * c0 : T(0);
+                    e1 = (lyA && vk && kp) ? P1[G::PL + sA] + bE1 * c1 : T(0);
+                    e2 = (lzA && vk) ? P1[2 * G::PL + sA] + bE2 * c2 : T(0);
                 }
-                if (valid)
+                if (smask && vk)
                     for (int r = 0; r < src.n; ++r)
-                        if (src.k[r] == kk && src.i[r] == i && src.j[r] == j) {
+                        if (((smask >> r) & 1u) && src.k[r] == kk) {
                             const int sc = src.c[r];
                             const T qv = q[r];
-                            if (sc == 0) en[0] = en[0] - qv;
-                            if (sc == 1) en[1] = en[1] - qv;
-                            if (sc == 2) en[2] = en[2] - qv;
+                            if (sc == 0) e0 = e0 - qv;
+                            if (sc == 1) e1 = e1 - qv;
+                            if (sc == 2) e2 = e2 - qv;
                         }
-#pragma unroll
-                for (int c = 0; c < 3; ++c) R1[c * G::RP + q2] = en[c];
-                if (ii < BX && jj < BY && valid && kk >= kb && kk < ke) {
-                    const int64_t gi = D.idx(i, j, kk);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) out[c * D.cs + gi] = en[c];
+                R1[tid] = e0;
+                R1[G::RP + tid] = e1;
+                R1[2 * G::RP + tid] = e2;
+                if (wrA && vk && kk >= kb && kk < ke) {
+                    T *o = oA + (int64_t)kk * D.plane;
+                    o[0] = e0;
+                    o[D.cs] = e1;
+                    o[2 * D.cs] = e2;
                 }
             }
             __syncthreads();
-            // ---- h'(k) on the tile ----
-            if (k >= kb && tid < G::NT) {
-                const T *R0 = ring + (k & 1) * 3 * G::RP;
-                const int i = x0 + tx, j = y0 + ty;
-                const int r = ty * G::EX + tx;
-                const T ex0 = R0[r], ey0 = R0[G::RP + r], ez0 = R0[2 * G::RP + r];
-                const T ez_jp = R0[2 * G::RP + r + G::EX], ex_jp = R0[r + G::EX];
-                const T ez_ip = R0[2 * G::RP + r + 1], ey_ip = R0[G::RP + r + 1];
-                const T ex_kp = R1[r], ey_kp = R1[G::RP + r];
+            if (ONEBAR && tid == 0 && p >= 1 && p - 1 + S < nplanes) {
+                const uint32_t L = lcount + p - 1 + S;
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                          &tm_cH, x0, y0, kb - 1 + p - 1 + S);
+            }
+            // ---- phase B: h'(k) on the tile ----
+            if (k >= kb && inB) {
+                const T *R0 = ring + (k % NR) * 3 * G::RP;
+                const T ex0 = R0[rB], ey0 = R0[G::RP + rB], ez0 = R0[2 * G::RP + rB];
+                const T ez_jp = R0[2 * G::RP + rB + G::EX], ex_jp = R0[rB + G::EX];
+                const T ez_ip = R0[2 * G::RP + rB + 1], ey_ip = R0[G::RP + rB + 1];
+                const T ex_kp = R1[rB], ey_kp = R1[G::RP + rB];
                 const T c0 = ((ey0 + ez_jp) - ey_kp) - ez0;
                 const T c1 = ((ez0 + ex_kp) - ez_ip) - ex0;
                 const T c2 = ((ex0 + ey_ip) - ex_jp) - ey0;
-                const int s = (ty + 1) * G::WX + (tx + G::OX);
-                if (i < D.nx && j < D.ny) {
-                    const int64_t gi = D.idx(i, j, k);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const T cc = c == 0 ? c0 : (c == 1 ? c1 : c2);
-                        const T hv = P0[(3 + c) * G::PL + s];
-                        out[(3 + c) * D.cs + gi] =
-                            D.h_live(c, i, j, k) ? hv - stage_bH<T, EM, HA, G>(cf, P0, c, s) * cc : hv;
-                    }
+                const T hx = P0[3 * G::PL + sB], hy = P0[4 * G::PL + sB], hz = P0[5 * G::PL + sB];
+                T *o = oB + (int64_t)k * D.plane;
+                if (HA) {
+                    const int ch = SL::ST + SL::CE;
+                    o[0] = lxB ? hx - (P0[ch + sB] * cf.sig) * c0 : hx;
+                    o[D.cs] = lyB ? hy - (P0[ch + G::PL + sB] * cf.sig) * c1 : hy;
+                    o[2 * D.cs] = k > 0 ? hz - (P0[ch + 2 * G::PL + sB] * cf.sig) * c2 : hz;
+                } else {
+                    o[0] = lxB ? hx - bH0 * c0 : hx;
+                    o[D.cs] = lyB ? hy - bH1 * c1 : hy;
+                    o[2 * D.cs] = k > 0 ? hz - bH2 * c2 : hz;
                 }
             }
-            __syncthreads();
-            // plane k is consumed: refill its slot with plane k + S
-            if (tid == 0 && p + S < nplanes) {
-                const uint32_t L = lcount + p + S;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * StageL<T, EM, HA, G>::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                          &tm_cH, x0, y0, kb - 1 + p + S);
+            if (!ONEBAR) {
+                __syncthreads();
+                // plane k is consumed: refill its slot with plane k + S
+                if (tid == 0 && p + S < nplanes) {
+                    const uint32_t L = lcount + p + S;
+                    issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                              &tm_cH, x0, y0, kb - 1 + p + S);
+                }
             }
         }
+        if (ONEBAR) __syncthreads();
         lcount += nplanes;
     }
 }
@@ -274,20 +318,33 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
 // ---------------------------------------------------------------------------------------
 // K2: fused Newton pair  u = X w ; y <- (init?0:y) + a w + b u ; [w' = X u + e2 w]
 // ---------------------------------------------------------------------------------------
-template <typename T, int EM, bool HA, int BX, int BY, int S>
+// Phase A of iteration k: u_e(k+1) on the +1 halo and u_h(k) on the -1 halo; phase B: the
+// tile's w'(k) and y(k).  Ring depth 2 (two barriers per plane) or 3 (ONEBAR).
+template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
 __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
     T *__restrict__ y, Sched sch, T a, T b, T e2, int init, int do_w) {
     using G = Geo<T, BX, BY>;
-    constexpr int NC = NComp<T, EM, HA>::value;
+    using SL = StageL<T, EM, HA, G>;
+    constexpr int NR = ONEBAR ? 3 : 2;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *stages = reinterpret_cast<T *>(smem_raw);
-    T *UE = stages + S * StageL<T, EM, HA, G>::SZ;                    // [2][3][EY][EX]: u_e at (ii, jj) in [0,BX]x[0,BY]
-    T *UH = UE + 2 * 3 * G::RP;                         // [2][3][EY][EX]: u_h at (ii-1, jj-1)
-    uint64_t *bars = reinterpret_cast<uint64_t *>(UH + 2 * 3 * G::RP);
+    T *UE = stages + S * SL::SZ;                         // [NR][3][EY][EX]: u_e at (ii, jj)
+    T *UH = UE + NR * 3 * G::RP;                         // [NR][3][EY][EX]: u_h at (ii-1, jj-1)
+    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(UH + NR * 3 * G::RP) + 15) & ~uintptr_t(15));
     const int tid = threadIdx.x;
+    const bool hasA = tid < G::RP;
+    const int ii = tid % G::EX, jj = tid / G::EX;
+    const int sE = (jj + 1) * G::WX + ii + G::OX;         // stage index of the u_e point
+    const int sH = jj * G::WX + ii - 1 + G::OX;           // stage index of the u_h point
+    const bool hasB = tid < G::NT;
     const int tx = tid % BX, ty = tid / BX;
+    const int re = ty * G::EX + tx;                       // u_e ring index of the own point
+    const int rh = (ty + 1) * G::EX + (tx + 1);           // u_h ring index of the own point
+    const int sB = (ty + 1) * G::WX + tx + G::OX;         // stage index of the own point
+    T bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
+    const T bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_barrier_init();
@@ -299,81 +356,116 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
         const int nplanes = ke - kb + 2;
+        // phase-A validity (k-independent parts)
+        const int iE = x0 + ii, jE = y0 + jj;             // u_e point
+        const bool inE = hasA && iE < D.nx && jE < D.ny;
+        const bool lxE = inE && jE > 0, lyE = inE && iE > 0, lzE = inE && iE > 0 && jE > 0;
+        const int iH = iE - 1, jH = jE - 1;               // u_h point
+        const bool inH = hasA && iH >= 0 && jH >= 0 && iH < D.nx && jH < D.ny;
+        const bool lxH = inH && iH > 0, lyH = inH && jH > 0;
+        // own point
+        const int iB = x0 + tx, jB = y0 + ty;
+        const bool inB = hasB && iB < D.nx && jB < D.ny;
+        const bool lxBe = jB > 0, lyBe = iB > 0, lzBe = iB > 0 && jB > 0;
+        const bool lxBh = iB > 0, lyBh = jB > 0;
+        const int64_t gB = D.idx(inB ? iB : 0, inB ? jB : 0, 0);
         if (tid == 0)
             for (int p = 0; p < min(S, nplanes); ++p) {
                 const uint32_t L = lcount + p;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * StageL<T, EM, HA, G>::SZ, &bars[L % S], &tm_state, &tm_cE,
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
                                           &tm_cH, x0, y0, kb - 1 + p);
             }
-        const int i_own = x0 + tx, j_own = y0 + ty;
-        const bool own_in = tid < G::NT && i_own < D.nx && j_own < D.ny;
         for (int p = 0; p + 1 < nplanes; ++p) {
-            const int k = kb - 1 + p;
+            const int k = kb - 1 + p, kk = k + 1;
             const uint32_t L0 = lcount + p, L1 = L0 + 1;
+            const bool doB = k >= kb && inB;
             // prefetch y(k) for the own point (consumed after the halo phase)
-            T yv[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
-            if (k >= kb && own_in && !init) {
-                const int64_t gi = D.idx(i_own, j_own, k);
-#pragma unroll
-                for (int c = 0; c < 6; ++c) yv[c] = y[c * D.cs + gi];
+            T yv0 = T(0), yv1 = T(0), yv2 = T(0), yv3 = T(0), yv4 = T(0), yv5 = T(0);
+            if (doB && !init) {
+                const T *yp = y + gB + (int64_t)k * D.plane;
+                yv0 = yp[0];
+                yv1 = yp[D.cs];
+                yv2 = yp[2 * D.cs];
+                yv3 = yp[3 * D.cs];
+                yv4 = yp[4 * D.cs];
+                yv5 = yp[5 * D.cs];
             }
             if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
             mbar_wait(&bars[L1 % S], (L1 / S) & 1);
-            const T *P0 = stages + (L0 % S) * StageL<T, EM, HA, G>::SZ;   // w plane k
-            const T *P1 = stages + (L1 % S) * StageL<T, EM, HA, G>::SZ;   // w plane k+1
-            T *UE1 = UE + ((k + 1) & 1) * 3 * G::RP;         // u_e(k+1)
-            T *UH0 = UH + (k & 1) * 3 * G::RP;               // u_h(k)
-            const int kk = k + 1;
-            for (int q2 = tid; q2 < G::RP; q2 += G::NTHR) {
-                const int ii = q2 % G::EX, jj = q2 / G::EX;
-                // u_e(k+1) at (x0+ii, y0+jj)
-                {
-                    const int i = x0 + ii, j = y0 + jj;
-                    const int s = (jj + 1) * G::WX + (ii + G::OX);
-                    T c0, c1, c2;
-                    curlT_stage<T, G>(P1, P0, s, c0, c1, c2);
-                    const bool valid = i < D.nx && j < D.ny && kk < D.nz;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const T cc = c == 0 ? c0 : (c == 1 ? c1 : c2);
-                        UE1[c * G::RP + q2] = (valid && D.e_live(c, i, j, kk))
-                                                  ? stage_bE<T, EM, HA, G>(cf, P1, c, kk, s) * cc
-                                                  : T(0);
-                    }
+            const T *P0 = stages + (L0 % S) * SL::SZ;    // w plane k
+            const T *P1 = stages + (L1 % S) * SL::SZ;    // w plane k+1
+            T *UE1 = UE + (kk % NR) * 3 * G::RP;           // u_e(k+1)
+            T *UH0 = UH + ((k + NR) % NR) * 3 * G::RP;    // u_h(k)
+            T bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;         // coefficients at plane k (phase B)
+            if (EM == 1) {
+                if (kk < D.nz) {
+                    bE0 = __ldg(cf.tab + kk) * cf.sig;
+                    bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
+                    bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
                 }
-                // u_h(k) at (x0+ii-1, y0+jj-1)
+                if (k >= 0) {
+                    bEk0 = __ldg(cf.tab + k) * cf.sig;
+                    bEk1 = __ldg(cf.tab + D.nz + k) * cf.sig;
+                    bEk2 = __ldg(cf.tab + 2 * D.nz + k) * cf.sig;
+                }
+            }
+            if (hasA) {
+                // u_e(k+1) = bE .* C^T w_h
                 {
-                    const int i = x0 + ii - 1, j = y0 + jj - 1;
-                    const int s = jj * G::WX + (ii - 1 + G::OX);
                     T c0, c1, c2;
-                    curl_stage<T, G>(P0, P1, s, c0, c1, c2);
-                    const bool valid = i >= 0 && j >= 0 && i < D.nx && j < D.ny && k >= 0 && k < D.nz;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const T cc = c == 0 ? c0 : (c == 1 ? c1 : c2);
-                        UH0[c * G::RP + q2] = (valid && D.h_live(c, i, j, k))
-                                                  ? -(stage_bH<T, EM, HA, G>(cf, P0, c, s) * cc)
-                                                  : T(0);
+                    curlT_stage<T, G>(P1, P0, sE, c0, c1, c2);
+                    const bool vk = kk < D.nz, kp = kk > 0;
+                    T u0, u1, u2;
+                    if (EM == 2) {
+                        u0 = (lxE && vk && kp) ? (P1[SL::ST + sE] * cf.sig) * c0 : T(0);
+                        u1 = (lyE && vk && kp) ? (P1[SL::ST + G::PL + sE] * cf.sig) * c1 : T(0);
+                        u2 = (lzE && vk) ? (P1[SL::ST + 2 * G::PL + sE] * cf.sig) * c2 : T(0);
+                    } else {
+                        u0 = (lxE && vk && kp) ? bE0 * c0 : T(0);
+                        u1 = (lyE && vk && kp) ? bE1 * c1 : T(0);
+                        u2 = (lzE && vk) ? bE2 * c2 : T(0);
                     }
+                    UE1[tid] = u0;
+                    UE1[G::RP + tid] = u1;
+                    UE1[2 * G::RP + tid] = u2;
+                }
+                // u_h(k) = -bH .* C w_e
+                {
+                    T c0, c1, c2;
+                    curl_stage<T, G>(P0, P1, sH, c0, c1, c2);
+                    const bool vk = k >= 0 && k < D.nz;
+                    T u0, u1, u2;
+                    if (HA) {
+                        const int ch = SL::ST + SL::CE;
+                        u0 = (lxH && vk) ? -((P0[ch + sH] * cf.sig) * c0) : T(0);
+                        u1 = (lyH && vk) ? -((P0[ch + G::PL + sH] * cf.sig) * c1) : T(0);
+                        u2 = (inH && vk && k > 0) ? -((P0[ch + 2 * G::PL + sH] * cf.sig) * c2) : T(0);
+                    } else {
+                        u0 = (lxH && vk) ? -(bH0 * c0) : T(0);
+                        u1 = (lyH && vk) ? -(bH1 * c1) : T(0);
+                        u2 = (inH && vk && k > 0) ? -(bH2 * c2) : T(0);
+                    }
+                    UH0[tid] = u0;
+                    UH0[G::RP + tid] = u1;
+                    UH0[2 * G::RP + tid] = u2;
                 }
             }
             __syncthreads();
-            if (k >= kb && own_in) {
-                const T *UE0 = UE + (k & 1) * 3 * G::RP;     // u_e(k)
-                const T *UHm = UH + ((k - 1) & 1) * 3 * G::RP; // u_h(k-1)
-                const int re = ty * G::EX + tx;              // u_e ring index of the own point
-                const int rh = (ty + 1) * G::EX + (tx + 1);  // u_h ring index of the own point
-                const int s = (ty + 1) * G::WX + (tx + G::OX);   // stage index of the own point
-                const int64_t gi = D.idx(i_own, j_own, k);
-                T un[6], wn[6];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    un[c] = UE0[c * G::RP + re];
-                    un[3 + c] = UH0[c * G::RP + rh];
-                }
+            if (ONEBAR && tid == 0 && p >= 1 && p - 1 + S < nplanes) {
+                const uint32_t L = lcount + p - 1 + S;
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                          &tm_cH, x0, y0, kb - 1 + p - 1 + S);
+            }
+            if (doB) {
+                const T *UE0 = UE + (k % NR) * 3 * G::RP;        // u_e(k)
+                const T *UHm = UH + ((k - 1 + NR) % NR) * 3 * G::RP; // u_h(k-1)
+                const T ux0 = UE0[re], uy0 = UE0[G::RP + re], uz0 = UE0[2 * G::RP + re];
+                const T hx0 = UH0[rh], hy0 = UH0[G::RP + rh], hz0 = UH0[2 * G::RP + rh];
+                const T w0 = P0[sB], w1 = P0[G::PL + sB], w2 = P0[2 * G::PL + sB];
+                const T w3 = P0[3 * G::PL + sB], w4 = P0[4 * G::PL + sB], w5 = P0[5 * G::PL + sB];
+                const int64_t go = gB + (int64_t)k * D.plane;
                 if (do_w) {
                     // w'_h(k) = -bH C u_e + e2 w_h
-                    const T ux0 = un[0], uy0 = un[1], uz0 = un[2];
                     const T uz_jp = UE0[2 * G::RP + re + G::EX], ux_jp = UE0[re + G::EX];
                     const T uz_ip = UE0[2 * G::RP + re + 1], uy_ip = UE0[G::RP + re + 1];
                     const T ux_kp = UE1[re], uy_kp = UE1[G::RP + re];
@@ -381,35 +473,51 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
                     const T c1 = ((uz0 + ux_kp) - uz_ip) - ux0;
                     const T c2 = ((ux0 + uy_ip) - ux_jp) - uy0;
                     // w'_e(k) = bE C^T u_h + e2 w_e
-                    const T hx0 = un[3], hy0 = un[4], hz0 = un[5];
                     const T hz_jm = UH0[2 * G::RP + rh - G::EX], hx_jm = UH0[rh - G::EX];
                     const T hz_im = UH0[2 * G::RP + rh - 1], hy_im = UH0[G::RP + rh - 1];
                     const T hy_km = UHm[G::RP + rh], hx_km = UHm[rh];
                     const T d0 = ((hz0 - hz_jm) - hy0) + hy_km;
                     const T d1 = ((hx0 - hx_km) - hz0) + hz_im;
                     const T d2 = ((hy0 - hy_im) - hx0) + hx_jm;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const T ce = c == 0 ? d0 : (c == 1 ? d1 : d2);
-                        const T ch = c == 0 ? c0 : (c == 1 ? c1 : c2);
-                        const T xe = D.e_live(c, i_own, j_own, k) ? stage_bE<T, EM, HA, G>(cf, P0, c, k, s) * ce : T(0);
-                        const T xh = D.h_live(c, i_own, j_own, k) ? -(stage_bH<T, EM, HA, G>(cf, P0, c, s) * ch) : T(0);
-                        wn[c] = xe + e2 * P0[c * G::PL + s];
-                        wn[3 + c] = xh + e2 * P0[(3 + c) * G::PL + s];
+                    T be0 = bEk0, be1 = bEk1, be2 = bEk2, bh0 = bH0, bh1 = bH1, bh2 = bH2;
+                    if (EM == 2) {
+                        be0 = P0[SL::ST + sB] * cf.sig;
+                        be1 = P0[SL::ST + G::PL + sB] * cf.sig;
+                        be2 = P0[SL::ST + 2 * G::PL + sB] * cf.sig;
                     }
-#pragma unroll
-                    for (int c = 0; c < 6; ++c) wout[c * D.cs + gi] = wn[c];
+                    if (HA) {
+                        const int ch = SL::ST + SL::CE;
+                        bh0 = P0[ch + sB] * cf.sig;
+                        bh1 = P0[ch + G::PL + sB] * cf.sig;
+                        bh2 = P0[ch + 2 * G::PL + sB] * cf.sig;
+                    }
+                    const bool kp = k > 0;
+                    T *wo = wout + go;
+                    wo[0] = ((lxBe && kp) ? be0 * d0 : T(0)) + e2 * w0;
+                    wo[D.cs] = ((lyBe && kp) ? be1 * d1 : T(0)) + e2 * w1;
+                    wo[2 * D.cs] = (lzBe ? be2 * d2 : T(0)) + e2 * w2;
+                    wo[3 * D.cs] = (lxBh ? -(bh0 * c0) : T(0)) + e2 * w3;
+                    wo[4 * D.cs] = (lyBh ? -(bh1 * c1) : T(0)) + e2 * w4;
+                    wo[5 * D.cs] = (kp ? -(bh2 * c2) : T(0)) + e2 * w5;
                 }
-#pragma unroll
-                for (int c = 0; c < 6; ++c) y[c * D.cs + gi] = (yv[c] + a * P0[c * G::PL + s]) + b * un[c];
+                T *yo = y + go;
+                yo[0] = (yv0 + a * w0) + b * ux0;
+                yo[D.cs] = (yv1 + a * w1) + b * uy0;
+                yo[2 * D.cs] = (yv2 + a * w2) + b * uz0;
+                yo[3 * D.cs] = (yv3 + a * w3) + b * hx0;
+                yo[4 * D.cs] = (yv4 + a * w4) + b * hy0;
+                yo[5 * D.cs] = (yv5 + a * w5) + b * hz0;
             }
-            __syncthreads();
-            if (tid == 0 && p + S < nplanes) {
-                const uint32_t L = lcount + p + S;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * StageL<T, EM, HA, G>::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                          &tm_cH, x0, y0, kb - 1 + p + S);
+            if (!ONEBAR) {
+                __syncthreads();
+                if (tid == 0 && p + S < nplanes) {
+                    const uint32_t L = lcount + p + S;
+                    issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                              &tm_cH, x0, y0, kb - 1 + p + S);
+                }
             }
         }
+        if (ONEBAR) __syncthreads();
         lcount += nplanes;
     }
 }
@@ -493,29 +601,42 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
     return s;
 }
 
-template <typename T, int EM, bool HA, int BX, int BY, int S>
+template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
 struct FusedCfg {
     using G = Geo<T, BX, BY>;
-    static constexpr int NC = NComp<T, EM, HA>::value;
-    static constexpr size_t lf_smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 2 * 3 * G::RP) * sizeof(T) + 8 * S + 16;
-    static constexpr size_t pair_smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 4 * 3 * G::RP) * sizeof(T) + 8 * S + 16;
+    static constexpr int NR = ONEBAR ? 3 : 2;
+    static constexpr size_t lf_smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + NR * 3 * G::RP) * sizeof(T) + 8 * S + 16;
+    static constexpr size_t pair_smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 2 * NR * 3 * G::RP) * sizeof(T) + 8 * S + 16;
 };
 
-template <typename T, int EM, bool HA>
-static int leapfrog_fused_T(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev *,
-                            int nsrc, const void *q_dev, const std::vector<SrcDev> &hsrc) {
-    constexpr int BX = 32, BY = 8, S = 3;
-    using Cfg = FusedCfg<T, EM, HA, BX, BY, S>;
+// kernel variant: (S = 3, two barriers per plane) by default; PARAEXP_ONEBAR=1 selects
+// (S = 4, one barrier per plane).
+static bool onebar() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PARAEXP_ONEBAR");
+        v = (e && atoi(e) != 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+template <typename K>
+static int resident_per_sm(K kern, int threads, size_t smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    return per_sm;
+}
+
+template <typename T, int EM, bool HA, int S, bool ONEBAR>
+static int leapfrog_fused_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int nsrc,
+                            const void *q_dev, const std::vector<SrcDev> &hsrc) {
+    constexpr int BX = 32, BY = 8;
+    using Cfg = FusedCfg<T, EM, HA, BX, BY, S, ONEBAR>;
     using G = Geo<T, BX, BY>;
     const Grid &g = *ka.g;
-    auto kern = leapfrog_fused_kernel<T, EM, HA, BX, BY, S>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::lf_smem);
-        attr_set = true;
-    }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::NTHR, Cfg::lf_smem);
+    auto kern = leapfrog_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR>;
+    static const int per_sm = resident_per_sm(kern, G::NTHR, Cfg::lf_smem);
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "fused leapfrog kernel does not fit on an SM");
     const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
     const int grid = std::min(sch.units, per_sm * num_sms());
@@ -555,27 +676,22 @@ int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const 
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
-        return leapfrog_fused_T<T, EM, HA>(ka, bufs, nsteps, src_dev, nsrc, q_dev, hsrc);
+        if (onebar()) return leapfrog_fused_V<T, EM, HA, 4, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc);
+        return leapfrog_fused_V<T, EM, HA, 3, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc);
     });
 }
 
 int zero_node_launch(const KernelArgs &ka, const Plan &plan, const void *w, void *wn, void *y,
                      double c, int init, int do_w);
 
-template <typename T, int EM, bool HA>
-static int poly_fused_T(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
-    constexpr int BX = 32, BY = 8, S = 3;
-    using Cfg = FusedCfg<T, EM, HA, BX, BY, S>;
+template <typename T, int EM, bool HA, int S, bool ONEBAR>
+static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
+    constexpr int BX = 32, BY = 8;
+    using Cfg = FusedCfg<T, EM, HA, BX, BY, S, ONEBAR>;
     using G = Geo<T, BX, BY>;
     const Grid &g = *ka.g;
-    auto kern = pair_fused_kernel<T, EM, HA, BX, BY, S>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::pair_smem);
-        attr_set = true;
-    }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::NTHR, Cfg::pair_smem);
+    auto kern = pair_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR>;
+    static const int per_sm = resident_per_sm(kern, G::NTHR, Cfg::pair_smem);
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "fused pair kernel does not fit on an SM");
     const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
     const int grid = std::min(sch.units, per_sm * num_sms());
@@ -587,20 +703,27 @@ static int poly_fused_T(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     if (HA && (rc = make_map<T>(&tmH, g, g.d_cH_arr, 3, G::WX, G::HY))) return rc;
     cudaStream_t s = (cudaStream_t)ka.stream;
     T *w = (T *)bufs[0], *yy = (T *)bufs[1], *sp = (T *)bufs[2], *sp2 = (T *)bufs[3];
+    CUtensorMap tmW, tmS;   // maps of the two ping-pong w buffers
+    if ((rc = make_map<T>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
+    if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
     int init = 1;
     for (const Op &op : plan.ops) {
         if (op.kind == 0 || op.kind == 1) {
-            CUtensorMap tmW;
-            if ((rc = make_map<T>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
             const int do_w = op.kind == 0;
             kern<<<grid, G::NTHR, Cfg::pair_smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, sch, T(op.a), T(op.b),
                                                        T(op.e2), init, do_w);
             ++*ka.launches;
-            if (do_w) std::swap(w, sp);
+            if (do_w) {
+                std::swap(w, sp);
+                std::swap(tmW, tmS);
+            }
         } else {
             const int do_w = op.kind == 2;
             if ((rc = zero_node_launch(ka, plan, w, sp, yy, op.a, init, do_w))) return rc;
-            if (do_w) std::swap(w, sp);
+            if (do_w) {
+                std::swap(w, sp);
+                std::swap(tmW, tmS);
+            }
         }
         init = 0;
     }
@@ -616,7 +739,8 @@ int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
-        return poly_fused_T<T, EM, HA>(ka, plan, bufs);
+        if (onebar()) return poly_fused_V<T, EM, HA, 4, true>(ka, plan, bufs);
+        return poly_fused_V<T, EM, HA, 3, false>(ka, plan, bufs);
     });
 }
 
