@@ -319,11 +319,25 @@ def make_plan(method: str, m: int, s: int, tau: float, rho: float) -> Plan:
         return Plan("taylor", m, s, tau, rho, 0.0, 1.0, nodes, d)
     a = 1.05 * h * rho
     gamma = a / 2.0
-    xi = leja_points(m + 1)
+    if gamma == 0:       # degenerate interval: the c -> 0 limit is Taylor
+        nodes = [0j] * (m + 1)
+        d = [1.0 / math.factorial(k) + 0j for k in range(m + 1)]
+        return Plan("leja", m, s, tau, rho, 0.0, 1.0, nodes, d)
+    xi = newton_order(m)
     nodes = [2j * x for x in xi]
-    d = divided_differences(nodes, gamma) if gamma > 0 else [1.0 / math.factorial(k) + 0j
-                                                             for k in range(m + 1)]
+    d = divided_differences(nodes, gamma)
     return Plan("leja", m, s, tau, rho, a, gamma, nodes, d)
+
+
+def newton_order(m: int) -> tuple:
+    """Evaluation order of the degree-m Leja node set (DESIGN reading 29): the same set as the
+    greedy prefix (1, -1, 0, +eta_1, -eta_1, ..., +eta_L, -eta_L), L = (m-2)/2, with the zero
+    node moved last:  (1, -1, +eta_1, -eta_1, ..., +eta_L, -eta_L, 0).  The interpolation
+    polynomial depends only on the node set, so L_{m,c} is unchanged; m = 1 uses (1, -1)."""
+    if m == 1:
+        return (1.0, -1.0)
+    xs = leja_points(m + 1)
+    return tuple([xs[0], xs[1]] + list(xs[3:m + 1]) + [xs[2]])
 
 
 def newton_eval_scalar(plan: Plan, lam: complex) -> complex:
@@ -396,44 +410,34 @@ def expmv_newton_complex(g: Grid, plan: Plan, e, h, check_imag=True):
 
 
 def pair_schedule(plan: Plan):
-    """Real conjugate-pair schedule of one substep.  Returns a list of
-    ('pair', k, eta_hat) / ('half', k, eta_hat) / ('zero', k, last) entries."""
-    ops = []
+    """Real conjugate-pair schedule of one substep (readings 28-29): nodes come
+    in conjugate pairs (k, k+1) = (+i eta, -i eta); the zero node is last.  Entries:
+    ('pair', k, eta) / ('last', k, eta) (the final pair, which also adds d_m w_m) /
+    ('half', k, eta) (m = 1)."""
     m = plan.m
-    eta0 = abs(plan.nodes[0].imag)
-    ops.append(("half" if m == 1 else "pair", 0, eta0))
     if m == 1:
-        return ops
-    ops.append(("zero", 2, m == 2))
-    k = 3
-    while k < m:
-        eta = abs(plan.nodes[k].imag)
-        ops.append(("half" if k + 1 == m else "pair", k, eta))
-        k += 2
-    return ops
+        return [("half", 0, abs(plan.nodes[0].imag))]
+    return [("last" if k == m - 2 else "pair", k, abs(plan.nodes[k].imag)) for k in range(0, m, 2)]
 
 
 def pair_constants(plan: Plan, dtype: str = "f64"):
     """Per-op constants, each computed in fp64 and rounded once to dtype (reading 24):
-    pair/half: a = Re d_k + eta Im d_{k+1}, b = Re d_{k+1}, e2 = eta^2;  zero: c = Re d_k."""
+    a = Re d_k + eta Im d_{k+1}, b = Re d_{k+1}, e2 = eta^2 and, for 'last', c = Re d_m."""
     out = []
-    for op in pair_schedule(plan):
-        kind, k = op[0], op[1]
-        if kind == "zero":
-            out.append((kind, float(_round(plan.d[k].real, dtype)), op[2]))
-        else:
-            eta = op[2]
-            a = plan.d[k].real + eta * plan.d[k + 1].imag
-            b = plan.d[k + 1].real
-            out.append((kind, float(_round(a, dtype)), float(_round(b, dtype)),
-                        float(_round(eta * eta, dtype))))
+    for kind, k, eta in pair_schedule(plan):
+        a = plan.d[k].real + eta * plan.d[k + 1].imag
+        b = plan.d[k + 1].real
+        c = plan.d[k + 2].real if kind == "last" else 0.0
+        out.append((kind, float(_round(a, dtype)), float(_round(b, dtype)),
+                    float(_round(eta * eta, dtype)), float(_round(c, dtype))))
     return out
 
 
 def expmv_pairs(g: Grid, plan: Plan, e, h, dtype: str = "f64"):
-    """The same polynomial in real arithmetic, conjugate pairs folded:
-        pair: u = X w; y += a w + b u; w = X u + e2 w     half: u = X w; y += a w + b u
-        zero: y += c w; w = X w (unless last)             substep: w = b; y = 0; ...; b = y
+    """The same polynomial in real arithmetic, conjugate pairs folded (readings 28-29):
+        pair: u = X w; y += a w + b u; w = X u + e2 w
+        last: u = X w; y += a w + b u + c (X u + e2 w)      half (m = 1): u = X w; y += a w + b u
+        substep: w = b; y = 0; ...; b = y
     Arithmetic fp64; constants rounded to `dtype` (reading 24).  Pinned against
     expmv_newton_complex in fp64."""
     X = ScaledOp(g, (plan.tau / plan.s) / (plan.gamma * g.dt), dtype)
@@ -444,22 +448,19 @@ def expmv_pairs(g: Grid, plan: Plan, e, h, dtype: str = "f64"):
         we, wh = be, bh
         ye = np.zeros_like(be)
         yh = np.zeros_like(bh)
-        for op in consts:
-            if op[0] == "zero":
-                _, c, last = op
-                ye = ye + c * we
-                yh = yh + c * wh
-                if not last:
-                    we, wh = X(we, wh)
-            else:
-                kind, a, b, e2 = op
-                ue, uh = X(we, wh)
-                ye = ye + a * we + b * ue
-                yh = yh + a * wh + b * uh
-                if kind == "pair":
-                    xe, xh = X(ue, uh)
-                    we = xe + e2 * we
-                    wh = xh + e2 * wh
+        for kind, a, b, e2, c in consts:
+            ue, uh = X(we, wh)
+            ye = ye + a * we + b * ue
+            yh = yh + a * wh + b * uh
+            if kind != "half":
+                xe, xh = X(ue, uh)
+                we2 = xe + e2 * we
+                wh2 = xh + e2 * wh
+                if kind == "last":
+                    ye = ye + c * we2
+                    yh = yh + c * wh2
+                else:
+                    we, wh = we2, wh2
         be, bh = ye, yh
     return be, bh
 

@@ -324,7 +324,7 @@ template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
 __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
-    T *__restrict__ y, Sched sch, T a, T b, T e2, int init, int do_w) {
+    T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode) {
     using G = Geo<T, BX, BY>;
     using SL = StageL<T, EM, HA, G>;
     constexpr int NR = ONEBAR ? 3 : 2;
@@ -464,7 +464,8 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
                 const T w0 = P0[sB], w1 = P0[G::PL + sB], w2 = P0[2 * G::PL + sB];
                 const T w3 = P0[3 * G::PL + sB], w4 = P0[4 * G::PL + sB], w5 = P0[5 * G::PL + sB];
                 const int64_t go = gB + (int64_t)k * D.plane;
-                if (do_w) {
+                T wn0 = T(0), wn1 = T(0), wn2 = T(0), wn3 = T(0), wn4 = T(0), wn5 = T(0);
+                if (mode != 1) {
                     // w'_h(k) = -bH C u_e + e2 w_h
                     const T uz_jp = UE0[2 * G::RP + re + G::EX], ux_jp = UE0[re + G::EX];
                     const T uz_ip = UE0[2 * G::RP + re + 1], uy_ip = UE0[G::RP + re + 1];
@@ -492,21 +493,40 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
                         bh2 = P0[ch + 2 * G::PL + sB] * cf.sig;
                     }
                     const bool kp = k > 0;
-                    T *wo = wout + go;
-                    wo[0] = ((lxBe && kp) ? be0 * d0 : T(0)) + e2 * w0;
-                    wo[D.cs] = ((lyBe && kp) ? be1 * d1 : T(0)) + e2 * w1;
-                    wo[2 * D.cs] = (lzBe ? be2 * d2 : T(0)) + e2 * w2;
-                    wo[3 * D.cs] = (lxBh ? -(bh0 * c0) : T(0)) + e2 * w3;
-                    wo[4 * D.cs] = (lyBh ? -(bh1 * c1) : T(0)) + e2 * w4;
-                    wo[5 * D.cs] = (kp ? -(bh2 * c2) : T(0)) + e2 * w5;
+                    wn0 = ((lxBe && kp) ? be0 * d0 : T(0)) + e2 * w0;
+                    wn1 = ((lyBe && kp) ? be1 * d1 : T(0)) + e2 * w1;
+                    wn2 = (lzBe ? be2 * d2 : T(0)) + e2 * w2;
+                    wn3 = (lxBh ? -(bh0 * c0) : T(0)) + e2 * w3;
+                    wn4 = (lyBh ? -(bh1 * c1) : T(0)) + e2 * w4;
+                    wn5 = (kp ? -(bh2 * c2) : T(0)) + e2 * w5;
+                    if (mode == 0) {
+                        T *wo = wout + go;
+                        wo[0] = wn0;
+                        wo[D.cs] = wn1;
+                        wo[2 * D.cs] = wn2;
+                        wo[3 * D.cs] = wn3;
+                        wo[4 * D.cs] = wn4;
+                        wo[5 * D.cs] = wn5;
+                    }
+                }
+                T y0 = (yv0 + a * w0) + b * ux0, y1 = (yv1 + a * w1) + b * uy0;
+                T y2 = (yv2 + a * w2) + b * uz0, y3 = (yv3 + a * w3) + b * hx0;
+                T y4 = (yv4 + a * w4) + b * hy0, y5 = (yv5 + a * w5) + b * hz0;
+                if (mode == 2) {
+                    y0 = y0 + cl * wn0;
+                    y1 = y1 + cl * wn1;
+                    y2 = y2 + cl * wn2;
+                    y3 = y3 + cl * wn3;
+                    y4 = y4 + cl * wn4;
+                    y5 = y5 + cl * wn5;
                 }
                 T *yo = y + go;
-                yo[0] = (yv0 + a * w0) + b * ux0;
-                yo[D.cs] = (yv1 + a * w1) + b * uy0;
-                yo[2 * D.cs] = (yv2 + a * w2) + b * uz0;
-                yo[3 * D.cs] = (yv3 + a * w3) + b * hx0;
-                yo[4 * D.cs] = (yv4 + a * w4) + b * hy0;
-                yo[5 * D.cs] = (yv5 + a * w5) + b * hz0;
+                yo[0] = y0;
+                yo[D.cs] = y1;
+                yo[2 * D.cs] = y2;
+                yo[3 * D.cs] = y3;
+                yo[4 * D.cs] = y4;
+                yo[5 * D.cs] = y5;
             }
             if (!ONEBAR) {
                 __syncthreads();
@@ -620,6 +640,22 @@ static bool onebar() {
     return v == 1;
 }
 
+static int env_stages(const char *name, int dflt) {
+    const char *e = getenv(name);
+    const int v = e ? atoi(e) : dflt;
+    return (v >= 2 && v <= 5) ? v : dflt;
+}
+// measured on B200 (tools/kbench.py, 256^3): fp64 pair S = 3, fp32 pair S = 4
+static int pair_stages(bool fp64) {
+    static int v64 = env_stages("PARAEXP_PAIR_S", 3);
+    static int v32 = env_stages("PARAEXP_PAIR_S", 4);
+    return fp64 ? v64 : v32;
+}
+static int lf_stages() {
+    static int v = env_stages("PARAEXP_LF_S", 3);
+    return v;
+}
+
 template <typename K>
 static int resident_per_sm(K kern, int threads, size_t smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -677,12 +713,10 @@ int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const 
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
         if (onebar()) return leapfrog_fused_V<T, EM, HA, 4, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc);
+        if (lf_stages() == 4) return leapfrog_fused_V<T, EM, HA, 4, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc);
         return leapfrog_fused_V<T, EM, HA, 3, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc);
     });
 }
-
-int zero_node_launch(const KernelArgs &ka, const Plan &plan, const void *w, void *wn, void *y,
-                     double c, int init, int do_w);
 
 template <typename T, int EM, bool HA, int S, bool ONEBAR>
 static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
@@ -708,22 +742,12 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
     int init = 1;
     for (const Op &op : plan.ops) {
-        if (op.kind == 0 || op.kind == 1) {
-            const int do_w = op.kind == 0;
-            kern<<<grid, G::NTHR, Cfg::pair_smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, sch, T(op.a), T(op.b),
-                                                       T(op.e2), init, do_w);
-            ++*ka.launches;
-            if (do_w) {
-                std::swap(w, sp);
-                std::swap(tmW, tmS);
-            }
-        } else {
-            const int do_w = op.kind == 2;
-            if ((rc = zero_node_launch(ka, plan, w, sp, yy, op.a, init, do_w))) return rc;
-            if (do_w) {
-                std::swap(w, sp);
-                std::swap(tmW, tmS);
-            }
+        kern<<<grid, G::NTHR, Cfg::pair_smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, sch, T(op.a), T(op.b),
+                                                   T(op.e2), T(op.c), init, op.kind);
+        ++*ka.launches;
+        if (op.kind == 0) {
+            std::swap(w, sp);
+            std::swap(tmW, tmS);
         }
         init = 0;
     }
@@ -740,7 +764,12 @@ int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
         if (onebar()) return poly_fused_V<T, EM, HA, 4, true>(ka, plan, bufs);
-        return poly_fused_V<T, EM, HA, 3, false>(ka, plan, bufs);
+        switch (pair_stages(sizeof(T) == 8)) {
+            case 2: return poly_fused_V<T, EM, HA, 2, false>(ka, plan, bufs);
+            case 4: return poly_fused_V<T, EM, HA, 4, false>(ka, plan, bufs);
+            case 5: return poly_fused_V<T, EM, HA, 5, false>(ka, plan, bufs);
+            default: return poly_fused_V<T, EM, HA, 3, false>(ka, plan, bufs);
+        }
     });
 }
 

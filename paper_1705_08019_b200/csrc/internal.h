@@ -71,9 +71,11 @@ void grid_free_device(Grid &G);
 int grid_create(const paraexp_grid_desc *d, paraexp_grid **out);
 
 // ---- plan ----
-struct Op {           // one step of the real conjugate-pair schedule (DESIGN a6)
-    int kind;         // 0 pair, 1 half pair, 2 zero node (with w update), 3 zero node last
-    double a, b, e2;  // pair/half: y += a w + b u ; w = X u + e2 w.   zero: y += a w
+struct Op {              // one conjugate pair of the real Newton schedule (readings 28-29)
+    int kind;            // 0 pair: u = Xw; y += a w + b u; w <- Xu + e2 w
+                         // 1 half (m = 1): u = Xw; y += a w + b u
+                         // 2 last pair: u = Xw; y += a w + b u + c (Xu + e2 w)
+    double a, b, e2, c;
 };
 struct Plan {
     int method, m, s;

@@ -185,20 +185,21 @@ __global__ void __launch_bounds__(256) applyX_kernel(Dev<T> D, Coef<T, EM, HA> c
     out[5 * D.cs + idx] = D.h_live(2, i, j, k) ? -(cf.bH(2, idx) * b2) : T(0);
 }
 
-// y <- (init ? 0 : y) + a w + b u ;  if do_w:  w <- X u + e2 w   (in place on w)
+// y <- (init ? 0 : y) + a w + b u ;  mode 0: w <- X u + e2 w (in place on w);
+// mode 1 (half): no w update;  mode 2 (last pair): y += c (X u + e2 w), w untouched
 template <typename T, int EM, bool HA>
 __global__ void __launch_bounds__(256) pair_update_kernel(Dev<T> D, Coef<T, EM, HA> cf,
                                                           T *__restrict__ w,
                                                           const T *__restrict__ u,
-                                                          T *__restrict__ y, T a, T b, T e2,
-                                                          int init, int do_w) {
+                                                          T *__restrict__ y, T a, T b, T e2, T cl,
+                                                          int init, int mode) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y * blockDim.y + threadIdx.y;
     const int k = blockIdx.z;
     if (i >= D.nx || j >= D.ny) return;
     const int64_t idx = D.idx(i, j, k);
-    T xu[6];
-    if (do_w) {
+    T xu[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
+    if (mode != 1) {
         T a0, a1, a2, b0, b1, b2;
         curlT_at(D, u + 3 * D.cs, u + 4 * D.cs, u + 5 * D.cs, i, j, k, idx, a0, a1, a2);
         curl_at(D, u, u + D.cs, u + 2 * D.cs, i, j, k, idx, b0, b1, b2);
@@ -215,39 +216,10 @@ __global__ void __launch_bounds__(256) pair_update_kernel(Dev<T> D, Coef<T, EM, 
         const T wv = w[q];
         const T uv = u[q];
         const T y0 = init ? T(0) : y[q];
-        y[q] = (y0 + a * wv) + b * uv;
-        if (do_w) w[q] = xu[c] + e2 * wv;
-    }
-}
-
-// zero node: y <- (init ? 0 : y) + c w ; if do_w: wn <- X w
-template <typename T, int EM, bool HA>
-__global__ void __launch_bounds__(256) zero_node_kernel(Dev<T> D, Coef<T, EM, HA> cf,
-                                                        const T *__restrict__ w,
-                                                        T *__restrict__ wn,
-                                                        T *__restrict__ y, T cc, int init,
-                                                        int do_w) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y * blockDim.y + threadIdx.y;
-    const int k = blockIdx.z;
-    if (i >= D.nx || j >= D.ny) return;
-    const int64_t idx = D.idx(i, j, k);
-    if (do_w) {
-        T a0, a1, a2, b0, b1, b2;
-        curlT_at(D, w + 3 * D.cs, w + 4 * D.cs, w + 5 * D.cs, i, j, k, idx, a0, a1, a2);
-        curl_at(D, w, w + D.cs, w + 2 * D.cs, i, j, k, idx, b0, b1, b2);
-        wn[idx] = D.e_live(0, i, j, k) ? cf.bE(0, k, idx) * a0 : T(0);
-        wn[D.cs + idx] = D.e_live(1, i, j, k) ? cf.bE(1, k, idx) * a1 : T(0);
-        wn[2 * D.cs + idx] = D.e_live(2, i, j, k) ? cf.bE(2, k, idx) * a2 : T(0);
-        wn[3 * D.cs + idx] = D.h_live(0, i, j, k) ? -(cf.bH(0, idx) * b0) : T(0);
-        wn[4 * D.cs + idx] = D.h_live(1, i, j, k) ? -(cf.bH(1, idx) * b1) : T(0);
-        wn[5 * D.cs + idx] = D.h_live(2, i, j, k) ? -(cf.bH(2, idx) * b2) : T(0);
-    }
-#pragma unroll
-    for (int c = 0; c < 6; ++c) {
-        const int64_t q = c * D.cs + idx;
-        const T y0 = init ? T(0) : y[q];
-        y[q] = y0 + cc * w[q];
+        T yn = (y0 + a * wv) + b * uv;
+        if (mode == 2) yn = yn + cl * (xu[c] + e2 * wv);
+        y[q] = yn;
+        if (mode == 0) w[q] = xu[c] + e2 * wv;
     }
 }
 
@@ -406,41 +378,18 @@ int k_poly_substep_unfused(const KernelArgs &ka, const Plan &plan, void *bufs[4]
         auto cf = make_coef<T, EM, HA>(*ka.g, plan.sigma);
         const dim3 grid = cell_grid(ka.g->L, false);
         cudaStream_t s = (cudaStream_t)ka.stream;
-        T *w = (T *)bufs[0], *yy = (T *)bufs[1], *uu = (T *)bufs[2], *sp = (T *)bufs[3];
+        T *w = (T *)bufs[0], *yy = (T *)bufs[1], *uu = (T *)bufs[2];
         int init = 1;
         for (const Op &op : plan.ops) {
-            if (op.kind == 0 || op.kind == 1) {
-                applyX_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, w, uu);
-                pair_update_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(
-                    D, cf, w, uu, yy, T(op.a), T(op.b), T(op.e2), init, op.kind == 0);
-                *ka.launches += 2;
-            } else {
-                const int do_w = op.kind == 2;
-                zero_node_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, w, sp, yy, T(op.a), init, do_w);
-                ++*ka.launches;
-                if (do_w) std::swap(w, sp);
-            }
+            applyX_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, w, uu);
+            pair_update_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, w, uu, yy, T(op.a), T(op.b), T(op.e2),
+                                                                  T(op.c), init, op.kind);
+            *ka.launches += 2;
             init = 0;
         }
         bufs[0] = yy;
         bufs[1] = w;
-        bufs[2] = uu;
-        bufs[3] = sp;
         return check_cuda("poly substep");
-    });
-}
-
-int zero_node_launch(const KernelArgs &ka, const Plan &plan, const void *w, void *wn, void *y,
-                     double c, int init, int do_w) {
-    return with_types(*ka.g, plan.sigma, [&](auto tT, auto tEM, auto tHA) {
-        using T = decltype(tT);
-        constexpr int EM = decltype(tEM)::value;
-        constexpr bool HA = decltype(tHA)::value;
-        zero_node_kernel<T, EM, HA><<<cell_grid(ka.g->L, false), kBlock, 0, (cudaStream_t)ka.stream>>>(
-            make_dev<T>(*ka.g), make_coef<T, EM, HA>(*ka.g, plan.sigma), (const T *)w, (T *)wn, (T *)y,
-            T(c), init, do_w);
-        ++*ka.launches;
-        return check_cuda("zero node");
     });
 }
 

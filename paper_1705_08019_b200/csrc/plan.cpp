@@ -105,10 +105,27 @@ static void divdiff_exp_imag(const std::vector<double> &y, double gamma, std::ve
     }
 }
 
+// Evaluation order of the degree-m node set (DESIGN reading 29): the greedy prefix
+// (1, -1, 0, +eta_1, -eta_1, ..., +eta_L, -eta_L) with the zero node moved last, so that every
+// conjugate pair is closed and the zero-node term folds into the final pair.
+static void newton_order(int m, std::vector<double> &xi) {
+    std::vector<double> g;
+    leja_sequence(m + 1, g);
+    xi.clear();
+    if (m == 1) {
+        xi = {g[0], g[1]};
+        return;
+    }
+    xi.push_back(g[0]);
+    xi.push_back(g[1]);
+    for (int k = 3; k <= m; ++k) xi.push_back(g[k]);
+    xi.push_back(g[2]);
+}
+
 static void leja_coefficients(int m, double gamma, std::vector<double> &xi,
                               std::vector<double> &dre, std::vector<double> &dim,
                               bool quad) {
-    leja_sequence(m + 1, xi);
+    newton_order(m, xi);
     std::vector<double> y(m + 1);
     for (int k = 0; k <= m; ++k) y[k] = 2.0 * xi[k];   // capacity-scaled nodes 2i*xi'_k
     dre.resize(m + 1);
@@ -194,26 +211,20 @@ double theta_m(int method, int m, double tol) {
 
 // ---- schedule of one substep (DESIGN a6) ------------------------------------------------
 static void build_ops(Plan &p) {
+    // conjugate pairs (k, k+1), k = 0, 2, ..., m-2; the last one also adds Re d_m * w_m
     p.ops.clear();
     const int m = p.m;
-    auto pair_op = [&](int kind, int k, double eta) {
+    auto eta_at = [&](int k) { return p.node_im.empty() ? 0.0 : std::fabs(p.node_im[k]); };
+    for (int k = 0; k < std::max(m, 1); k += 2) {
         Op o;
-        o.kind = kind;
+        const double eta = eta_at(k);
+        o.kind = m == 1 ? 1 : (k == m - 2 ? 2 : 0);
         o.a = p.d_re[k] + eta * p.d_im[k + 1];
         o.b = p.d_re[k + 1];
         o.e2 = eta * eta;
+        o.c = o.kind == 2 ? p.d_re[k + 2] : 0.0;
         p.ops.push_back(o);
-    };
-    auto eta_at = [&](int k) { return p.node_im.empty() ? 0.0 : std::fabs(p.node_im[k]); };
-    pair_op(m == 1 ? 1 : 0, 0, eta_at(0));
-    if (m == 1) return;
-    Op z;
-    z.kind = (m == 2) ? 3 : 2;
-    z.a = p.d_re[2];
-    z.b = 0;
-    z.e2 = 0;
-    p.ops.push_back(z);
-    for (int k = 3; k < m; k += 2) pair_op(k + 1 == m ? 1 : 0, k, eta_at(k));
+    }
 }
 
 int make_plan(int method, int m, int s, double eps_A, double tau, double rho, double dt,
@@ -276,7 +287,7 @@ int make_plan(int method, int m, int s, double eps_A, double tau, double rho, do
         out.a = 0;
         out.gamma = 1.0;
         taylor_coefficients(out.m, out.d_re, out.d_im);
-        if (method == PARAEXP_LEJA) leja_sequence(out.m + 1, out.xi);
+        if (method == PARAEXP_LEJA) newton_order(out.m, out.xi);
     }
     out.sigma = h / (out.gamma * dt);
     build_ops(out);
