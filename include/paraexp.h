@@ -174,6 +174,37 @@ int paraexp_leapfrog(paraexp_grid *grid, const paraexp_source *src, int32_t nsrc
                      int64_t nsteps, void *e, void *h, int32_t check_finite, void *stream,
                      paraexp_stats *stats);
 
+/* ---- trace: energy and probe outputs (Fig. 7) ------- */
+/* Probes are e-field edges (comp, i, j, k) (the paper's probe is a grid voltage, Fig. 3).
+ * All output pointers are caller-owned DEVICE pointers of doubles (stream-ordered), or
+ * NULL to skip that output.
+ *   leapfrog: energy[m] = E_{m+1} = e^(m+1)' M_eps e^(m+1) + h^(m+1/2)' M_mu h^(m+3/2)
+ *             (eq:energy; conserved exactly by leapfrog without source),
+ *             probe[m*nprobe + r] = e_r^(m+1), for m = 0 .. nsteps-1.  The energy
+ *             weights are M_eps = dt/cE_T and M_mu = dt/cH_T, evaluated in fp64 from the
+ *             run-dtype coefficients (joules with volts/amperes as grid voltages).
+ *   solve:    one row per sub-interval boundary T_i = t0 + S_i dt, i = 1 .. p:
+ *             energy[i-1] = <e,e>_eps + <h,h>_mu of the reconstructed same-time solution
+ *             u(T_i) = v_i(T_i) + sum_{j<i} w_j(T_i) (E(t) of PAPER:742-747, with h at
+ *             T_i from reading 9) and probe[(i-1)*nprobe + r] = e_r(T_i).  With more
+ *             than one rank the probe rows are summed over ranks (a few doubles) and
+ *             delivered on every rank; the energy rows need the whole summed field and are
+ *             delivered for i = p only (others NaN) -- the root computes E(T_p).
+ * Errors: EINVAL (nprobe out of range, probe edge out of range or dead). */
+#define PARAEXP_MAX_PROBES 16
+typedef struct {
+    int32_t nprobe;
+    int32_t comp[PARAEXP_MAX_PROBES], i[PARAEXP_MAX_PROBES], j[PARAEXP_MAX_PROBES],
+        k[PARAEXP_MAX_PROBES];
+    double *energy;  /* device, nsteps (leapfrog) or p (solve) doubles, or NULL        */
+    double *probe;   /* device, rows x nprobe doubles, or NULL                        */
+} paraexp_trace;
+
+/* paraexp_leapfrog with a trace (trace == NULL is paraexp_leapfrog). */
+int paraexp_leapfrog_trace(paraexp_grid *grid, const paraexp_source *src, int32_t nsrc,
+                           double t0, int64_t nsteps, void *e, void *h,
+                           const paraexp_trace *trace, void *stream, paraexp_stats *stats);
+
 /* ---- exp(tau A) v (a5, a6) -------------------------------------------------------- */
 /* Options:
  *   method   PARAEXP_LEJA (Newton form on Leja points of i[-a,a], a = 1.05 h rho,
@@ -247,6 +278,14 @@ int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *
                   const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
                   const void *e0, const void *h0, void *e_out, void *h_out, void *stream,
                   paraexp_stats *stats);
+
+/* paraexp_solve (tail_mode EXP) with a trace of the reconstructed solution at the
+ * sub-interval boundaries T_1 .. T_p (see paraexp_trace above; f1).  Collective. */
+int paraexp_solve_trace(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
+                        int32_t nsrc, double t0, int64_t nsteps, int32_t p,
+                        const paraexp_expmv_opts *opts, int32_t broadcast_out, const void *e0,
+                        const void *h0, void *e_out, void *h_out, const paraexp_trace *trace,
+                        void *stream, paraexp_stats *stats);
 
 /* ---- host-only helpers (no GPU needed) -------------------------------------------- */
 /* Partition of nsteps into p sub-intervals: bounds[0..p], bounds[0] = 0, bounds[p] = nsteps

@@ -76,6 +76,23 @@ def _round(x, dtype):
     return np.asarray(x, dtype=np.float64)
 
 
+# eq:cfl: min over cells of sqrt(eps mu / (dx^-2 + dy^-2 + dz^-2))
+def cfl_dt(nx, ny, nz, dx, dy, dz, eps_r=None, mu_r=None):
+    """dt_CFL of a grid; dx/dy/dz per-cell spacing arrays, eps_r/mu_r per cell (None = 1).
+    Needs no FIT matrices, so it also serves grids too large to assemble here."""
+    dx, dy, dz = (np.asarray(a, float) for a in (dx, dy, dz))
+    best = math.inf
+    eps = None if eps_r is None else np.asarray(eps_r, float).reshape(nz, ny, nx)
+    mu = None if mu_r is None else np.asarray(mu_r, float).reshape(nz, ny, nx)
+    for k in range(nz):                      # one z-layer of cells (ny x nx) at a time
+        inv = 1.0 / dx[None, :] ** 2 + 1.0 / dy[:, None] ** 2 + 1.0 / dz[k] ** 2
+        er = 1.0 if eps is None else eps[k]
+        mr = 1.0 if mu is None else mu[k]
+        v = np.sqrt(EPS0 * er * MU0 * mr / inv)
+        best = min(best, float(np.min(v)))
+    return best
+
+
 # ---------------------------------------------------------------------------
 # Grid (PAPER:150-180, 246-254)
 # ---------------------------------------------------------------------------
@@ -125,18 +142,8 @@ class Grid:
         return cls(w.nx, w.ny, w.nz, d0=w.d0, eps_r=w.eps_r, pec_cell=w.pec_cell,
                    dt_frac=w.dt_frac, dtype=dtype or w.dtype)
 
-    # eq:cfl: min over cells of sqrt(eps mu / (dx^-2 + dy^-2 + dz^-2))
     def cfl(self):
-        best = math.inf
-        nx, ny = self.nx, self.ny
-        eps = self.eps_r.reshape(self.nz, self.ny, self.nx)
-        mu = self.mu_r.reshape(self.nz, self.ny, self.nx)
-        for k in range(self.nz):
-            for j in range(ny):
-                inv = 1.0 / self.dx ** 2 + 1.0 / self.dy[j] ** 2 + 1.0 / self.dz[k] ** 2
-                v = np.sqrt(EPS0 * eps[k, j, :] * MU0 * mu[k, j, :] / inv)
-                best = min(best, float(v.min()))
-        return best
+        return cfl_dt(self.nx, self.ny, self.nz, self.dx, self.dy, self.dz, self.eps_r, self.mu_r)
 
     # --- vectors -----------------------------------------------------------
     def zeros(self):
@@ -242,6 +249,24 @@ def sync_h(g: Grid, e, h):
 def energy_staggered(g: Grid, e_m, h_mmh, h_mph):
     """E_m = e^m' M_eps e^m + h^(m-1/2)' M_mu h^(m+1/2) (eq:energy)."""
     return float(np.dot(e_m * g.M_eps_w(), e_m) + np.dot(h_mmh * g.M_mu_w(), h_mph))
+
+
+def leapfrog_trace(g: Grid, e, h, nsteps, sources=(), t0=0.0, probes=()):
+    """Leapfrog with per-step outputs: one step at a time,
+    energy[m] = E_{m+1} = e^(m+1)' M_eps e^(m+1) + h^(m+1/2)' M_mu h^(m+3/2) (eq:energy,
+    PAPER:256-275) and probe[m, r] = e^(m+1) at the probe edges (comp, i, j, k).
+    Returns (e^(n), h^(n+1/2), energy, probe)."""
+    e = np.array(e, dtype=np.float64, copy=True)
+    h = np.array(h, dtype=np.float64, copy=True)
+    dofs = [g.edge_dof(*pr) for pr in probes]
+    energy = np.zeros(nsteps)
+    probe = np.zeros((nsteps, len(dofs)))
+    for m in range(nsteps):
+        e1, h1 = leapfrog(g, e, h, 1, sources, t0, m)
+        energy[m] = energy_staggered(g, e1, h, h1)
+        probe[m] = [e1[d] for d in dofs]
+        e, h = e1, h1
+    return e, h, energy, probe
 
 
 # ---------------------------------------------------------------------------
@@ -573,6 +598,38 @@ def paraexp(g: Grid, sources, t0: float, nsteps: int, p: int, plan_for, u0=None,
         return e_p.copy(), h_p.copy()
     _, Wh_half = expmv(g, Ehalf, We, Wh, mode, dtype)
     return e_p + We, h_p + Wh_half
+
+
+def paraexp_boundary_states(g: Grid, sources, t0: float, nsteps: int, p: int, plan_for, u0=None,
+                            rho=None, dtype: Optional[str] = None, mode: str = "pairs"):
+    """The reconstructed same-time solution at every sub-interval boundary (f1; the E(t) of
+    PAPER:742-747 sampled at T_i, i = 1..p), written as its plain definition with independent
+    tails (a different association from the library's Horner accumulator):
+        u(T_i) = s_i + sum_{j<i} E_i ... E_{j+1} s_j  (+ E_i ... E_1 u0),
+    s_j = (e_j, h_sync_j) the seed of sub-interval j (reading 9).  Returns [(e, h)] * p."""
+    dtype = dtype or g.dtype
+    S = partition(nsteps, p)
+
+    def E(i, we, wh):
+        return expmv(g, plan_for((S[i] - S[i - 1]) * g.dt), we, wh, mode, dtype)
+
+    seeds = []
+    for i in range(1, p + 1):
+        z_e, z_h = g.zeros()
+        ei, hi = leapfrog(g, z_e, z_h, S[i] - S[i - 1], sources, t0, S[i - 1])
+        seeds.append((ei, sync_h(g, ei, hi)))
+    states = []
+    for i in range(1, p + 1):
+        ue, uh = seeds[i - 1][0].copy(), seeds[i - 1][1].copy()
+        starts = [(j, seeds[j - 1]) for j in range(1, i)]
+        if u0 is not None:
+            starts.insert(0, (0, g.clean(*u0)))
+        for j, (te, th) in starts:
+            for q in range(j + 1, i + 1):
+                te, th = E(q, te, th)
+            ue, uh = ue + te, uh + th
+        states.append((ue, uh))
+    return states
 
 
 def paraexp_block(g: Grid, sources, t0: float, nsteps: int, p: int, plan_for, first: int,

@@ -16,7 +16,8 @@ from . import abi
 from .abi import (EDIVERGED, EINVAL, ENOTSUP, EOVERFLOW, F32, F64, KERNELS_AUTO, KERNELS_FUSED,  # noqa
                   KERNELS_UNFUSED, LEJA, TAIL_EXP, TAIL_LEAPFROG, TAYLOR, ParaexpError, check)
 
-__all__ = ["Grid", "Comm", "leapfrog", "expmv", "expmv_plan", "solve", "partition", "schedule",
+__all__ = ["Grid", "Comm", "leapfrog", "leapfrog_trace", "expmv", "expmv_plan", "solve", "solve_trace",
+           "partition", "schedule",
            "leja_points", "plan_host", "theta", "version", "make_sources", "ParaexpError"]
 
 _DT = {"f64": F64, "f32": F32}
@@ -165,6 +166,42 @@ def leapfrog(grid: Grid, e, h, nsteps: int, sources=None, t0: float = 0.0,
     return st.as_dict()
 
 
+def _trace(grid, rows, probes, energy):
+    """paraexp_trace with device output tensors (fp64) of `rows` energies / rows x nprobe probes."""
+    import torch
+    probes = list(probes or [])
+    if len(probes) > abi.MAX_PROBES:
+        raise ValueError(f"at most {abi.MAX_PROBES} probes")
+    t = abi.paraexp_trace()
+    t.nprobe = len(probes)
+    for r, (c, i, j, k) in enumerate(probes):
+        t.comp[r], t.i[r], t.j[r], t.k[r] = int(c), int(i), int(j), int(k)
+    dev = f"cuda:{grid.device}"
+    en = torch.zeros(max(rows, 1), dtype=torch.float64, device=dev) if energy else None
+    pr = torch.zeros(max(rows, 1) * max(len(probes), 1), dtype=torch.float64, device=dev) if probes else None
+    t.energy = en.data_ptr() if en is not None else None
+    t.probe = pr.data_ptr() if pr is not None else None
+    return t, en, pr
+
+
+def leapfrog_trace(grid: Grid, e, h, nsteps: int, sources=None, t0: float = 0.0, probes=None,
+                   energy: bool = True, stream=None):
+    """paraexp_leapfrog_trace: leapfrog in place plus per-step outputs (f1).  Returns
+    (stats, energy[nsteps] fp64 tensor or None, probe[nsteps, nprobe] fp64 tensor or None):
+    energy[m] = E_{m+1} (eq:energy), probe[m, r] = e_r^(m+1); probes = [(comp, i, j, k), ...]."""
+    arr, n = make_sources(sources)
+    t, en, pr = _trace(grid, nsteps, probes, energy)
+    st = abi.paraexp_stats()
+    check(abi.lib.paraexp_leapfrog_trace(grid.handle, arr, n, float(t0), int(nsteps), _field(e, grid, "e"),
+                                         _field(h, grid, "h"), C.byref(t), _stream(stream, grid),
+                                         C.byref(st)), "paraexp_leapfrog_trace")
+    if pr is not None:
+        pr = pr[:nsteps * len(probes)].view(nsteps, len(probes))
+    if en is not None:
+        en = en[:nsteps]
+    return st.as_dict(), en, pr
+
+
 def expmv(grid: Grid, tau: float, e, h, method="leja", m=0, s=0, eps_A=1e-12, rho=0.0,
           stream=None) -> dict:
     """paraexp_expmv: (h, e) <- exp(tau A_orig)(h, e) in place."""
@@ -282,3 +319,29 @@ def solve(grid: Grid, nsteps: int, p: int, sources=None, t0: float = 0.0, method
                                 int(bool(broadcast_out)), e0, h0, eo, ho, _stream(stream, grid),
                                 C.byref(st)), "paraexp_solve")
     return st.as_dict()
+
+
+def solve_trace(grid: Grid, nsteps: int, p: int, sources=None, t0: float = 0.0, method="leja", m=0,
+                s=0, eps_A=1e-12, rho=0.0, u0=None, e_out=None, h_out=None, probes=None,
+                energy: bool = True, comm: Optional[Comm] = None, broadcast_out=False, stream=None):
+    """paraexp_solve_trace: solve plus the energy / probe rows at the sub-interval boundaries
+    T_1..T_p (f1).  Returns (stats, energy[p] or None, probe[p, nprobe] or None)."""
+    arr, n = make_sources(sources)
+    o = _opts(method, m, s, eps_A, rho)
+    t, en, pr = _trace(grid, p, probes, energy)
+    st = abi.paraexp_stats()
+    e0 = h0 = C.c_void_p(0)
+    if u0 is not None:
+        e0 = _field(u0[0], grid, "e0")
+        h0 = _field(u0[1], grid, "h0")
+    eo = _field(e_out, grid, "e_out") if e_out is not None else C.c_void_p(0)
+    ho = _field(h_out, grid, "h_out") if h_out is not None else C.c_void_p(0)
+    check(abi.lib.paraexp_solve_trace(grid.handle, comm.handle if comm else C.c_void_p(0), arr, n,
+                                      float(t0), int(nsteps), int(p), C.byref(o),
+                                      int(bool(broadcast_out)), e0, h0, eo, ho, C.byref(t),
+                                      _stream(stream, grid), C.byref(st)), "paraexp_solve_trace")
+    if pr is not None:
+        pr = pr[:p * len(probes)].view(p, len(probes))
+    if en is not None:
+        en = en[:p]
+    return st.as_dict(), en, pr

@@ -27,6 +27,7 @@ TAIL_EXP, TAIL_LEAPFROG = 0, 1
 MAT_SCALAR, MAT_ZTABLE, MAT_ARRAY = 0, 1, 2
 KERNELS_AUTO, KERNELS_UNFUSED, KERNELS_FUSED = 0, 1, 2
 MAX_DEGREE = 100
+MAX_PROBES = 16
 
 _dp = C.POINTER(C.c_double)
 
@@ -82,6 +83,12 @@ class paraexp_plan_info(C.Structure):
                 ("d_re", C.c_double * (MAX_DEGREE + 1)), ("d_im", C.c_double * (MAX_DEGREE + 1))]
 
 
+class paraexp_trace(C.Structure):
+    _fields_ = [("nprobe", C.c_int32), ("comp", C.c_int32 * MAX_PROBES), ("i", C.c_int32 * MAX_PROBES),
+                ("j", C.c_int32 * MAX_PROBES), ("k", C.c_int32 * MAX_PROBES),
+                ("energy", C.c_void_p), ("probe", C.c_void_p)]
+
+
 _vp = C.c_void_p
 _sigs = {
     "paraexp_grid_create": (C.c_int, [C.POINTER(paraexp_grid_desc), C.POINTER(_vp)]),
@@ -101,6 +108,13 @@ _sigs = {
     "paraexp_solve": (C.c_int, [_vp, _vp, C.POINTER(paraexp_source), C.c_int32, C.c_double,
                                 C.c_int64, C.c_int32, C.POINTER(paraexp_expmv_opts), C.c_int32,
                                 C.c_int32, _vp, _vp, _vp, _vp, _vp, C.POINTER(paraexp_stats)]),
+    "paraexp_leapfrog_trace": (C.c_int, [_vp, C.POINTER(paraexp_source), C.c_int32, C.c_double,
+                                         C.c_int64, _vp, _vp, C.POINTER(paraexp_trace), _vp,
+                                         C.POINTER(paraexp_stats)]),
+    "paraexp_solve_trace": (C.c_int, [_vp, _vp, C.POINTER(paraexp_source), C.c_int32, C.c_double,
+                                      C.c_int64, C.c_int32, C.POINTER(paraexp_expmv_opts), C.c_int32,
+                                      _vp, _vp, _vp, _vp, C.POINTER(paraexp_trace), _vp,
+                                      C.POINTER(paraexp_stats)]),
     "paraexp_partition": (C.c_int, [C.c_int64, C.c_int32, C.POINTER(C.c_int64)]),
     "paraexp_schedule": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),

@@ -195,15 +195,40 @@ static double default_rho(Grid &G, const paraexp_expmv_opts *o, void *stream, in
 
 // ---- dispatch fused / unfused -------------------------------------------------------------
 int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev *src_dev,
-                     int nsrc, const void *q_dev);
+                     int nsrc, const void *q_dev, const TraceDev *tr);
 int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]);
 bool fused_supported(const Grid &g);
 
 int k_leapfrog(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev *src_dev,
-               int nsrc, const void *q_dev) {
+               int nsrc, const void *q_dev, const TraceDev *tr) {
     if (ka.g->kernels == PARAEXP_KERNELS_FUSED && fused_supported(*ka.g))
-        return k_leapfrog_fused(ka, bufs, nsteps, src_dev, nsrc, q_dev);
-    return k_leapfrog_unfused(ka, bufs[0], nsteps, src_dev, nsrc, q_dev);
+        return k_leapfrog_fused(ka, bufs, nsteps, src_dev, nsrc, q_dev, tr);
+    return k_leapfrog_unfused(ka, bufs[0], nsteps, src_dev, nsrc, q_dev, tr);
+}
+
+// validate a paraexp_trace and build its device view (probe offsets in the device layout)
+static int prepare_trace(const Grid &G, const paraexp_trace *t, TraceDev &tr) {
+    tr = TraceDev();
+    tr.dt = G.dt;
+    if (!t) return PARAEXP_OK;
+    if (t->nprobe < 0 || t->nprobe > PARAEXP_MAX_PROBES) return fail(PARAEXP_EINVAL, "nprobe out of range");
+    const int64_t NX = G.nx + 1, NY = G.ny + 1;
+    for (int r = 0; r < t->nprobe; ++r) {
+        const int c = t->comp[r], i = t->i[r], j = t->j[r], k = t->k[r];
+        if (c < 0 || c > 2 || i < 0 || j < 0 || k < 0 || i > G.nx || j > G.ny || k > G.nz)
+            return fail(PARAEXP_EINVAL, "probe edge out of range");
+        if (G.cE64[c * G.npts + i + NX * (j + NY * (int64_t)k)] == 0.0)
+            return fail(PARAEXP_EINVAL, "probe on a dead (PEC/virtual) edge");
+        tr.c[r] = c;
+        tr.i[r] = i;
+        tr.j[r] = j;
+        tr.k[r] = k;
+        tr.off[r] = c * G.L.cs + i + G.L.px * (j + (int64_t)G.ny * k);
+    }
+    tr.np = t->probe ? t->nprobe : 0;
+    tr.energy = t->energy;
+    tr.probe = t->probe;
+    return PARAEXP_OK;
 }
 int k_poly_substep(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     if (ka.g->kernels == PARAEXP_KERNELS_FUSED && fused_supported(*ka.g))
@@ -281,6 +306,7 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*Reduce)(const void *, void *, size_t, int, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Broadcast)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi g_nccl;
@@ -299,9 +325,10 @@ int load_nccl() {
     g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
     g_nccl.Reduce = (decltype(g_nccl.Reduce))dlsym(h, "ncclReduce");
     g_nccl.Broadcast = (decltype(g_nccl.Broadcast))dlsym(h, "ncclBroadcast");
+    g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
     g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
     if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.CommDestroy || !g_nccl.Reduce ||
-        !g_nccl.Broadcast || !g_nccl.GetErrorString)
+        !g_nccl.Broadcast || !g_nccl.AllReduce || !g_nccl.GetErrorString)
         return pe::fail(PARAEXP_ENCCL, "libnccl.so.2 lacks required symbols");
     g_nccl.ok = true;
     return PARAEXP_OK;
@@ -397,9 +424,25 @@ int paraexp_grid_info(paraexp_grid *grid, int32_t compute_rho_pow, void *stream,
     return PARAEXP_OK;
 }
 
+static int leapfrog_impl(paraexp_grid *grid, const paraexp_source *src, int32_t nsrc, double t0,
+                         int64_t nsteps, void *e, void *h, int32_t check_finite,
+                         const paraexp_trace *trace, void *stream, paraexp_stats *st);
+
 int paraexp_leapfrog(paraexp_grid *grid, const paraexp_source *src, int32_t nsrc, double t0,
                      int64_t nsteps, void *e, void *h, int32_t check_finite, void *stream,
                      paraexp_stats *st) {
+    return leapfrog_impl(grid, src, nsrc, t0, nsteps, e, h, check_finite, nullptr, stream, st);
+}
+
+int paraexp_leapfrog_trace(paraexp_grid *grid, const paraexp_source *src, int32_t nsrc, double t0,
+                           int64_t nsteps, void *e, void *h, const paraexp_trace *trace, void *stream,
+                           paraexp_stats *st) {
+    return leapfrog_impl(grid, src, nsrc, t0, nsteps, e, h, 0, trace, stream, st);
+}
+
+static int leapfrog_impl(paraexp_grid *grid, const paraexp_source *src, int32_t nsrc, double t0,
+                         int64_t nsteps, void *e, void *h, int32_t check_finite,
+                         const paraexp_trace *trace, void *stream, paraexp_stats *st) {
     using namespace pe;
     if (!grid) return fail(PARAEXP_EINVAL, "null grid");
     Grid &G = grid->g;
@@ -413,6 +456,10 @@ int paraexp_leapfrog(paraexp_grid *grid, const paraexp_source *src, int32_t nsrc
     if (rc) return rc;
     std::vector<SrcDev> sd;
     if ((rc = prepare_sources(G, src, nsrc, t0, 0, nsteps, stream, sd))) return rc;
+    TraceDev tr;
+    if ((rc = prepare_trace(G, trace, tr))) return rc;
+    const bool tracing = tr.energy || tr.np > 0;
+    if (tr.energy && nsteps > 0 && (rc = dev_memset_async(tr.energy, 0, sizeof(double) * nsteps, stream))) return rc;
     if ((rc = ensure_ws(G, 2))) return rc;
     KernelArgs ka{&G, stream, &S.kernel_launches};
     Events ev(stream);
@@ -420,7 +467,7 @@ int paraexp_leapfrog(paraexp_grid *grid, const paraexp_source *src, int32_t nsrc
     void *bufs[2] = {G.ws[0], G.ws[1]};
     if ((rc = k_pack(ka, e, h, bufs[0]))) return rc;
     const int id5 = ev.open(5);
-    if ((rc = k_leapfrog(ka, bufs, nsteps, (const SrcDev *)G.d_src, nsrc, G.d_q))) return rc;
+    if ((rc = k_leapfrog(ka, bufs, nsteps, (const SrcDev *)G.d_src, nsrc, G.d_q, tracing ? &tr : nullptr))) return rc;
     ev.close(id5);
     if ((rc = k_unpack(ka, bufs[0], e, h))) return rc;
     ev.close(id);
@@ -529,11 +576,35 @@ void paraexp_comm_destroy(paraexp_comm *comm) {
     delete comm;
 }
 
+static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
+                      int32_t nsrc, double t0, int64_t nsteps, int32_t p,
+                      const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
+                      const void *e0, const void *h0, void *e_out, void *h_out,
+                      const paraexp_trace *trace, void *stream, paraexp_stats *st);
+
 int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
                   int32_t nsrc, double t0, int64_t nsteps, int32_t p,
                   const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
                   const void *e0, const void *h0, void *e_out, void *h_out, void *stream,
                   paraexp_stats *st) {
+    return solve_impl(grid, comm, src, nsrc, t0, nsteps, p, opts, tail_mode, broadcast_out, e0, h0, e_out,
+                      h_out, nullptr, stream, st);
+}
+
+int paraexp_solve_trace(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
+                        int32_t nsrc, double t0, int64_t nsteps, int32_t p,
+                        const paraexp_expmv_opts *opts, int32_t broadcast_out, const void *e0,
+                        const void *h0, void *e_out, void *h_out, const paraexp_trace *trace,
+                        void *stream, paraexp_stats *st) {
+    return solve_impl(grid, comm, src, nsrc, t0, nsteps, p, opts, PARAEXP_TAIL_EXP, broadcast_out, e0, h0,
+                      e_out, h_out, trace, stream, st);
+}
+
+static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
+                      int32_t nsrc, double t0, int64_t nsteps, int32_t p,
+                      const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
+                      const void *e0, const void *h0, void *e_out, void *h_out,
+                      const paraexp_trace *trace, void *stream, paraexp_stats *st) {
     using namespace pe;
     if (!grid) return fail(PARAEXP_EINVAL, "null grid");
     Grid &G = grid->g;
@@ -542,6 +613,7 @@ int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *
     if (p > 1000) return fail(PARAEXP_EINVAL, "p > 1000 not supported");
     if (tail_mode != PARAEXP_TAIL_EXP && tail_mode != PARAEXP_TAIL_LEAPFROG) return fail(PARAEXP_EINVAL, "bad tail mode");
     if ((e0 == nullptr) != (h0 == nullptr)) return fail(PARAEXP_EINVAL, "e0 and h0 must both be given or both NULL");
+    if (trace && tail_mode != PARAEXP_TAIL_EXP) return fail(PARAEXP_EINVAL, "trace needs tail_mode EXP");
     const int rank = comm ? comm->rank : 0, world = comm ? comm->world : 1;
     paraexp_stats local{};
     paraexp_stats &S = st ? *st : local;
@@ -587,6 +659,17 @@ int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *
 
     std::vector<SrcDev> sd;
     if ((rc = prepare_sources(G, src, nsrc, t0, 0, nsteps, stream, sd))) return rc;
+    TraceDev tr;
+    if ((rc = prepare_trace(G, trace, tr))) return rc;
+    const bool tracing = tr.energy || tr.np > 0;
+    if (tracing) {
+        // rows i < p of the energy need the summed field: NaN with several ranks (paraexp.h)
+        std::vector<double> init(p, world > 1 ? std::nan("") : 0.0);
+        init[p - 1] = 0.0;
+        if (tr.energy && (rc = dev_memcpy_h2d_async(tr.energy, init.data(), sizeof(double) * p, stream))) return rc;
+        if (tr.np > 0 && (rc = dev_memset_async(tr.probe, 0, sizeof(double) * p * tr.np, stream))) return rc;
+        if ((rc = dev_sync(stream))) return rc;
+    }
     if ((rc = ensure_ws(G, 5))) return rc;
     KernelArgs ka{&G, stream, &S.kernel_launches};
     const size_t sbytes = (size_t)G.L.state_elems() * G.esize();
@@ -622,6 +705,15 @@ int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *
         return r;
     };
 
+    // f1: the Horner accumulator after sub-interval i (seed added) is this rank's share of the
+    // same-time solution u(T_i) = v_i(T_i) + sum_{j<i} w_j(T_i)
+    auto trace_row = [&](int i) -> int {
+        int r = PARAEXP_OK;
+        if (tr.np > 0) r = k_gather(ka, W, tr, tr.probe + (int64_t)(i - 1) * tr.np, 0);
+        if (!r && tr.energy && world == 1) r = k_dot_M_async(ka, W, W, tr.energy + (i - 1), G.dt);
+        return r;
+    };
+
     if (first >= 1) {
         if (first == 1 && has_u0) {
             if ((rc = k_pack(ka, e0, h0, W))) return rc;
@@ -652,12 +744,15 @@ int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *
                     if ((rc = dev_memcpy_d2d_async(W, P, sbytes, stream))) return rc;
                     W_valid = true;
                 }
+                if (tracing && (rc = trace_row(i))) return rc;
             }
             ev.close(id);
         }
         const int id = ev.open(1);
-        for (int i = last + 1; i <= p; ++i)
+        for (int i = last + 1; i <= p; ++i) {
             if (W_valid && (rc = propagate(i))) return rc;
+            if (tracing && i < p && W_valid && (rc = trace_row(i))) return rc;
+        }
         ev.close(id);
     }
     if (!W_valid && (rc = dev_memset_async(W, 0, sbytes, stream))) return rc;
@@ -673,6 +768,20 @@ int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *
     }
     // a9: reconstruction on the root (eq:averaging1/2, reading 10)
     const int idf = ev.open(3);
+    if (rank == root && tracing) {
+        // row p: u(T_p) = sync(v_p) + W, same-time (reading 9)
+        if ((rc = dev_memcpy_d2d_async(X[0], P, sbytes, stream))) return rc;
+        if ((rc = k_sync(ka, X[0]))) return rc;
+        if ((rc = k_axpy(ka, X[0], W, 1.0))) return rc;
+        if (tr.np > 0 && (rc = k_gather(ka, X[0], tr, tr.probe + (int64_t)(p - 1) * tr.np, 0))) return rc;
+        if (tr.energy && (rc = k_dot_M_async(ka, X[0], X[0], tr.energy + (p - 1), G.dt))) return rc;
+    }
+    if (tracing && world > 1) {
+        if (tr.np > 0 && (rc = nccl_check(g_nccl.AllReduce(tr.probe, tr.probe, (size_t)p * tr.np, kNcclF64, kNcclSum,
+                                                          comm->comm, (cudaStream_t)stream), "ncclAllReduce"))) return rc;
+        if (tr.energy && (rc = nccl_check(g_nccl.AllReduce(tr.energy, tr.energy, (size_t)p, kNcclF64, kNcclSum,
+                                                           comm->comm, (cudaStream_t)stream), "ncclAllReduce"))) return rc;
+    }
     if (rank == root) {
         if (tail_mode == PARAEXP_TAIL_EXP) {
             if ((rc = k_axpy_comps(ka, P, W, 1.0, 0, 3))) return rc;       // e_out = e_p + W_e

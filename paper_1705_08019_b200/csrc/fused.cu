@@ -171,11 +171,13 @@ __device__ __forceinline__ void curl_stage(const T *E0, const T *E1, int s, T &c
 //   end of iteration k.
 // ONEBAR = true: one barrier per plane, ring depth 3, the slot of plane k-1 is refilled right
 //   after the barrier of iteration k (every warp has then left phase B of iteration k-1).
-template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
+// TR: also accumulate the step's energy E_{m+1} = dt [sum e'^2/cE + sum h h'/cH] (eq:energy)
+// and write the probe values e' (f1; paraexp.h trace).
+template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR, bool TR>
 __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ out,
-    Sched sch, SrcList src, const T *__restrict__ q) {
+    Sched sch, SrcList src, const T *__restrict__ q, const __grid_constant__ TraceDev tr) {
     using G = Geo<T, BX, BY>;
     using SL = StageL<T, EM, HA, G>;
     constexpr int NR = ONEBAR ? 3 : 2;
@@ -201,6 +203,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
     }
     __syncthreads();
     uint32_t lcount = 0;   // planes loaded by this CTA so far (ring position)
+    double eacc = 0.0;     // TR: this thread's energy contributions
     for (int unit = blockIdx.x; unit < sch.units; unit += gridDim.x) {
         const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
@@ -210,9 +213,12 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
         const bool inA = hasA && iA < D.nx && jA < D.ny;
         const bool lxA = inA && jA > 0, lyA = inA && iA > 0, lzA = inA && iA > 0 && jA > 0;
         const bool wrA = inA && tileA;
-        uint32_t smask = 0;
+        uint32_t smask = 0, pmask = 0;
         for (int r = 0; r < src.n; ++r)
             if (inA && src.i[r] == iA && src.j[r] == jA) smask |= 1u << r;
+        if (TR)
+            for (int r = 0; r < tr.np; ++r)
+                if (wrA && tr.i[r] == iA && tr.j[r] == jA) pmask |= 1u << r;
         T *oA = out + D.idx(wrA ? iA : 0, wrA ? jA : 0, 0);
         const int iB = x0 + tx, jB = y0 + ty;
         const bool inB = hasB && iB < D.nx && jB < D.ny;
@@ -269,6 +275,21 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
                     o[0] = e0;
                     o[D.cs] = e1;
                     o[2 * D.cs] = e2;
+                    if (TR) {
+                        T w0 = bE0, w1 = bE1, w2 = bE2;
+                        if (EM == 2) {
+                            w0 = P1[SL::ST + sA] * cf.sig;
+                            w1 = P1[SL::ST + G::PL + sA] * cf.sig;
+                            w2 = P1[SL::ST + 2 * G::PL + sA] * cf.sig;
+                        }
+                        if (w0 != T(0)) eacc += (double)e0 * (double)e0 / (double)w0;
+                        if (w1 != T(0)) eacc += (double)e1 * (double)e1 / (double)w1;
+                        if (w2 != T(0)) eacc += (double)e2 * (double)e2 / (double)w2;
+                        if (pmask)
+                            for (int r = 0; r < tr.np; ++r)
+                                if (((pmask >> r) & 1u) && tr.k[r] == kk)
+                                    tr.probe[r] = (double)(tr.c[r] == 0 ? e0 : (tr.c[r] == 1 ? e1 : e2));
+                    }
                 }
             }
             __syncthreads();
@@ -289,15 +310,23 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
                 const T c2 = ((ex0 + ey_ip) - ex_jp) - ey0;
                 const T hx = P0[3 * G::PL + sB], hy = P0[4 * G::PL + sB], hz = P0[5 * G::PL + sB];
                 T *o = oB + (int64_t)k * D.plane;
+                T g0 = bH0, g1 = bH1, g2 = bH2;
                 if (HA) {
                     const int ch = SL::ST + SL::CE;
-                    o[0] = lxB ? hx - (P0[ch + sB] * cf.sig) * c0 : hx;
-                    o[D.cs] = lyB ? hy - (P0[ch + G::PL + sB] * cf.sig) * c1 : hy;
-                    o[2 * D.cs] = k > 0 ? hz - (P0[ch + 2 * G::PL + sB] * cf.sig) * c2 : hz;
-                } else {
-                    o[0] = lxB ? hx - bH0 * c0 : hx;
-                    o[D.cs] = lyB ? hy - bH1 * c1 : hy;
-                    o[2 * D.cs] = k > 0 ? hz - bH2 * c2 : hz;
+                    g0 = P0[ch + sB] * cf.sig;
+                    g1 = P0[ch + G::PL + sB] * cf.sig;
+                    g2 = P0[ch + 2 * G::PL + sB] * cf.sig;
+                }
+                const T n0 = lxB ? hx - g0 * c0 : hx;
+                const T n1 = lyB ? hy - g1 * c1 : hy;
+                const T n2 = k > 0 ? hz - g2 * c2 : hz;
+                o[0] = n0;
+                o[D.cs] = n1;
+                o[2 * D.cs] = n2;
+                if (TR) {
+                    if (lxB && g0 != T(0)) eacc += (double)hx * (double)n0 / (double)g0;
+                    if (lyB && g1 != T(0)) eacc += (double)hy * (double)n1 / (double)g1;
+                    if (k > 0 && g2 != T(0)) eacc += (double)hz * (double)n2 / (double)g2;
                 }
             }
             if (!ONEBAR) {
@@ -312,6 +341,10 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
         }
         if (ONEBAR) __syncthreads();
         lcount += nplanes;
+    }
+    if (TR && tr.energy) {
+        const double sum = block_sum(eacc);
+        if (tid == 0 && sum != 0.0) atomicAdd(tr.energy, sum * tr.dt);
     }
 }
 
@@ -664,14 +697,14 @@ static int resident_per_sm(K kern, int threads, size_t smem) {
     return per_sm;
 }
 
-template <typename T, int EM, bool HA, int S, bool ONEBAR>
+template <typename T, int EM, bool HA, int S, bool ONEBAR, bool TR>
 static int leapfrog_fused_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int nsrc,
-                            const void *q_dev, const std::vector<SrcDev> &hsrc) {
+                            const void *q_dev, const std::vector<SrcDev> &hsrc, const TraceDev *tr) {
     constexpr int BX = 32, BY = 8;
     using Cfg = FusedCfg<T, EM, HA, BX, BY, S, ONEBAR>;
     using G = Geo<T, BX, BY>;
     const Grid &g = *ka.g;
-    auto kern = leapfrog_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR>;
+    auto kern = leapfrog_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR, TR>;
     static const int per_sm = resident_per_sm(kern, G::NTHR, Cfg::lf_smem);
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "fused leapfrog kernel does not fit on an SM");
     const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
@@ -693,11 +726,18 @@ static int leapfrog_fused_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps,
         sl.k[r] = hsrc[r].k;
     }
     cudaStream_t s = (cudaStream_t)ka.stream;
+    TraceDev trm;
+    if (TR) trm = *tr;
     for (int64_t m = 0; m < nsteps; ++m) {
         const bool even = (m % 2) == 0;
+        if (TR) {
+            trm.energy = tr->energy ? tr->energy + m : nullptr;
+            trm.probe = tr->probe ? tr->probe + m * tr->np : nullptr;
+            if (!trm.probe) trm.np = 0;
+        }
         kern<<<grid, G::NTHR, Cfg::lf_smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf,
                                                  (T *)(even ? bufs[1] : bufs[0]), sch, sl,
-                                                 nsrc ? (const T *)q_dev + m * nsrc : nullptr);
+                                                 nsrc ? (const T *)q_dev + m * nsrc : nullptr, trm);
         ++*ka.launches;
     }
     if (nsteps % 2) std::swap(bufs[0], bufs[1]);
@@ -705,16 +745,18 @@ static int leapfrog_fused_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps,
 }
 
 int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev *src_dev,
-                     int nsrc, const void *q_dev) {
-    if (nsrc > 16) return k_leapfrog_unfused(ka, bufs[0], nsteps, src_dev, nsrc, q_dev);
+                     int nsrc, const void *q_dev, const TraceDev *tr) {
+    if (nsrc > 16) return k_leapfrog_unfused(ka, bufs[0], nsteps, src_dev, nsrc, q_dev, tr);
     const std::vector<SrcDev> &hsrc = ka.g->h_src;
+    const bool trace = tr && (tr->energy || (tr->probe && tr->np > 0));
     return with_types(*ka.g, 1.0, [&](auto tT, auto tEM, auto tHA) {
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
-        if (onebar()) return leapfrog_fused_V<T, EM, HA, 4, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc);
-        if (lf_stages() == 4) return leapfrog_fused_V<T, EM, HA, 4, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc);
-        return leapfrog_fused_V<T, EM, HA, 3, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc);
+        if (trace) return leapfrog_fused_V<T, EM, HA, 3, false, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
+        if (onebar()) return leapfrog_fused_V<T, EM, HA, 4, true, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
+        if (lf_stages() == 4) return leapfrog_fused_V<T, EM, HA, 4, false, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
+        return leapfrog_fused_V<T, EM, HA, 3, false, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
     });
 }
 

@@ -108,16 +108,28 @@ struct KernelArgs {
     int64_t *launches;
 };
 
+// per-step trace outputs of a leapfrog sequence (f1): device pointers at the row of the
+// first step; probes are e components at state offsets (comp*cs + idx).
+struct TraceDev {
+    double *energy = nullptr;   // one double per step (accumulated: zeroed by the caller)
+    double *probe = nullptr;    // np doubles per step
+    int np = 0;
+    int c[PARAEXP_MAX_PROBES], i[PARAEXP_MAX_PROBES], j[PARAEXP_MAX_PROBES], k[PARAEXP_MAX_PROBES];
+    int64_t off[PARAEXP_MAX_PROBES];
+    double dt = 0;
+};
+
 // pack canonical (e, h) -> device state (zeroing dead DOFs); unpack the reverse.
 int k_pack(const KernelArgs &ka, const void *e, const void *h, void *state);
 int k_unpack(const KernelArgs &ka, const void *state, void *e, void *h);
 // leapfrog: `nsteps` steps; bufs[0] = state in/out, bufs[1] = spare (fused kernels
 // ping-pong; on return bufs[0] names the buffer holding the result).  q_dev points at the
 // amplitude row of the first step (nsrc values per step).
+// tr (optional): energy E_{m+1} and probe values e^(m+1) per step (paraexp.h trace).
 int k_leapfrog(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev *src_dev,
-               int nsrc, const void *q_dev);
+               int nsrc, const void *q_dev, const TraceDev *tr = nullptr);
 int k_leapfrog_unfused(const KernelArgs &ka, void *state, int64_t nsteps, const SrcDev *src_dev,
-                       int nsrc, const void *q_dev);
+                       int nsrc, const void *q_dev, const TraceDev *tr = nullptr);
 // h <- h + 0.5 cH (C e)  (seed sync, a4)
 int k_sync(const KernelArgs &ka, void *state);
 // h <- h - 0.5 cH (C e)  (staggered start, reading 11)
@@ -134,6 +146,10 @@ int k_check_finite_async(const KernelArgs &ka, const void *state, int *dflag);
 int k_check_finite(const KernelArgs &ka, const void *state, int *host_flag);
 // energy-weighted dot products for K5 Lanczos: out[0] = <x,y>_M (host, synchronous)
 int k_dot_M(const KernelArgs &ka, const void *x, const void *y, double *out);
+// *dout += scale * <x,y>_M / dt  (device accumulator, stream-ordered; energy with scale = dt)
+int k_dot_M_async(const KernelArgs &ka, const void *x, const void *y, double *dout, double scale);
+// dout[r] = state[off[r]] (as double), r < np; or 0 if zero != 0
+int k_gather(const KernelArgs &ka, const void *state, const TraceDev &tr, double *dout, int zero);
 // y <- sigma*dt*A_orig x  (one A-application, unfused)
 int k_apply_A(const KernelArgs &ka, const void *x, void *y, double sigma);
 // z <- alpha x + beta y + gamma z

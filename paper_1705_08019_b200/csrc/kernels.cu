@@ -161,6 +161,46 @@ __global__ void inject_kernel(T *__restrict__ st, const SrcDev *__restrict__ src
     for (int s = 0; s < nsrc; ++s) st[src[s].off] = st[src[s].off] - q[s];
 }
 
+// trace of one unfused leapfrog step (f1), evaluated between the e- and h-halves, i.e. on
+// (e^(m+1), h^(m+1/2)):  energy += dt * [sum e'^2/cE + sum h * h'/cH] with h' = h - bH.*(C e')
+// evaluated exactly as h_half_kernel does (eq:energy); probes <- e'.
+template <typename T, int EM, bool HA>
+__global__ void __launch_bounds__(256) trace_kernel(Dev<T> D, Coef<T, EM, HA> cf,
+                                                    const T *__restrict__ st, double *energy,
+                                                    double dt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    double acc = 0.0;
+    if (i < D.nx && j < D.ny) {
+        const int64_t idx = D.idx(i, j, k);
+        const T *ex = st, *ey = st + D.cs, *ez = st + 2 * D.cs;
+        T c[3];
+        curl_at(D, ex, ey, ez, i, j, k, idx, c[0], c[1], c[2]);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const T ce = cf.bE(q, k, idx);
+            const T ev = st[q * D.cs + idx];
+            if (D.e_live(q, i, j, k) && ce != T(0)) acc += (double)ev * (double)ev / (double)ce;
+            const T ch = cf.bH(q, idx);
+            if (D.h_live(q, i, j, k) && ch != T(0)) {
+                const T hv = st[(3 + q) * D.cs + idx];
+                const T hn = hv - (T(1) * ch) * c[q];
+                acc += (double)hv * (double)hn / (double)ch;
+            }
+        }
+    }
+    acc = block_sum(acc);
+    if (threadIdx.x == 0 && threadIdx.y == 0 && acc != 0.0) atomicAdd(energy, acc * dt);
+}
+
+// dout[r] = (double) st[off[r]]  (probe gather; zero => 0)
+template <typename T>
+__global__ void gather_kernel(const T *__restrict__ st, TraceDev tr, double *dout, int zero) {
+    const int r = threadIdx.x;
+    if (r < tr.np) dout[r] = zero ? 0.0 : (double)st[tr.off[r]];
+}
+
 // ---------------------------------------------------------------------------------------
 // Polynomial recurrence, unfused (a6): u = X w ;  pair/half/zero updates
 // ---------------------------------------------------------------------------------------
@@ -274,6 +314,32 @@ __global__ void __launch_bounds__(256) dotM_kernel(Dev<T> D, Coef<T, EM, HA> cf,
     if (threadIdx.x == 0 && threadIdx.y == 0) atomicAdd(out, acc);
 }
 
+// *out += scale * <x, y>_M / dt
+template <typename T, int EM, bool HA>
+__global__ void __launch_bounds__(256) dotM_scaled_kernel(Dev<T> D, Coef<T, EM, HA> cf,
+                                                          const T *__restrict__ x,
+                                                          const T *__restrict__ y, double *out,
+                                                          double scale) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    double acc = 0.0;
+    if (i < D.nx && j < D.ny) {
+        const int64_t idx = D.idx(i, j, k);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double ce = (double)cf.bE(c, k, idx);
+            if (D.e_live(c, i, j, k) && ce != 0.0)
+                acc += (double)x[c * D.cs + idx] * (double)y[c * D.cs + idx] / ce;
+            const double ch = (double)cf.bH(c, idx);
+            if (D.h_live(c, i, j, k) && ch != 0.0)
+                acc += (double)x[(3 + c) * D.cs + idx] * (double)y[(3 + c) * D.cs + idx] / ch;
+        }
+    }
+    acc = block_sum(acc);
+    if (threadIdx.x == 0 && threadIdx.y == 0 && acc != 0.0) atomicAdd(out, acc * scale);
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
     z += 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -333,7 +399,7 @@ int k_unpack(const KernelArgs &ka, const void *state, void *e, void *h) {
 }
 
 int k_leapfrog_unfused(const KernelArgs &ka, void *state, int64_t nsteps, const SrcDev *src_dev,
-                       int nsrc, const void *q_dev) {
+                       int nsrc, const void *q_dev, const TraceDev *tr) {
     return with_types(*ka.g, 1.0, [&](auto tT, auto tEM, auto tHA) {
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
@@ -346,6 +412,14 @@ int k_leapfrog_unfused(const KernelArgs &ka, void *state, int64_t nsteps, const 
             e_half_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, (T *)state);
             if (nsrc > 0)
                 inject_kernel<T><<<1, 32, 0, s>>>((T *)state, src_dev, nsrc, (const T *)q_dev + m * nsrc);
+            if (tr && tr->energy) {
+                trace_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, (const T *)state, tr->energy + m, tr->dt);
+                ++*ka.launches;
+            }
+            if (tr && tr->probe && tr->np > 0) {
+                gather_kernel<T><<<1, 32, 0, s>>>((const T *)state, *tr, tr->probe + m * tr->np, 0);
+                ++*ka.launches;
+            }
             h_half_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, (T *)state, T(1));
             *ka.launches += 2 + (nsrc > 0);
         }
@@ -462,6 +536,30 @@ int k_dot_M(const KernelArgs &ka, const void *x, const void *y, double *out) {
     });
     if (rc) return rc;
     return dev_memcpy_d2h(out, dred, sizeof(double), ka.stream);
+}
+
+int k_dot_M_async(const KernelArgs &ka, const void *x, const void *y, double *dout, double scale) {
+    // dotM_kernel accumulates <x,y>_M / dt into *dout; the scale is applied by a follow-up
+    // multiply only when it is not 1 (energy: scale = dt)
+    return with_types(*ka.g, 1.0, [&](auto tT, auto tEM, auto tHA) {
+        using T = decltype(tT);
+        constexpr int EM = decltype(tEM)::value;
+        constexpr bool HA = decltype(tHA)::value;
+        dotM_scaled_kernel<T, EM, HA><<<cell_grid(ka.g->L, false), kBlock, 0, (cudaStream_t)ka.stream>>>(
+            make_dev<T>(*ka.g), make_coef<T, EM, HA>(*ka.g, 1.0), (const T *)x, (const T *)y, dout, scale);
+        ++*ka.launches;
+        return check_cuda("dotM async");
+    });
+}
+
+int k_gather(const KernelArgs &ka, const void *state, const TraceDev &tr, double *dout, int zero) {
+    if (tr.np <= 0 || !dout) return PARAEXP_OK;
+    if (ka.g->dtype == PARAEXP_F64)
+        gather_kernel<double><<<1, 32, 0, (cudaStream_t)ka.stream>>>((const double *)state, tr, dout, zero);
+    else
+        gather_kernel<float><<<1, 32, 0, (cudaStream_t)ka.stream>>>((const float *)state, tr, dout, zero);
+    ++*ka.launches;
+    return check_cuda("gather");
 }
 
 int k_apply_A(const KernelArgs &ka, const void *x, void *y, double sigma) {

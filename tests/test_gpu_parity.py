@@ -200,3 +200,59 @@ def test_spiral_pec_small():
     ge, gh, _ = lib_leapfrog(lg, e, h, 400, src)
     assert_parity((ge, gh), ref, "f64", "spiral leapfrog")
     assert np.linalg.norm(ref[0]) > 0
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("kind", ["layered", "random"])
+@pytest.mark.parametrize("kernels", KERNELS)
+def test_leapfrog_trace(dtype, kind, kernels):
+    """f1: per-step energy E_{m+1} (eq:energy) and probe values, fused (in-kernel block
+    reductions) and unfused (trace kernel between the halves), vs the oracle."""
+    n = (37, 23, 11)
+    og, lg = _grids(n, kind, dtype, kernels)
+    e, h = inputs(og, *random_fields(*n, seed=43))
+    src = _sources(og, n)
+    probes = [(s.comp, s.i, s.j, s.k) for s in src] + [(0, 5, 7, 3), (2, 36, 22, 10)]
+    probes = [q for q in probes if og.cE[og.edge_dof(*q)] != 0]
+    ref_e, ref_h, ref_en, ref_pr = fit.leapfrog_trace(og, e, h, 120, src, t0=1e-12, probes=probes)
+    import torch
+    from gpu_util import to_dev, to_host
+    te, th = to_dev(e, lg), to_dev(h, lg)
+    st, en, pr = pe.leapfrog_trace(lg, te, th, 120, src, 1e-12, probes=probes)
+    torch.cuda.synchronize()
+    assert_parity((to_host(te), to_host(th)), (ref_e, ref_h), dtype, "trace fields")
+    tol = TOL[dtype]
+    assert rel_l2(en.cpu().numpy(), ref_en) <= tol
+    assert rel_l2(pr.cpu().numpy(), ref_pr) <= tol
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_solve_trace(dtype):
+    """f1: energy / probes of the reconstructed solution at every sub-interval boundary vs
+    the oracle's independent-tail boundary states."""
+    n = (19, 17, 9)
+    og, lg = _grids(n, "random", dtype, "auto")
+    u0 = inputs(og, *random_fields(*n, seed=78))
+    src = _sources(og, n)
+    probes = [(s.comp, s.i, s.j, s.k) for s in src] + [(1, 3, 4, 5)]
+    nsteps, p, m, s = 61, 4, 24, 6
+    rho = og.rho_cfl
+    states = fit.paraexp_boundary_states(og, src, 1e-12, nsteps, p,
+                                         lambda tau: fit.make_plan("leja", m, s, tau, rho), u0=u0,
+                                         rho=rho, dtype=dtype)
+    ref_en = np.array([og.energy_norm2(ue, uh) for ue, uh in states])
+    ref_pr = np.array([[ue[og.edge_dof(*q)] for q in probes] for ue, _ in states])
+    import torch
+    from gpu_util import to_dev
+    eo = torch.zeros(3 * lg.npts, dtype=lg.torch_dtype(), device="cuda:0")
+    ho = torch.zeros_like(eo)
+    st, en, pr = pe.solve_trace(lg, nsteps, p, src, 1e-12, method="leja", m=m, s=s, rho=rho,
+                                u0=(to_dev(u0[0], lg), to_dev(u0[1], lg)), e_out=eo, h_out=ho,
+                                probes=probes)
+    torch.cuda.synchronize()
+    tol = TOL[dtype]
+    assert rel_l2(en.cpu().numpy(), ref_en) <= tol
+    assert rel_l2(pr.cpu().numpy(), ref_pr) <= tol
+    ref = fit.paraexp(og, src, 1e-12, nsteps, p, lambda tau: fit.make_plan("leja", m, s, tau, rho),
+                      u0=u0, rho=rho, dtype=dtype)
+    assert_parity((eo.double().cpu().numpy(), ho.double().cpu().numpy()), ref, dtype, "solve_trace output")
