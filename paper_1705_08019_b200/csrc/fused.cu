@@ -576,300 +576,6 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
 }
 
 // ---------------------------------------------------------------------------------------
-// K2x2: two Newton pairs (four A-applications) in ONE pass over HBM
-// ---------------------------------------------------------------------------------------
-//   u1 = X w ;  w1 = X u1 + e1 w ;  u2 = X w1 ;  w2 = X u2 + e2 w1
-//   y <- ((y + a1 w) + b1 u1 + a2 w1) + b2 u2  [+ c2 w2 if LAST]        (readings 28-29)
-// The input w carries a 2-cell halo (TMA box (BX+4) x (BY+4)); the intermediates live in
-// shared-memory plane rings on shrinking halo regions (tile T = [x0,x0+BX) x [y0,y0+BY)):
-//   u1_e on E1 = T-1 .. T+2   u1_h on H1 = T-2 .. T+1      ((BX+3) x (BY+3))
-//   w1   on W1 = T-1 .. T+1                                ((BX+2) x (BY+2))
-//   u2_e on E2 = T .. T+1     u2_h on H2 = T-1 .. T        ((BX+1) x (BY+1))
-// z-march: iteration q (input plane q has arrived) computes
-//   A: u1_e(q), u1_h(q-1)   B: w1(q-1)   C: u2_e(q-1), u2_h(q-2)   D: w2(q-2), y(q-2)
-// HBM traffic per 4 A-applications: read w, y; write w2, y (24 values) = 6 values per
-// cell-update.  w(q-2) and y(q-2) for the y-update are read from global
-// (L2-resident: the TMA brought w through L2 two planes earlier).
-template <typename T, int BX, int BY>
-struct Geo2 {
-    static constexpr int VEC = 16 / (int)sizeof(T);
-    static constexpr int OX = VEC >= 2 ? VEC : 2;                    // >= 2 halo cells, 16 B aligned start
-    static constexpr int WX = ((OX + BX + 2 + VEC - 1) / VEC) * VEC;
-    static constexpr int HY = BY + 4;
-    static constexpr int PL = WX * HY;
-    static constexpr int X1 = BX + 3, Y1 = BY + 3, R1 = X1 * Y1;   // E1 / H1
-    static constexpr int XW = BX + 2, YW = BY + 2, RW = XW * YW;   // W1
-    static constexpr int X2 = BX + 1, Y2 = BY + 1, R2 = X2 * Y2;   // E2 / H2
-    static constexpr int NTHR = ((R1 + 31) / 32) * 32;
-    // ring layout (elements): u1_e [3][3][R1] | u1_h [2][3][R1] | w1 [2][6][RW] | u2_e [2][3][R2] | u2_h [2][3][R2]
-    static constexpr int OFF_U1E = 0;
-    static constexpr int OFF_U1H = OFF_U1E + 9 * R1;
-    static constexpr int OFF_W1 = OFF_U1H + 6 * R1;
-    static constexpr int OFF_U2E = OFF_W1 + 12 * RW;
-    static constexpr int OFF_U2H = OFF_U2E + 6 * R2;
-    static constexpr int RING = OFF_U2H + 6 * R2;
-};
-
-template <typename T, int EM, int BX, int BY, int S, bool LAST>
-__global__ void __launch_bounds__(Geo2<T, BX, BY>::NTHR) pair2_fused_kernel(
-    const __grid_constant__ CUtensorMap tm_w, Dev<T> D, Coef<T, EM, false> cf,
-    const T *__restrict__ win, T *__restrict__ wout, T *__restrict__ y, Sched sch, T a1, T b1, T e1, T a2,
-    T b2, T e2, T c2, int init) {
-    using G = Geo2<T, BX, BY>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    T *stages = reinterpret_cast<T *>(smem_raw);
-    constexpr int SZ = ((6 * G::PL + 128 / (int)sizeof(T) - 1) / (128 / (int)sizeof(T))) * (128 / (int)sizeof(T));
-    T *ring = stages + S * SZ;
-    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(ring + G::RING) + 15) & ~uintptr_t(15));
-    T *U1E = ring + G::OFF_U1E, *U1H = ring + G::OFF_U1H, *W1 = ring + G::OFF_W1;
-    T *U2E = ring + G::OFF_U2E, *U2H = ring + G::OFF_U2H;
-    const int tid = threadIdx.x;
-    // phase A/B/C/D point of this thread (local coordinates of each region)
-    const int ax = tid % G::X1, ay = tid / G::X1;         // E1 / H1
-    const bool hasA = tid < G::R1;
-    const int bx = tid % G::XW, by = tid / G::XW;         // W1
-    const bool hasB = tid < G::RW;
-    const int cx = tid % G::X2, cy = tid / G::X2;         // E2 / H2
-    const bool hasC = tid < G::R2;
-    const int dx = tid % BX, dy = tid / BX;               // T
-    const bool hasD = tid < BX * BY;
-    T bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
-    const T bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
-    auto bEk = [&](int c, int k) -> T {                   // coefficient of plane k
-        if (EM == 1) return __ldg(cf.tab + c * cf.nz + k) * cf.sig;
-        return c == 0 ? bE0 : (c == 1 ? bE1 : bE2);
-    };
-    if (tid == 0) {
-        for (int s2 = 0; s2 < S; ++s2) mbar_init(&bars[s2], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    constexpr uint32_t BYTES = (uint32_t)(6 * G::PL * sizeof(T));
-    uint32_t lcount = 0;
-    for (int unit = blockIdx.x; unit < sch.units; unit += gridDim.x) {
-        const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
-        const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
-        const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
-        const int zfirst = kb - 2;                        // first input plane
-        const int nplanes = ke - kb + 4;                  // planes kb-2 .. ke+1
-        // global coordinates of this thread's points
-        const int iE1 = x0 - 1 + ax, jE1 = y0 - 1 + ay;   // u1_e
-        const int iH1 = x0 - 2 + ax, jH1 = y0 - 2 + ay;   // u1_h
-        const int iW = x0 - 1 + bx, jW = y0 - 1 + by;     // w1
-        const int iE2 = x0 + cx, jE2 = y0 + cy;           // u2_e
-        const int iH2 = x0 - 1 + cx, jH2 = y0 - 1 + cy;   // u2_h
-        const int iD = x0 + dx, jD = y0 + dy;             // tile
-        auto inxy = [&](int i, int j) { return i >= 0 && j >= 0 && i < D.nx && j < D.ny; };
-        const bool vE1 = hasA && inxy(iE1, jE1), vH1 = hasA && inxy(iH1, jH1);
-        const bool vW = hasB && inxy(iW, jW);
-        const bool vE2 = hasC && inxy(iE2, jE2), vH2 = hasC && inxy(iH2, jH2);
-        const bool vD = hasD && iD < D.nx && jD < D.ny;
-        // stage indices (stage x = global x - x0 + OX, stage y = global y - y0 + 2)
-        const int sE1 = (ay + 1) * G::WX + ax - 1 + G::OX;   // (iE1, jE1)
-        const int sH1 = ay * G::WX + ax - 2 + G::OX;         // (iH1, jH1)
-        const int sW = (by + 1) * G::WX + bx - 1 + G::OX;    // (iW, jW)
-        const int64_t gD = D.idx(vD ? iD : 0, vD ? jD : 0, 0);
-        if (tid == 0)
-            for (int p = 0; p < min(S, nplanes); ++p) {
-                const uint32_t L = lcount + p;
-                mbar_expect_tx(&bars[L % S], BYTES);
-                tma_load_4d(stages + (L % S) * SZ, &tm_w, &bars[L % S], x0 - G::OX, y0 - 2, zfirst + p, 0);
-            }
-        for (int p = 1; p < nplanes; ++p) {               // iteration q = zfirst + p
-            const int q = zfirst + p;
-            const uint32_t Lq = lcount + p, Lm = Lq - 1;
-            // prefetch w(k), y(k) of the output plane k = q-2 (own tile point)
-            const int k = q - 2;
-            const bool doD = vD && k >= kb && k < ke;
-            T wv[6], yv[6];
-#pragma unroll
-            for (int c = 0; c < 6; ++c) {
-                wv[c] = T(0);
-                yv[c] = T(0);
-            }
-            if (doD) {
-                const int64_t go = gD + (int64_t)k * D.plane;
-#pragma unroll
-                for (int c = 0; c < 6; ++c) wv[c] = win[go + c * D.cs];
-                if (!init) {
-#pragma unroll
-                    for (int c = 0; c < 6; ++c) yv[c] = y[go + c * D.cs];
-                }
-            }
-            if (p == 1) mbar_wait(&bars[Lm % S], (Lm / S) & 1);
-            mbar_wait(&bars[Lq % S], (Lq / S) & 1);
-            const T *Pq = stages + (Lq % S) * SZ;         // w plane q
-            const T *Pm = stages + (Lm % S) * SZ;         // w plane q-1
-            // ---- A: u1_e(q) on E1, u1_h(q-1) on H1 ----
-            if (hasA) {
-                T *ue = U1E + (((q % 3) + 3) % 3) * 3 * G::R1;
-                T *uh = U1H + ((((q - 1) % 2) + 2) % 2) * 3 * G::R1;
-                {
-                    T c0, c1, c2;
-                    curlT_stage<T, G>(Pq, Pm, sE1, c0, c1, c2);
-                    const bool vk = vE1 && q >= 0 && q < D.nz;
-                    ue[tid] = (vk && jE1 > 0 && q > 0) ? bEk(0, q) * c0 : T(0);
-                    ue[G::R1 + tid] = (vk && iE1 > 0 && q > 0) ? bEk(1, q) * c1 : T(0);
-                    ue[2 * G::R1 + tid] = (vk && iE1 > 0 && jE1 > 0) ? bEk(2, q) * c2 : T(0);
-                }
-                {
-                    T c0, c1, c2;
-                    curl_stage<T, G>(Pm, Pq, sH1, c0, c1, c2);
-                    const int kq = q - 1;
-                    const bool vk = vH1 && kq >= 0 && kq < D.nz;
-                    uh[tid] = (vk && iH1 > 0) ? -(bH0 * c0) : T(0);
-                    uh[G::R1 + tid] = (vk && jH1 > 0) ? -(bH1 * c1) : T(0);
-                    uh[2 * G::R1 + tid] = (vk && kq > 0) ? -(bH2 * c2) : T(0);
-                }
-            }
-            __syncthreads();
-            // ---- B: w1(q-1) on W1 ----
-            if (hasB) {
-                const int kq = q - 1;
-                const T *ue0 = U1E + ((((kq) % 3) + 3) % 3) * 3 * G::R1;      // u1_e(q-1)
-                const T *ue1 = U1E + (((q % 3) + 3) % 3) * 3 * G::R1;         // u1_e(q)
-                const T *uh0 = U1H + ((((kq) % 2) + 2) % 2) * 3 * G::R1;      // u1_h(q-1)
-                const T *uhm = U1H + ((((kq - 1) % 2) + 2) % 2) * 3 * G::R1;  // u1_h(q-2)
-                // W1 point (bx, by) in E1 local coords: (bx, by); in H1 local: (bx+1, by+1)
-                const int re = by * G::X1 + bx;
-                const int rh = (by + 1) * G::X1 + bx + 1;
-                const bool vk = vW && kq >= 0 && kq < D.nz;
-                // w1_h = -bH C u1_e + e1 w_h
-                const T ux0 = ue0[re], uy0 = ue0[G::R1 + re], uz0 = ue0[2 * G::R1 + re];
-                const T uz_jp = ue0[2 * G::R1 + re + G::X1], ux_jp = ue0[re + G::X1];
-                const T uz_ip = ue0[2 * G::R1 + re + 1], uy_ip = ue0[G::R1 + re + 1];
-                const T ux_kp = ue1[re], uy_kp = ue1[G::R1 + re];
-                const T c0 = ((uy0 + uz_jp) - uy_kp) - uz0;
-                const T c1 = ((uz0 + ux_kp) - uz_ip) - ux0;
-                const T c2 = ((ux0 + uy_ip) - ux_jp) - uy0;
-                // w1_e = bE C^T u1_h + e1 w_e
-                const T hx0 = uh0[rh], hy0 = uh0[G::R1 + rh], hz0 = uh0[2 * G::R1 + rh];
-                const T hz_jm = uh0[2 * G::R1 + rh - G::X1], hx_jm = uh0[rh - G::X1];
-                const T hz_im = uh0[2 * G::R1 + rh - 1], hy_im = uh0[G::R1 + rh - 1];
-                const T hy_km = uhm[G::R1 + rh], hx_km = uhm[rh];
-                const T d0 = ((hz0 - hz_jm) - hy0) + hy_km;
-                const T d1 = ((hx0 - hx_km) - hz0) + hz_im;
-                const T d2 = ((hy0 - hy_im) - hx0) + hx_jm;
-                const T w0 = Pm[sW], w1v = Pm[G::PL + sW], w2v = Pm[2 * G::PL + sW];
-                const T w3 = Pm[3 * G::PL + sW], w4 = Pm[4 * G::PL + sW], w5 = Pm[5 * G::PL + sW];
-                T *wo = W1 + ((((kq) % 2) + 2) % 2) * 6 * G::RW;
-                const bool kp = kq > 0;
-                wo[by * G::XW + bx] = ((vk && jW > 0 && kp) ? bEk(0, kq) * d0 : T(0)) + e1 * w0;
-                wo[G::RW + by * G::XW + bx] = ((vk && iW > 0 && kp) ? bEk(1, kq) * d1 : T(0)) + e1 * w1v;
-                wo[2 * G::RW + by * G::XW + bx] = ((vk && iW > 0 && jW > 0) ? bEk(2, kq) * d2 : T(0)) + e1 * w2v;
-                wo[3 * G::RW + by * G::XW + bx] = ((vk && iW > 0) ? -(bH0 * c0) : T(0)) + e1 * w3;
-                wo[4 * G::RW + by * G::XW + bx] = ((vk && jW > 0) ? -(bH1 * c1) : T(0)) + e1 * w4;
-                wo[5 * G::RW + by * G::XW + bx] = ((vk && kp) ? -(bH2 * c2) : T(0)) + e1 * w5;
-            }
-            __syncthreads();
-            // plane q-1 of the stage is consumed: refill its slot with plane q+S-1
-            if (tid == 0 && p - 1 + S < nplanes) {
-                const uint32_t L = lcount + p - 1 + S;
-                mbar_expect_tx(&bars[L % S], BYTES);
-                tma_load_4d(stages + (L % S) * SZ, &tm_w, &bars[L % S], x0 - G::OX, y0 - 2, zfirst + p - 1 + S, 0);
-            }
-            // ---- C: u2_e(q-1) on E2, u2_h(q-2) on H2 ----
-            if (hasC) {
-                const T *W1a = W1 + ((((q - 1) % 2) + 2) % 2) * 6 * G::RW;   // w1(q-1)
-                const T *W1b = W1 + ((((q - 2) % 2) + 2) % 2) * 6 * G::RW;   // w1(q-2)
-                {   // u2_e(q-1) at E2 (cx, cy) = W1 local (cx+1, cy+1): bE C^T w1_h
-                    const int kq = q - 1;
-                    const int r = (cy + 1) * G::XW + cx + 1;
-                    const T *H1p = W1a + 3 * G::RW, *H0p = W1b + 3 * G::RW;
-                    const T hx0 = H1p[r], hy0 = H1p[G::RW + r], hz0 = H1p[2 * G::RW + r];
-                    const T hz_jm = H1p[2 * G::RW + r - G::XW], hx_jm = H1p[r - G::XW];
-                    const T hz_im = H1p[2 * G::RW + r - 1], hy_im = H1p[G::RW + r - 1];
-                    const T hy_km = H0p[G::RW + r], hx_km = H0p[r];
-                    const T d0 = ((hz0 - hz_jm) - hy0) + hy_km;
-                    const T d1 = ((hx0 - hx_km) - hz0) + hz_im;
-                    const T d2 = ((hy0 - hy_im) - hx0) + hx_jm;
-                    const bool vk = vE2 && kq >= 0 && kq < D.nz;
-                    T *uo = U2E + ((((kq) % 2) + 2) % 2) * 3 * G::R2;
-                    uo[tid] = (vk && jE2 > 0 && kq > 0) ? bEk(0, kq) * d0 : T(0);
-                    uo[G::R2 + tid] = (vk && iE2 > 0 && kq > 0) ? bEk(1, kq) * d1 : T(0);
-                    uo[2 * G::R2 + tid] = (vk && iE2 > 0 && jE2 > 0) ? bEk(2, kq) * d2 : T(0);
-                }
-                {   // u2_h(q-2) at H2 (cx, cy) = W1 local (cx, cy): -bH C w1_e
-                    const int kq = q - 2;
-                    const int r = cy * G::XW + cx;
-                    const T *E0p = W1b, *E1p = W1a;
-                    const T ex0 = E0p[r], ey0 = E0p[G::RW + r], ez0 = E0p[2 * G::RW + r];
-                    const T ez_jp = E0p[2 * G::RW + r + G::XW], ex_jp = E0p[r + G::XW];
-                    const T ez_ip = E0p[2 * G::RW + r + 1], ey_ip = E0p[G::RW + r + 1];
-                    const T ex_kp = E1p[r], ey_kp = E1p[G::RW + r];
-                    const T c0 = ((ey0 + ez_jp) - ey_kp) - ez0;
-                    const T c1 = ((ez0 + ex_kp) - ez_ip) - ex0;
-                    const T c2 = ((ex0 + ey_ip) - ex_jp) - ey0;
-                    const bool vk = vH2 && kq >= 0 && kq < D.nz;
-                    T *uo = U2H + ((((kq) % 2) + 2) % 2) * 3 * G::R2;
-                    uo[tid] = (vk && iH2 > 0) ? -(bH0 * c0) : T(0);
-                    uo[G::R2 + tid] = (vk && jH2 > 0) ? -(bH1 * c1) : T(0);
-                    uo[2 * G::R2 + tid] = (vk && kq > 0) ? -(bH2 * c2) : T(0);
-                }
-            }
-            __syncthreads();
-            // ---- D: w2(k), y(k) on the tile, k = q-2 ----
-            if (doD) {
-                const T *ue = U1E + (((k % 3) + 3) % 3) * 3 * G::R1;          // u1_e(k)
-                const T *uh = U1H + (((k % 2) + 2) % 2) * 3 * G::R1;          // u1_h(k)
-                const T *w1 = W1 + (((k % 2) + 2) % 2) * 6 * G::RW;           // w1(k)
-                const T *v0 = U2E + (((k % 2) + 2) % 2) * 3 * G::R2;          // u2_e(k)
-                const T *v1 = U2E + ((((k + 1) % 2) + 2) % 2) * 3 * G::R2;    // u2_e(k+1)
-                const T *g0 = U2H + (((k % 2) + 2) % 2) * 3 * G::R2;          // u2_h(k)
-                const T *gm = U2H + ((((k - 1) % 2) + 2) % 2) * 3 * G::R2;    // u2_h(k-1)
-                const int r1e = (dy + 1) * G::X1 + dx + 1;                     // tile point in E1
-                const int r1h = (dy + 2) * G::X1 + dx + 2;                     // tile point in H1
-                const int rw = (dy + 1) * G::XW + dx + 1;                      // in W1
-                const int r2e = dy * G::X2 + dx;                               // in E2
-                const int r2h = (dy + 1) * G::X2 + dx + 1;                     // in H2
-                const T u1v[6] = {ue[r1e], ue[G::R1 + r1e], ue[2 * G::R1 + r1e],
-                                  uh[r1h], uh[G::R1 + r1h], uh[2 * G::R1 + r1h]};
-                T w1v[6];
-#pragma unroll
-                for (int c = 0; c < 6; ++c) w1v[c] = w1[c * G::RW + rw];
-                const T u2v[6] = {v0[r2e], v0[G::R2 + r2e], v0[2 * G::R2 + r2e],
-                                  g0[r2h], g0[G::R2 + r2h], g0[2 * G::R2 + r2h]};
-                // w2_h = -bH C u2_e + e2 w1_h
-                const T ux0 = u2v[0], uy0 = u2v[1], uz0 = u2v[2];
-                const T uz_jp = v0[2 * G::R2 + r2e + G::X2], ux_jp = v0[r2e + G::X2];
-                const T uz_ip = v0[2 * G::R2 + r2e + 1], uy_ip = v0[G::R2 + r2e + 1];
-                const T ux_kp = v1[r2e], uy_kp = v1[G::R2 + r2e];
-                const T c0 = ((uy0 + uz_jp) - uy_kp) - uz0;
-                const T c1 = ((uz0 + ux_kp) - uz_ip) - ux0;
-                const T c2 = ((ux0 + uy_ip) - ux_jp) - uy0;
-                // w2_e = bE C^T u2_h + e2 w1_e
-                const T hx0 = u2v[3], hy0 = u2v[4], hz0 = u2v[5];
-                const T hz_jm = g0[2 * G::R2 + r2h - G::X2], hx_jm = g0[r2h - G::X2];
-                const T hz_im = g0[2 * G::R2 + r2h - 1], hy_im = g0[G::R2 + r2h - 1];
-                const T hy_km = gm[G::R2 + r2h], hx_km = gm[r2h];
-                const T d0 = ((hz0 - hz_jm) - hy0) + hy_km;
-                const T d1 = ((hx0 - hx_km) - hz0) + hz_im;
-                const T d2 = ((hy0 - hy_im) - hx0) + hx_jm;
-                const bool kp = k > 0;
-                T wn[6];
-                wn[0] = ((jD > 0 && kp) ? bEk(0, k) * d0 : T(0)) + e2 * w1v[0];
-                wn[1] = ((iD > 0 && kp) ? bEk(1, k) * d1 : T(0)) + e2 * w1v[1];
-                wn[2] = ((iD > 0 && jD > 0) ? bEk(2, k) * d2 : T(0)) + e2 * w1v[2];
-                wn[3] = ((iD > 0) ? -(bH0 * c0) : T(0)) + e2 * w1v[3];
-                wn[4] = ((jD > 0) ? -(bH1 * c1) : T(0)) + e2 * w1v[4];
-                wn[5] = (kp ? -(bH2 * c2) : T(0)) + e2 * w1v[5];
-                const int64_t go = gD + (int64_t)k * D.plane;
-#pragma unroll
-                for (int c = 0; c < 6; ++c) {
-                    T yn = (yv[c] + a1 * wv[c]) + b1 * u1v[c];
-                    yn = (yn + a2 * w1v[c]) + b2 * u2v[c];
-                    if (LAST) yn = yn + c2 * wn[c];
-                    else wout[go + c * D.cs] = wn[c];
-                    y[go + c * D.cs] = yn;
-                }
-            }
-            __syncthreads();
-        }
-        lcount += nplanes;
-    }
-}
-
-// ---------------------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -921,7 +627,7 @@ static int num_sms() {
 
 // choose the z-chunk so that units / resident CTAs is close to an integer and halo planes
 // (2 per chunk) stay a small fraction
-static Sched make_sched(const Grid &g, int BX, int BY, int resident, int halo = 2) {
+static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
     Sched s;
     s.tiles_x = (g.nx + BX - 1) / BX;
     s.tiles_y = (g.ny + BY - 1) / BY;
@@ -935,7 +641,7 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident, int halo = 
         const double waves = units / resident;
         const double eff_waves = std::ceil(waves);
         // cost ~ rounds * (chunk + 2 halo planes)
-        const double cost = eff_waves * (double)(ch + halo);
+        const double cost = eff_waves * (double)(ch + 2);
         if (cost < best - 1e-9) {
             best = cost;
             bc = ch;
@@ -1094,84 +800,11 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     return check_cuda("poly fused");
 }
 
-// K2x2 launcher: the plan's ops in groups of two (a leading odd op runs on K2).
-template <typename T, int EM, int S>
-static int poly_fused2_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
-    constexpr int BX = 32, BY = 8;
-    using G = Geo2<T, BX, BY>;
-    constexpr int A = 128 / (int)sizeof(T);
-    constexpr int SZ = ((6 * G::PL + A - 1) / A) * A;
-    constexpr size_t smem = (size_t)(S * SZ + G::RING) * sizeof(T) + 8 * S + 16;
-    const Grid &g = *ka.g;
-    auto kmid = pair2_fused_kernel<T, EM, BX, BY, S, false>;
-    auto klast = pair2_fused_kernel<T, EM, BX, BY, S, true>;
-    static const int per_sm = resident_per_sm(kmid, G::NTHR, smem);
-    static const int per_sm2 = resident_per_sm(klast, G::NTHR, smem);
-    if (per_sm < 1 || per_sm2 < 1) return fail(PARAEXP_ECUDA, "fused pair2 kernel does not fit on an SM");
-    Sched sch = make_sched(g, BX, BY, per_sm * num_sms(), 4);
-    const int grid = std::min(sch.units, per_sm * num_sms());
-    auto D = make_dev<T>(g);
-    auto cf = make_coef<T, EM, false>(g, plan.sigma);
-    cudaStream_t s = (cudaStream_t)ka.stream;
-    const size_t nops = plan.ops.size();
-    size_t q0 = 0;
-    int init = 1;
-    if (nops % 2 == 1) {
-        // leading single pair on K2 (keeps the final 'last' op inside a K2x2 launch)
-        Plan one = plan;
-        one.ops.assign(plan.ops.begin(), plan.ops.begin() + 1);
-        int rc = poly_fused_V<T, EM, false, 3, false>(ka, one, bufs);
-        if (rc) return rc;
-        // poly_fused_V returns bufs = {y, w, spare, spare2}
-        std::swap(bufs[0], bufs[1]);                    // -> {w, y, ...}
-        q0 = 1;
-        init = 0;
-    }
-    T *w = (T *)bufs[0], *yy = (T *)bufs[1], *sp = (T *)bufs[2], *sp2 = (T *)bufs[3];
-    CUtensorMap tmW, tmS;
-    int rc;
-    if ((rc = make_map<T>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
-    if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
-    for (size_t q = q0; q + 1 < nops; q += 2) {
-        const Op &o1 = plan.ops[q], &o2 = plan.ops[q + 1];
-        const bool last = o2.kind == 2;
-        (last ? klast : kmid)<<<grid, G::NTHR, smem, s>>>(tmW, D, cf, w, sp, yy, sch, T(o1.a), T(o1.b), T(o1.e2),
-                                                          T(o2.a), T(o2.b), T(o2.e2), T(o2.c), init);
-        ++*ka.launches;
-        if (!last) {
-            std::swap(w, sp);
-            std::swap(tmW, tmS);
-        }
-        init = 0;
-    }
-    bufs[0] = yy;
-    bufs[1] = w;
-    bufs[2] = sp;
-    bufs[3] = sp2;
-    return check_cuda("poly fused2");
-}
-
-static bool use_pair2() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PARAEXP_PAIR2");
-        v = (e && atoi(e) == 0) ? 0 : 1;
-    }
-    return v == 1;
-}
-
 int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     return with_types(*ka.g, plan.sigma, [&](auto tT, auto tEM, auto tHA) {
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
-        if constexpr (EM != 2 && !HA) {
-            // K2x2 when every op but a leading one pairs up and the plan has >= 2 ops of
-            // kinds pair/last (m = 1 'half' stays on K2)
-            bool ok = use_pair2() && plan.ops.size() >= 2;
-            for (const Op &o : plan.ops) ok = ok && o.kind != 1;
-            if (ok) return poly_fused2_V<T, EM, 3>(ka, plan, bufs);
-        }
         if (onebar()) return poly_fused_V<T, EM, HA, 4, true>(ka, plan, bufs);
         switch (pair_stages(sizeof(T) == 8)) {
             case 2: return poly_fused_V<T, EM, HA, 2, false>(ka, plan, bufs);
