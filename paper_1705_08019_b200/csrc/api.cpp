@@ -759,7 +759,10 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
     if ((rc = k_check_finite_async(ka, W, dflag + p + 1))) return rc;
 
     // a8: sum the tails onto the root
-    if (world > 1) {
+    // the collectives also run for a one-rank communicator when PARAEXP_FORCE_COLLECTIVES is
+    // set, so the NCCL code path can be exercised on a single GPU (tests)
+    const bool coll = comm && (world > 1 || getenv("PARAEXP_FORCE_COLLECTIVES"));
+    if (coll) {
         const int id = ev.open(2);
         const int dt = G.dtype == PARAEXP_F64 ? kNcclF64 : kNcclF32;
         if ((rc = nccl_check(g_nccl.Reduce(W, W, (size_t)G.L.state_elems(), dt, kNcclSum, root,
@@ -776,7 +779,7 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
         if (tr.np > 0 && (rc = k_gather(ka, X[0], tr, tr.probe + (int64_t)(p - 1) * tr.np, 0))) return rc;
         if (tr.energy && (rc = k_dot_M_async(ka, X[0], X[0], tr.energy + (p - 1), G.dt))) return rc;
     }
-    if (tracing && world > 1) {
+    if (tracing && coll) {
         if (tr.np > 0 && (rc = nccl_check(g_nccl.AllReduce(tr.probe, tr.probe, (size_t)p * tr.np, kNcclF64, kNcclSum,
                                                           comm->comm, (cudaStream_t)stream), "ncclAllReduce"))) return rc;
         if (tr.energy && (rc = nccl_check(g_nccl.AllReduce(tr.energy, tr.energy, (size_t)p, kNcclF64, kNcclSum,
@@ -793,7 +796,7 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
             if ((rc = k_axpy(ka, P, W, 1.0))) return rc;
         }
     }
-    if (broadcast_out && world > 1) {
+    if (broadcast_out && coll) {
         const int dt = G.dtype == PARAEXP_F64 ? kNcclF64 : kNcclF32;
         if ((rc = nccl_check(g_nccl.Broadcast(P, P, (size_t)G.L.state_elems(), dt, root, comm->comm,
                                              (cudaStream_t)stream), "ncclBroadcast"))) return rc;

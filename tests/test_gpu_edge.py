@@ -88,3 +88,30 @@ def test_rho_pow_bounds():
     lg2 = pe.Grid(32, 32, 32, d0=1e-3, eps_r=eps, dt_frac=0.95)
     inf2 = lg2.info(compute_rho_pow=True)
     assert 0.6 * inf2["rho_cfl"] < inf2["rho_pow"] < 0.85 * inf2["rho_cfl"]
+
+
+def test_nccl_path_one_rank(monkeypatch):
+    """a8 on one GPU: a one-rank NCCL communicator with the collectives forced on
+    (PARAEXP_FORCE_COLLECTIVES: ncclReduce of W, ncclAllReduce of the trace rows,
+    ncclBroadcast of the output) gives the same result as the communicator-free solve."""
+    import torch
+    monkeypatch.setenv("PARAEXP_FORCE_COLLECTIVES", "1")
+    n = (24, 16, 9)
+    og = fit.Grid(*n, d0=1e-3, dt_frac=0.9)
+    lg = pe.Grid(*n, d0=1e-3, dt_frac=0.9)
+    u0 = inputs(og, *random_fields(*n, seed=12))
+    src = [gauss_sine(2, 5, 5, 4, f0=60e9, bw=60e9)]
+    comm = pe.Comm(0, 1, 0, id_bytes=pe.Comm.unique_id())
+    outs = []
+    for c in (None, comm):
+        eo = torch.zeros(3 * lg.npts, dtype=torch.float64, device="cuda:0")
+        ho = torch.zeros_like(eo)
+        u = (torch.tensor(u0[0], device="cuda:0"), torch.tensor(u0[1], device="cuda:0"))
+        st, en, pr = pe.solve_trace(lg, 40, 4, src, u0=u, m=16, s=3, rho=og.rho_cfl, e_out=eo,
+                                    h_out=ho, probes=[(2, 5, 5, 4)], comm=c, broadcast_out=True)
+        torch.cuda.synchronize()
+        outs.append((eo.cpu().numpy(), ho.cpu().numpy(), en.cpu().numpy(), pr.cpu().numpy(), st))
+    for a, b in zip(outs[0][:4], outs[1][:4]):
+        assert np.array_equal(a, b)
+    assert outs[1][4]["ms_reduce"] > 0          # the collective ran
+    comm.close()
