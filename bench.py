@@ -119,6 +119,21 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------
+TRAFFIC_FILES = {("expmv_pair", "C3-f64-p8"): "profiles/r1_ncu_full_pair_c3_f64.json",
+                 ("leapfrog", "C3-f64-p8"): "profiles/r1_ncu_full_leapfrog_c3_f64.json"}
+
+
+def committed_traffic(kernel, w):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from the
+    committed `ncu --set full` summary of the same kernel on the same grid (or None)."""
+    path = TRAFFIC_FILES.get((kernel, w.name))
+    if not path or not os.path.exists(os.path.join(ROOT, path)):
+        return None, None
+    d = json.load(open(os.path.join(ROOT, path)))
+    vals = [x["dram_bytes"] for x in d]
+    return sum(vals) / len(vals), path
+
+
 def cpu_baseline(w, budget_steps=None):
     """The oracle as it stands, on the host cores, on a bounded sample of the workload:
     leapfrog steps + one degree-8 Leja substep on the full grid (cell-updates/s)."""
@@ -199,7 +214,17 @@ def main():
     grid = pe.Grid.from_workload(w, device=local, kernels=args.kernels)
     stream = torch.cuda.current_stream(local)
     info = grid.info(compute_rho_pow=True, stream=stream.cuda_stream)
-    comm = pe.Comm(rank, world, local) if world > 1 else None
+    # BENCH_FORCE_COMM=1: create the library's NCCL communicator (and run its collectives via
+    # PARAEXP_FORCE_COLLECTIVES) even at world size 1 -- exercises the multi-rank path on 1 GPU
+    force_comm = os.environ.get("BENCH_FORCE_COMM") == "1"
+    if force_comm:
+        os.environ["PARAEXP_FORCE_COLLECTIVES"] = "1"
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            dist.init_process_group("nccl", rank=rank, world_size=world,
+                                    device_id=torch.device("cuda", local))
+    comm = pe.Comm(rank, world, local) if (world > 1 or force_comm) else None
     tdt = grid.torch_dtype()
     e_out = torch.zeros(3 * grid.npts, dtype=tdt, device=f"cuda:{local}")
     h_out = torch.zeros_like(e_out)
@@ -254,7 +279,8 @@ def main():
         ms, cu, launches = ms_local, float(cu_local), launches_local
     value = cu / (ms * 1e-3)
 
-    # ---- e2e through the public API with host buffers (pinned), D2H of the result ----
+    # ---- e2e: the same C-ABI call with HOST buffers (pinned): the library copies u0 in and
+    # (e_out, h_out) out inside the call, inside the timed region ----
     e_host = torch.empty(3 * grid.npts, dtype=tdt, pin_memory=True)
     h_host = torch.empty_like(e_host)
     u0_host = None
@@ -269,18 +295,13 @@ def main():
     h2d = d2h = 0
     q_bytes = w.nsteps * len(w.sources) * (8 if w.dtype == "f64" else 4)
     for _ in range(args.steps):
-        ud = None
         if u0_host is not None:
-            ud = (u0_host[0].to(f"cuda:{local}", non_blocking=True),
-                  u0_host[1].to(f"cuda:{local}", non_blocking=True))
             h2d += 2 * u0_host[0].numel() * u0_host[0].element_size()
-        st = pe.solve(grid, w.nsteps, w.p, u0=ud, e_out=e_out, h_out=h_out, **kw)
+        st = pe.solve(grid, w.nsteps, w.p, u0=u0_host, e_out=e_host, h_out=h_host, **kw)
         h2d += q_bytes           # the library uploads the source amplitude table every call
         cu_e2e += st["cell_updates"]
         if rank == st["root"]:
-            e_host.copy_(e_out, non_blocking=True)
-            h_host.copy_(h_out, non_blocking=True)
-            d2h += 2 * e_out.numel() * e_out.element_size()
+            d2h += 2 * e_host.numel() * e_host.element_size()
     e2e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -317,7 +338,8 @@ def main():
 
     # ---- roofline of the dominant kernel family (HBM bound) ----
     es = 8 if w.dtype == "f64" else 4
-    per_cell = {0: 12, 1: 12, 2: 15}[info["material_mode"]]   # values per cell-update
+    # values per cell-update: 12 state values; a per-edge material array adds 3
+    # (leapfrog reads cE once per step) or 1.5 (a pair reads it once per 2 A-applications)
     peak, peak_kind = hbm_peak()
     fam = []
     if lf_ms > 0 and lf_steps > 0:
@@ -325,10 +347,15 @@ def main():
     if poly_ms > 0 and a_apps > 0:
         fam.append(("expmv_pair", poly_ms, a_apps))
     name, fam_ms, units = max(fam, key=lambda f: f[1])
-    bytes_per_unit = per_cell * es * w.cells
+    arr = info["material_mode"] == 2
+    per_cell = 12 + ((3 if name == "leapfrog" else 1.5) if arr else 0)
+    bytes_per_unit = int(per_cell * es * w.cells)
     achieved = bytes_per_unit * units / (fam_ms * 1e-3) / 1e9
+    traffic, traffic_src = committed_traffic(name, w)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "kernel": name,
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": bytes_per_unit * (2 if name == "expmv_pair" else 1),
+                "kernel": name,
                 "peak_kind": peak_kind,
                 "algorithmic_bytes_per_cell_update": per_cell * es,
                 "share_of_step": fam_ms / ms_local if ms_local else None,
@@ -344,7 +371,8 @@ def main():
                    "rho": stats[-1]["rho"], "m": stats[-1]["m"], "s_per_subinterval": stats[-1]["s_first"],
                    "material_mode": info["material_mode"], "kernels": args.kernels,
                    "parallelism": f"paraexp time-parallel x{world}",
-                   "l2": "inputs larger than L2 (815 MB/state fp64), no flush"},
+                   "l2": (f"inputs larger than L2 ({6 * w.cells * es / 1e6:.0f} MB per state vector "
+                          f"vs 126 MB L2), no flush")},
         "per_gpu": value / world,
         "paraexp": {"wall_ms": ms / args.steps, "serial_leapfrog_ms": serial_ms,
                     "speedup_vs_serial_leapfrog": (serial_ms / (ms / args.steps)) if serial_ms else None,

@@ -18,12 +18,16 @@
  *  Dead DOFs  PEC edges (tangential on the box, edges of PEC cells), virtual edges/faces
  *             and boundary-normal faces are ZEROED by the library on input and are
  *             always written as 0 (reading 5).
- *  Pointers   Field pointers passed to leapfrog/expmv/solve are caller-owned DEVICE
- *             pointers on the grid's device (e.g. torch tensors), unless stated.  The
- *             library never frees them.  `stream` is a cudaStream_t (NULL = legacy
- *             default stream); all device work is stream-ordered on it and the call
- *             returns after enqueue unless it must read back a status flag (then it
- *             synchronises that stream).
+ *  Pointers   Field pointers passed to leapfrog/expmv/solve are caller-owned pointers
+ *             to DEVICE memory on the grid's device (e.g. torch tensors) or to HOST memory
+ *             (pinned or pageable; told apart with cudaPointerGetAttributes).  Host fields
+ *             are copied through library-owned canonical-layout device buffers
+ *             (cudaMemcpyAsync on `stream`) and the call synchronises `stream` before it
+ *             returns.  The library never frees caller memory.  `stream` is a
+ *             cudaStream_t (NULL = legacy default stream); all device work is
+ *             stream-ordered on it and, with device fields, the call returns after
+ *             enqueue unless it must read back a status flag (then it synchronises).
+ *             Trace outputs (paraexp_trace) are device pointers.
  *  Errors     0 = PARAEXP_OK, negative = error (see codes), positive = warning bits.
  *             paraexp_last_error() returns a thread-local message for the last failure.
  *             On error the output buffers are unspecified.

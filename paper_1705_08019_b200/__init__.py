@@ -121,12 +121,13 @@ def _stream(stream, grid):
 
 
 def _field(t, grid, name, writable=True):
-    """Validate a canonical-layout field tensor and return its device pointer."""
+    """Validate a canonical-layout field tensor and return its pointer: a tensor on the
+    grid's device, or a host (CPU, ideally pinned) tensor that the library stages itself."""
     import torch
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch tensor")
-    if t.device.type != "cuda" or t.device.index != grid.device:
-        raise ValueError(f"{name} must live on cuda:{grid.device}")
+    if t.device.type != "cpu" and (t.device.type != "cuda" or t.device.index != grid.device):
+        raise ValueError(f"{name} must live on cuda:{grid.device} or on the host")
     if t.dtype != grid.torch_dtype() or not t.is_contiguous() or t.numel() != 3 * grid.npts:
         raise ValueError(f"{name} must be a contiguous {grid.torch_dtype()} tensor of 3*npts elements")
     return C.c_void_p(t.data_ptr())

@@ -39,6 +39,59 @@ static int ensure_ws(Grid &G, int n) {
     return PARAEXP_OK;
 }
 
+// ---- host or device field pointers ---------------------------------------------------------
+// Field arguments may be device pointers (stream-ordered, no copy) or host pointers (pinned or
+// pageable): host fields are staged through canonical-layout device buffers with
+// cudaMemcpyAsync and the call synchronises its stream before returning.
+static bool is_device_ptr(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static int ensure_canon(Grid &G) {
+    const size_t bytes = (size_t)3 * G.npts * G.esize();
+    for (int q = 0; q < 2; ++q)
+        if (!G.d_canon[q]) {
+            int rc = dev_alloc(&G.d_canon[q], bytes);
+            if (rc) return rc;
+            G.device_bytes += bytes;
+        }
+    return PARAEXP_OK;
+}
+
+// pack (e, h) from host or device into the device state; *host_io |= any host pointer
+static int pack_any(const KernelArgs &ka, Grid &G, const void *e, const void *h, void *state, bool *host_io) {
+    const bool de = is_device_ptr(e), dh = is_device_ptr(h);
+    if (de && dh) return k_pack(ka, e, h, state);
+    int rc = ensure_canon(G);
+    if (rc) return rc;
+    const size_t bytes = (size_t)3 * G.npts * G.esize();
+    if (!de && (rc = dev_memcpy_h2d_async(G.d_canon[0], e, bytes, ka.stream))) return rc;
+    if (!dh && (rc = dev_memcpy_h2d_async(G.d_canon[1], h, bytes, ka.stream))) return rc;
+    *host_io = true;
+    return k_pack(ka, de ? e : G.d_canon[0], dh ? h : G.d_canon[1], state);
+}
+
+// unpack the device state into (e, h) on host or device
+static int unpack_any(const KernelArgs &ka, Grid &G, const void *state, void *e, void *h, bool *host_io) {
+    const bool de = is_device_ptr(e), dh = is_device_ptr(h);
+    if (de && dh) return k_unpack(ka, state, e, h);
+    int rc = ensure_canon(G);
+    if (rc) return rc;
+    const size_t bytes = (size_t)3 * G.npts * G.esize();
+    if ((rc = k_unpack(ka, state, de ? e : G.d_canon[0], dh ? h : G.d_canon[1]))) return rc;
+    *host_io = true;
+    if (!de && cudaMemcpyAsync(e, G.d_canon[0], bytes, cudaMemcpyDeviceToHost, (cudaStream_t)ka.stream) != cudaSuccess)
+        return check_cuda("memcpy d2h");
+    if (!dh && cudaMemcpyAsync(h, G.d_canon[1], bytes, cudaMemcpyDeviceToHost, (cudaStream_t)ka.stream) != cudaSuccess)
+        return check_cuda("memcpy d2h");
+    return PARAEXP_OK;
+}
+
 // ---- sources (reading 6, 24) ---------------------------------------------------------------
 static double waveform(const paraexp_source &s, double t) {
     switch (s.kind) {
@@ -465,12 +518,14 @@ static int leapfrog_impl(paraexp_grid *grid, const paraexp_source *src, int32_t 
     Events ev(stream);
     const int id = ev.open(4);
     void *bufs[2] = {G.ws[0], G.ws[1]};
-    if ((rc = k_pack(ka, e, h, bufs[0]))) return rc;
+    bool host_io = false;
+    if ((rc = pack_any(ka, G, e, h, bufs[0], &host_io))) return rc;
     const int id5 = ev.open(5);
     if ((rc = k_leapfrog(ka, bufs, nsteps, (const SrcDev *)G.d_src, nsrc, G.d_q, tracing ? &tr : nullptr))) return rc;
     ev.close(id5);
-    if ((rc = k_unpack(ka, bufs[0], e, h))) return rc;
+    if ((rc = unpack_any(ka, G, bufs[0], e, h, &host_io))) return rc;
     ev.close(id);
+    if (host_io && (rc = dev_sync(stream))) return rc;
     S.leapfrog_steps = nsteps;
     S.curl_applications = 2 * nsteps;
     S.cell_updates = nsteps * (int64_t)G.nx * G.ny * G.nz;
@@ -527,9 +582,10 @@ int paraexp_expmv(paraexp_grid *grid, double tau, const paraexp_expmv_opts *opts
     Events ev(stream);
     const int id = ev.open(4);
     void *bufs[4] = {G.ws[0], G.ws[1], G.ws[2], G.ws[3]};
-    if ((rc = k_pack(ka, e, h, bufs[0]))) return rc;
+    bool host_io = false;
+    if ((rc = pack_any(ka, G, e, h, bufs[0], &host_io))) return rc;
     if ((rc = run_plan(ka, plan, bufs, &S, &ev))) return rc;
-    if ((rc = k_unpack(ka, bufs[0], e, h))) return rc;
+    if ((rc = unpack_any(ka, G, bufs[0], e, h, &host_io))) return rc;
     ev.close(id);
     S.rho = rho;
     S.method = plan.method;
@@ -677,6 +733,7 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
     Events ev(stream);
     const int idt = ev.open(4);
 
+    bool host_io = false;       // host-pointer fields (staged copies; the call syncs anyway)
     void *P = G.ws[0];          // particular state of the current sub-interval
     void *W = G.ws[1];          // Horner accumulator of the tails
     void *X[3] = {G.ws[2], G.ws[3], G.ws[4]};
@@ -716,7 +773,7 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
 
     if (first >= 1) {
         if (first == 1 && has_u0) {
-            if ((rc = k_pack(ka, e0, h0, W))) return rc;
+            if ((rc = pack_any(ka, G, e0, h0, W, &host_io))) return rc;
             if (tail_mode == PARAEXP_TAIL_LEAPFROG && (rc = k_half_start(ka, W))) return rc;
             W_valid = true;
         }
@@ -802,7 +859,7 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
                                              (cudaStream_t)stream), "ncclBroadcast"))) return rc;
     }
     if ((rank == root || broadcast_out) && e_out && h_out) {
-        if ((rc = k_unpack(ka, P, e_out, h_out))) return rc;
+        if ((rc = unpack_any(ka, G, P, e_out, h_out, &host_io))) return rc;
     }
     ev.close(idf);
     ev.close(idt);

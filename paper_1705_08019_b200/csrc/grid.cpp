@@ -230,6 +230,9 @@ void grid_free_device(Grid &G) {
     dev_free(G.d_red);
     dev_free(G.d_src);
     dev_free(G.d_q);
+    dev_free(G.d_canon[0]);
+    dev_free(G.d_canon[1]);
+    G.d_canon[0] = G.d_canon[1] = nullptr;
     G.d_cE_tab = G.d_cE_arr = G.d_cH_arr = G.d_flag = G.d_red = G.d_src = G.d_q = nullptr;
     G.device_bytes = 0;
     G.ws_bytes = 0;

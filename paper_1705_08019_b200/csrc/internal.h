@@ -59,6 +59,7 @@ struct Grid {
     void *d_src = nullptr;      // source descriptors
     std::vector<SrcDev> h_src;  // host copy of the current source descriptors
     void *d_q = nullptr;        // source amplitude table
+    void *d_canon[2] = {nullptr, nullptr};   // canonical-layout staging of host-pointer fields
     int64_t d_q_cap = 0;
     int64_t device_bytes = 0;
     size_t esize() const { return dtype == PARAEXP_F64 ? 8 : 4; }
