@@ -111,8 +111,10 @@ def test_nccl_path_one_rank(monkeypatch):
                                     h_out=ho, probes=[(2, 5, 5, 4)], comm=c, broadcast_out=True)
         torch.cuda.synchronize()
         outs.append((eo.cpu().numpy(), ho.cpu().numpy(), en.cpu().numpy(), pr.cpu().numpy(), st))
-    for a, b in zip(outs[0][:4], outs[1][:4]):
+    for a, b in zip(outs[0][:2] + outs[0][3:4], outs[1][:2] + outs[1][3:4]):   # e, h, probes
         assert np.array_equal(a, b)
+    # energy rows: block partial sums are combined with atomics (order not reproducible)
+    np.testing.assert_allclose(outs[1][2], outs[0][2], rtol=1e-13, atol=0)
     assert outs[1][4]["ms_reduce"] > 0          # the collective ran
     comm.close()
 
