@@ -349,6 +349,186 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
 }
 
 // ---------------------------------------------------------------------------------------
+// K1r: the leapfrog step with row-aligned warps and register-carried own values
+// ---------------------------------------------------------------------------------------
+// Same staging and phases as K1 (ONEBAR = false).  Differences:
+//  * phase-A points are mapped so that warps 0..BY cover whole 32-wide rows (the +1 halo
+//    column x0+BX is handled by the last warp): no warp straddles two rows;
+//  * the thread of tile point (tx, ty) is the phase-A thread of the same point, so phase B
+//    takes e'(k), e'(k+1) and h(k) at its own point from registers (only the four i+1 / j+1
+//    neighbours of e'(k) are read from shared memory), and phase A carries h(k) at its own
+//    point from the previous plane (only h(k+1) and its i-1 / j-1 neighbours are read).
+template <typename T, int EM, bool HA, int BX, int BY, int S, bool TR>
+__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_r_kernel(
+    const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
+    const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ out,
+    Sched sch, SrcList src, const T *__restrict__ q, const __grid_constant__ TraceDev tr) {
+    using G = Geo<T, BX, BY>;
+    using SL = StageL<T, EM, HA, G>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T *stages = reinterpret_cast<T *>(smem_raw);
+    T *ring = stages + S * SL::SZ;                       // [2][3][EY][EX] e' planes
+    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(ring + 2 * 3 * G::RP) + 15) & ~uintptr_t(15));
+    const int tid = threadIdx.x;
+    constexpr int MAIN = BX * G::EY;                      // row-aligned phase-A points
+    const bool hasA = tid < G::RP;
+    const int ii = tid < MAIN ? tid % BX : BX, jj = tid < MAIN ? tid / BX : tid - MAIN;
+    const int rA = jj * G::EX + ii;                       // ring index of the phase-A point
+    const int sA = (jj + 1) * G::WX + ii + G::OX;         // stage index of the phase-A point
+    const bool tileA = ii < BX && jj < BY;                // == phase-B thread of the same point
+    T bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
+    const T bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
+    if (tid == 0) {
+        for (int s2 = 0; s2 < S; ++s2) mbar_init(&bars[s2], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    uint32_t lcount = 0;
+    double eacc = 0.0;
+    for (int unit = blockIdx.x; unit < sch.units; unit += gridDim.x) {
+        const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
+        const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
+        const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
+        const int nplanes = ke - kb + 2;
+        const int iA = x0 + ii, jA = y0 + jj;
+        const bool inA = hasA && iA < D.nx && jA < D.ny;
+        const bool lxA = inA && jA > 0, lyA = inA && iA > 0, lzA = inA && iA > 0 && jA > 0;
+        const bool wrA = inA && tileA;
+        uint32_t smask = 0, pmask = 0;
+        for (int r = 0; r < src.n; ++r)
+            if (inA && src.i[r] == iA && src.j[r] == jA) smask |= 1u << r;
+        if (TR)
+            for (int r = 0; r < tr.np; ++r)
+                if (wrA && tr.i[r] == iA && tr.j[r] == jA) pmask |= 1u << r;
+        T *oA = out + D.idx(wrA ? iA : 0, wrA ? jA : 0, 0);
+        // carried own-point values: h(k) (x, y, z) and e'(k) (x, y, z) of the previous plane
+        T hxk = T(0), hyk = T(0), hzk = T(0), ek0 = T(0), ek1 = T(0), ek2 = T(0);
+        T g0 = bH0, g1 = bH1, g2 = bH2;                    // cH at the own point, plane k (HA)
+        if (tid == 0)
+            for (int p = 0; p < min(S, nplanes); ++p) {
+                const uint32_t L = lcount + p;
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                          &tm_cH, x0, y0, kb - 1 + p);
+            }
+        for (int p = 0; p + 1 < nplanes; ++p) {
+            const int k = kb - 1 + p, kk = k + 1;
+            const uint32_t L0 = lcount + p, L1 = L0 + 1;
+            if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
+            mbar_wait(&bars[L1 % S], (L1 / S) & 1);
+            const T *P0 = stages + (L0 % S) * SL::SZ;
+            const T *P1 = stages + (L1 % S) * SL::SZ;
+            T *R1 = ring + (kk & 1) * 3 * G::RP;
+            const T *R0 = ring + (k & 1) * 3 * G::RP;
+            if (EM == 1 && kk < D.nz) {
+                bE0 = __ldg(cf.tab + kk) * cf.sig;
+                bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
+                bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
+            }
+            if (p == 0 && hasA) {                         // h(kb-1) at the own point
+                hxk = P0[3 * G::PL + sA];
+                hyk = P0[4 * G::PL + sA];
+            }
+            T e0 = T(0), e1 = T(0), e2 = T(0), hx1 = T(0), hy1 = T(0), hz1 = T(0);
+            // ---- phase A: e'(k+1) on the tile and its +1 halo ----
+            if (hasA) {
+                const T *hx = P1 + 3 * G::PL, *hy = P1 + 4 * G::PL, *hz = P1 + 5 * G::PL;
+                hx1 = hx[sA];
+                hy1 = hy[sA];
+                hz1 = hz[sA];
+                const T hz_jm = hz[sA - G::WX], hx_jm = hx[sA - G::WX];
+                const T hz_im = hz[sA - 1], hy_im = hy[sA - 1];
+                const T c0 = ((hz1 - hz_jm) - hy1) + hyk;
+                const T c1 = ((hx1 - hxk) - hz1) + hz_im;
+                const T c2 = ((hy1 - hy_im) - hx1) + hx_jm;
+                const bool vk = kk < D.nz, kp = kk > 0;
+                T w0 = bE0, w1 = bE1, w2 = bE2;
+                if (EM == 2) {
+                    w0 = P1[SL::ST + sA] * cf.sig;
+                    w1 = P1[SL::ST + G::PL + sA] * cf.sig;
+                    w2 = P1[SL::ST + 2 * G::PL + sA] * cf.sig;
+                }
+                e0 = (lxA && vk && kp) ? P1[sA] + w0 * c0 : T(0);
+                e1 = (lyA && vk && kp) ? P1[G::PL + sA] + w1 * c1 : T(0);
+                e2 = (lzA && vk) ? P1[2 * G::PL + sA] + w2 * c2 : T(0);
+                if (smask && vk)
+                    for (int r = 0; r < src.n; ++r)
+                        if (((smask >> r) & 1u) && src.k[r] == kk) {
+                            const int sc = src.c[r];
+                            const T qv = q[r];
+                            if (sc == 0) e0 = e0 - qv;
+                            if (sc == 1) e1 = e1 - qv;
+                            if (sc == 2) e2 = e2 - qv;
+                        }
+                R1[rA] = e0;
+                R1[G::RP + rA] = e1;
+                R1[2 * G::RP + rA] = e2;
+                if (wrA && vk && kk >= kb && kk < ke) {
+                    T *o = oA + (int64_t)kk * D.plane;
+                    o[0] = e0;
+                    o[D.cs] = e1;
+                    o[2 * D.cs] = e2;
+                    if (TR) {
+                        if (w0 != T(0)) eacc += (double)e0 * (double)e0 / (double)w0;
+                        if (w1 != T(0)) eacc += (double)e1 * (double)e1 / (double)w1;
+                        if (w2 != T(0)) eacc += (double)e2 * (double)e2 / (double)w2;
+                        if (pmask)
+                            for (int r = 0; r < tr.np; ++r)
+                                if (((pmask >> r) & 1u) && tr.k[r] == kk)
+                                    tr.probe[r] = (double)(tr.c[r] == 0 ? e0 : (tr.c[r] == 1 ? e1 : e2));
+                    }
+                }
+            }
+            __syncthreads();
+            // ---- phase B: h'(k) on the tile (own e'(k), e'(k+1), h(k) from registers) ----
+            if (k >= kb && wrA) {
+                const T ez_jp = R0[2 * G::RP + rA + G::EX], ex_jp = R0[rA + G::EX];
+                const T ez_ip = R0[2 * G::RP + rA + 1], ey_ip = R0[G::RP + rA + 1];
+                const T c0 = ((ek1 + ez_jp) - e1) - ek2;
+                const T c1 = ((ek2 + e0) - ez_ip) - ek0;
+                const T c2 = ((ek0 + ey_ip) - ex_jp) - ek1;
+                if (HA) {
+                    const int ch = SL::ST + SL::CE;
+                    g0 = P0[ch + sA] * cf.sig;
+                    g1 = P0[ch + G::PL + sA] * cf.sig;
+                    g2 = P0[ch + 2 * G::PL + sA] * cf.sig;
+                }
+                const bool lxB = iA > 0, lyB = jA > 0;
+                const T n0 = lxB ? hxk - g0 * c0 : hxk;
+                const T n1 = lyB ? hyk - g1 * c1 : hyk;
+                const T n2 = k > 0 ? hzk - g2 * c2 : hzk;
+                T *o = oA + (int64_t)k * D.plane + 3 * D.cs;
+                o[0] = n0;
+                o[D.cs] = n1;
+                o[2 * D.cs] = n2;
+                if (TR) {
+                    if (lxB && g0 != T(0)) eacc += (double)hxk * (double)n0 / (double)g0;
+                    if (lyB && g1 != T(0)) eacc += (double)hyk * (double)n1 / (double)g1;
+                    if (k > 0 && g2 != T(0)) eacc += (double)hzk * (double)n2 / (double)g2;
+                }
+            }
+            // carry plane k+1 -> k
+            hxk = hx1;
+            hyk = hy1;
+            hzk = hz1;
+            ek0 = e0;
+            ek1 = e1;
+            ek2 = e2;
+            __syncthreads();
+            if (tid == 0 && p + S < nplanes) {
+                const uint32_t L = lcount + p + S;
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                          &tm_cH, x0, y0, kb - 1 + p + S);
+            }
+        }
+        lcount += nplanes;
+    }
+    if (TR && tr.energy) {
+        const double sum = block_sum(eacc);
+        if (tid == 0 && sum != 0.0) atomicAdd(tr.energy, sum * tr.dt);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // K2: fused Newton pair  u = X w ; y <- (init?0:y) + a w + b u ; [w' = X u + e2 w]
 // ---------------------------------------------------------------------------------------
 // Phase A of iteration k: u_e(k+1) on the +1 halo and u_h(k) on the -1 halo; phase B: the
@@ -576,6 +756,261 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
 }
 
 // ---------------------------------------------------------------------------------------
+// K2r: the Newton pair with one point set and register-carried own values
+// ---------------------------------------------------------------------------------------
+// Every thread owns one point of U = [x0-1, x0+BX] x [y0-1, y0+BY] ((BX+2) x (BY+2)) and
+// computes there u_e(k+1) if the point is in E = [x0, x0+BX] x [y0, y0+BY] and u_h(k) if it is
+// in H = [x0-1, x0+BX-1] x [y0-1, y0+BY-1].  Tile points are threads 0 .. BX*BY-1 (whole
+// 32-wide rows); the 2-cell-wide halo frame follows.  Phase B of a tile thread takes w(k),
+// u_e(k), u_e(k+1), u_h(k), u_h(k-1) at its own point from registers and reads only the four
+// i+1/j+1 neighbours of u_e(k) and the four i-1/j-1 neighbours of u_h(k) from shared memory.
+// Rings: u_e 2 planes, u_h 1 plane (its phase-B readers finish before the next phase A).
+template <typename T, int BX, int BY>
+struct GeoU {
+    static constexpr int XU = BX + 2, YU = BY + 2, RU = XU * YU;
+    static constexpr int NTHR = ((RU + 31) / 32) * 32;
+};
+
+template <typename T, int EM, bool HA, int BX, int BY, int S>
+__global__ void __launch_bounds__(GeoU<T, BX, BY>::NTHR) pair_r_kernel(
+    const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
+    const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
+    T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode) {
+    using G = Geo<T, BX, BY>;
+    using U = GeoU<T, BX, BY>;
+    using SL = StageL<T, EM, HA, G>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T *stages = reinterpret_cast<T *>(smem_raw);
+    T *UE = stages + S * SL::SZ;                         // [2][3][RU]
+    T *UH = UE + 2 * 3 * U::RU;                          // [3][RU]
+    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(UH + 3 * U::RU) + 15) & ~uintptr_t(15));
+    const int tid = threadIdx.x;
+    // own point (ui, uj) in U coordinates: global (x0 - 1 + ui, y0 - 1 + uj)
+    int ui, uj;
+    {
+        constexpr int NT = BX * BY, ROW = BX + 2;
+        if (tid < NT) { ui = 1 + tid % BX; uj = 1 + tid / BX; }
+        else if (tid < NT + ROW) { ui = tid - NT; uj = 0; }
+        else if (tid < NT + 2 * ROW) { ui = tid - NT - ROW; uj = BY + 1; }
+        else if (tid < NT + 2 * ROW + BY) { ui = 0; uj = 1 + (tid - NT - 2 * ROW); }
+        else { ui = BX + 1; uj = 1 + (tid - NT - 2 * ROW - BY); }
+    }
+    const bool has = tid < U::RU;
+    const bool isE = has && ui >= 1 && uj >= 1;          // ui <= BX+1, uj <= BY+1 always
+    const bool isH = has && ui <= BX && uj <= BY;
+    const bool isT = tid < BX * BY;
+    const int r = uj * U::XU + ui;                        // ring index
+    const int sS = uj * G::WX + ui - 1 + G::OX;           // stage index
+    T bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
+    const T bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
+    if (tid == 0) {
+        for (int s2 = 0; s2 < S; ++s2) mbar_init(&bars[s2], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    uint32_t lcount = 0;
+    for (int unit = blockIdx.x; unit < sch.units; unit += gridDim.x) {
+        const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
+        const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
+        const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
+        const int nplanes = ke - kb + 2;
+        const int ig = x0 - 1 + ui, jg = y0 - 1 + uj;
+        const bool in = has && ig >= 0 && jg >= 0 && ig < D.nx && jg < D.ny;
+        const bool inE = in && isE, inH = in && isH;
+        const bool lxE = inE && jg > 0, lyE = inE && ig > 0, lzE = inE && ig > 0 && jg > 0;
+        const bool lxH = inH && ig > 0, lyH = inH && jg > 0;
+        const bool doT = in && isT;
+        const int64_t gB = D.idx(doT ? ig : 0, doT ? jg : 0, 0);
+        // carried own-point values (plane k of the current iteration)
+        T hxk = T(0), hyk = T(0), hzk = T(0);      // w_h(k)
+        T exk = T(0), eyk = T(0);                  // w_e(k) (x, y)
+        T uek0 = T(0), uek1 = T(0), uek2 = T(0);   // u_e(k)
+        T uhm0 = T(0), uhm1 = T(0), uhm2 = T(0);   // u_h(k-1)
+        if (tid == 0)
+            for (int p = 0; p < min(S, nplanes); ++p) {
+                const uint32_t L = lcount + p;
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                          &tm_cH, x0, y0, kb - 1 + p);
+            }
+        for (int p = 0; p + 1 < nplanes; ++p) {
+            const int k = kb - 1 + p, kk = k + 1;
+            const uint32_t L0 = lcount + p, L1 = L0 + 1;
+            const bool doB = doT && k >= kb;
+            T yv0 = T(0), yv1 = T(0), yv2 = T(0), yv3 = T(0), yv4 = T(0), yv5 = T(0);
+            if (doB && !init) {
+                const T *yp = y + gB + (int64_t)k * D.plane;
+                yv0 = yp[0];
+                yv1 = yp[D.cs];
+                yv2 = yp[2 * D.cs];
+                yv3 = yp[3 * D.cs];
+                yv4 = yp[4 * D.cs];
+                yv5 = yp[5 * D.cs];
+            }
+            if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
+            mbar_wait(&bars[L1 % S], (L1 / S) & 1);
+            const T *P0 = stages + (L0 % S) * SL::SZ;
+            const T *P1 = stages + (L1 % S) * SL::SZ;
+            T *UE1 = UE + (kk & 1) * 3 * U::RU;
+            const T *UE0 = UE + (k & 1) * 3 * U::RU;
+            T bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;
+            if (EM == 1) {
+                if (kk < D.nz) {
+                    bE0 = __ldg(cf.tab + kk) * cf.sig;
+                    bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
+                    bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
+                }
+                if (k >= 0) {
+                    bEk0 = __ldg(cf.tab + k) * cf.sig;
+                    bEk1 = __ldg(cf.tab + D.nz + k) * cf.sig;
+                    bEk2 = __ldg(cf.tab + 2 * D.nz + k) * cf.sig;
+                }
+            }
+            if (p == 0 && has) {                          // w(kb-1) at the own point
+                hxk = P0[3 * G::PL + sS];
+                hyk = P0[4 * G::PL + sS];
+                hzk = P0[5 * G::PL + sS];
+                exk = P0[sS];
+                eyk = P0[G::PL + sS];
+            }
+            // ---- phase A ----
+            const T hx1 = has ? P1[3 * G::PL + sS] : T(0), hy1 = has ? P1[4 * G::PL + sS] : T(0);
+            const T hz1 = has ? P1[5 * G::PL + sS] : T(0);
+            const T ex1 = has ? P1[sS] : T(0), ey1 = has ? P1[G::PL + sS] : T(0);
+            const T ezk = has ? P0[2 * G::PL + sS] : T(0);
+            T ue0 = T(0), ue1 = T(0), ue2 = T(0), uh0 = T(0), uh1 = T(0), uh2 = T(0);
+            if (isE) {   // u_e(k+1) = bE C^T w_h at plane k+1
+                const T *hx = P1 + 3 * G::PL, *hy = P1 + 4 * G::PL, *hz = P1 + 5 * G::PL;
+                const T hz_jm = hz[sS - G::WX], hx_jm = hx[sS - G::WX];
+                const T hz_im = hz[sS - 1], hy_im = hy[sS - 1];
+                const T c0 = ((hz1 - hz_jm) - hy1) + hyk;
+                const T c1 = ((hx1 - hxk) - hz1) + hz_im;
+                const T c2 = ((hy1 - hy_im) - hx1) + hx_jm;
+                const bool vk = kk < D.nz, kp = kk > 0;
+                T w0 = bE0, w1 = bE1, w2 = bE2;
+                if (EM == 2) {
+                    w0 = P1[SL::ST + sS] * cf.sig;
+                    w1 = P1[SL::ST + G::PL + sS] * cf.sig;
+                    w2 = P1[SL::ST + 2 * G::PL + sS] * cf.sig;
+                }
+                ue0 = (lxE && vk && kp) ? w0 * c0 : T(0);
+                ue1 = (lyE && vk && kp) ? w1 * c1 : T(0);
+                ue2 = (lzE && vk) ? w2 * c2 : T(0);
+                UE1[r] = ue0;
+                UE1[U::RU + r] = ue1;
+                UE1[2 * U::RU + r] = ue2;
+            }
+            if (isH) {   // u_h(k) = -bH C w_e at plane k
+                const T *ex = P0, *ey = P0 + G::PL, *ez = P0 + 2 * G::PL;
+                const T ez_jp = ez[sS + G::WX], ex_jp = ex[sS + G::WX];
+                const T ez_ip = ez[sS + 1], ey_ip = ey[sS + 1];
+                const T c0 = ((eyk + ez_jp) - ey1) - ezk;
+                const T c1 = ((ezk + ex1) - ez_ip) - exk;
+                const T c2 = ((exk + ey_ip) - ex_jp) - eyk;
+                const bool vk = k >= 0 && k < D.nz;
+                T g0 = bH0, g1 = bH1, g2 = bH2;
+                if (HA) {
+                    const int ch = SL::ST + SL::CE;
+                    g0 = P0[ch + sS] * cf.sig;
+                    g1 = P0[ch + G::PL + sS] * cf.sig;
+                    g2 = P0[ch + 2 * G::PL + sS] * cf.sig;
+                }
+                uh0 = (lxH && vk) ? -(g0 * c0) : T(0);
+                uh1 = (lyH && vk) ? -(g1 * c1) : T(0);
+                uh2 = (inH && vk && k > 0) ? -(g2 * c2) : T(0);
+                UH[r] = uh0;
+                UH[U::RU + r] = uh1;
+                UH[2 * U::RU + r] = uh2;
+            }
+            __syncthreads();
+            if (doB) {
+                T wn0 = T(0), wn1 = T(0), wn2 = T(0), wn3 = T(0), wn4 = T(0), wn5 = T(0);
+                const T w0 = exk, w1 = eyk, w2 = ezk, w3 = hxk, w4 = hyk, w5 = hzk;
+                if (mode != 1) {
+                    // w'_h(k) = -bH C u_e(k) + e2 w_h
+                    const T uz_jp = UE0[2 * U::RU + r + U::XU], ux_jp = UE0[r + U::XU];
+                    const T uz_ip = UE0[2 * U::RU + r + 1], uy_ip = UE0[U::RU + r + 1];
+                    const T c0 = ((uek1 + uz_jp) - ue1) - uek2;
+                    const T c1 = ((uek2 + ue0) - uz_ip) - uek0;
+                    const T c2 = ((uek0 + uy_ip) - ux_jp) - uek1;
+                    // w'_e(k) = bE C^T u_h(k) + e2 w_e
+                    const T hz_jm = UH[2 * U::RU + r - U::XU], hx_jm = UH[r - U::XU];
+                    const T hz_im = UH[2 * U::RU + r - 1], hy_im = UH[U::RU + r - 1];
+                    const T d0 = ((uh2 - hz_jm) - uh1) + uhm1;
+                    const T d1 = ((uh0 - uhm0) - uh2) + hz_im;
+                    const T d2 = ((uh1 - hy_im) - uh0) + hx_jm;
+                    T be0 = bEk0, be1 = bEk1, be2 = bEk2, bh0 = bH0, bh1 = bH1, bh2 = bH2;
+                    if (EM == 2) {
+                        be0 = P0[SL::ST + sS] * cf.sig;
+                        be1 = P0[SL::ST + G::PL + sS] * cf.sig;
+                        be2 = P0[SL::ST + 2 * G::PL + sS] * cf.sig;
+                    }
+                    if (HA) {
+                        const int ch = SL::ST + SL::CE;
+                        bh0 = P0[ch + sS] * cf.sig;
+                        bh1 = P0[ch + G::PL + sS] * cf.sig;
+                        bh2 = P0[ch + 2 * G::PL + sS] * cf.sig;
+                    }
+                    const bool kp = k > 0, lxBe = jg > 0, lyBe = ig > 0, lzBe = ig > 0 && jg > 0;
+                    wn0 = ((lxBe && kp) ? be0 * d0 : T(0)) + e2 * w0;
+                    wn1 = ((lyBe && kp) ? be1 * d1 : T(0)) + e2 * w1;
+                    wn2 = (lzBe ? be2 * d2 : T(0)) + e2 * w2;
+                    wn3 = ((ig > 0) ? -(bh0 * c0) : T(0)) + e2 * w3;
+                    wn4 = ((jg > 0) ? -(bh1 * c1) : T(0)) + e2 * w4;
+                    wn5 = (kp ? -(bh2 * c2) : T(0)) + e2 * w5;
+                }
+                const int64_t go = gB + (int64_t)k * D.plane;
+                if (mode == 0) {
+                    T *wo = wout + go;
+                    wo[0] = wn0;
+                    wo[D.cs] = wn1;
+                    wo[2 * D.cs] = wn2;
+                    wo[3 * D.cs] = wn3;
+                    wo[4 * D.cs] = wn4;
+                    wo[5 * D.cs] = wn5;
+                }
+                T q0 = (yv0 + a * w0) + b * uek0, q1 = (yv1 + a * w1) + b * uek1;
+                T q2 = (yv2 + a * w2) + b * uek2, q3 = (yv3 + a * w3) + b * uh0;
+                T q4 = (yv4 + a * w4) + b * uh1, q5 = (yv5 + a * w5) + b * uh2;
+                if (mode == 2) {
+                    q0 = q0 + cl * wn0;
+                    q1 = q1 + cl * wn1;
+                    q2 = q2 + cl * wn2;
+                    q3 = q3 + cl * wn3;
+                    q4 = q4 + cl * wn4;
+                    q5 = q5 + cl * wn5;
+                }
+                T *yo = y + go;
+                yo[0] = q0;
+                yo[D.cs] = q1;
+                yo[2 * D.cs] = q2;
+                yo[3 * D.cs] = q3;
+                yo[4 * D.cs] = q4;
+                yo[5 * D.cs] = q5;
+            }
+            // carry plane k+1 -> k
+            hxk = hx1;
+            hyk = hy1;
+            hzk = hz1;
+            exk = ex1;
+            eyk = ey1;
+            uek0 = ue0;
+            uek1 = ue1;
+            uek2 = ue2;
+            uhm0 = uh0;
+            uhm1 = uh1;
+            uhm2 = uh2;
+            __syncthreads();
+            if (tid == 0 && p + S < nplanes) {
+                const uint32_t L = lcount + p + S;
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                          &tm_cH, x0, y0, kb - 1 + p + S);
+            }
+        }
+        lcount += nplanes;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -744,6 +1179,64 @@ static int leapfrog_fused_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps,
     return check_cuda("leapfrog fused");
 }
 
+// K1r launcher (same schedule and maps as K1)
+template <typename T, int EM, bool HA, int S, bool TR>
+static int leapfrog_r_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int nsrc, const void *q_dev,
+                        const std::vector<SrcDev> &hsrc, const TraceDev *tr) {
+    constexpr int BX = 32, BY = 8;
+    using G = Geo<T, BX, BY>;
+    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 2 * 3 * G::RP) * sizeof(T) + 8 * S + 16;
+    const Grid &g = *ka.g;
+    auto kern = leapfrog_r_kernel<T, EM, HA, BX, BY, S, TR>;
+    static const int per_sm = resident_per_sm(kern, G::NTHR, smem);
+    if (per_sm < 1) return fail(PARAEXP_ECUDA, "leapfrog_r kernel does not fit on an SM");
+    const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
+    const int grid = std::min(sch.units, per_sm * num_sms());
+    auto D = make_dev<T>(g);
+    auto cf = make_coef<T, EM, HA>(g, 1.0);
+    CUtensorMap tmE, tmH, tmA, tmB;
+    int rc;
+    if (EM == 2 && (rc = make_map<T>(&tmE, g, g.d_cE_arr, 3, G::WX, G::HY))) return rc;
+    if (HA && (rc = make_map<T>(&tmH, g, g.d_cH_arr, 3, G::WX, G::HY))) return rc;
+    if ((rc = make_map<T>(&tmA, g, bufs[0], 6, G::WX, G::HY))) return rc;
+    if ((rc = make_map<T>(&tmB, g, bufs[1], 6, G::WX, G::HY))) return rc;
+    SrcList sl;
+    sl.n = nsrc;
+    for (int r = 0; r < nsrc && r < 16; ++r) {
+        sl.c[r] = hsrc[r].comp;
+        sl.i[r] = hsrc[r].i;
+        sl.j[r] = hsrc[r].j;
+        sl.k[r] = hsrc[r].k;
+    }
+    cudaStream_t s = (cudaStream_t)ka.stream;
+    TraceDev trm;
+    if (TR) trm = *tr;
+    for (int64_t m = 0; m < nsteps; ++m) {
+        const bool even = (m % 2) == 0;
+        if (TR) {
+            trm.energy = tr->energy ? tr->energy + m : nullptr;
+            trm.probe = tr->probe ? tr->probe + m * tr->np : nullptr;
+            if (!trm.probe) trm.np = 0;
+        }
+        kern<<<grid, G::NTHR, smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf, (T *)(even ? bufs[1] : bufs[0]), sch,
+                                          sl, nsrc ? (const T *)q_dev + m * nsrc : nullptr, trm);
+        ++*ka.launches;
+    }
+    if (nsteps % 2) std::swap(bufs[0], bufs[1]);
+    return check_cuda("leapfrog_r");
+}
+
+// kernel generation: r (row-aligned, register-carried; default) or the first fused kernels
+// (PARAEXP_KERNEL_V1=1)
+static bool kernels_v1() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PARAEXP_KERNEL_V1");
+        v = (e && atoi(e) != 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
 int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev *src_dev,
                      int nsrc, const void *q_dev, const TraceDev *tr) {
     if (nsrc > 16) return k_leapfrog_unfused(ka, bufs[0], nsteps, src_dev, nsrc, q_dev, tr);
@@ -753,6 +1246,10 @@ int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const 
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
+        if (!kernels_v1()) {
+            if (trace) return leapfrog_r_V<T, EM, HA, 3, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
+            return leapfrog_r_V<T, EM, HA, 3, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
+        }
         if (trace) return leapfrog_fused_V<T, EM, HA, 3, false, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
         if (onebar()) return leapfrog_fused_V<T, EM, HA, 4, true, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
         if (lf_stages() == 4) return leapfrog_fused_V<T, EM, HA, 4, false, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
@@ -800,11 +1297,57 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     return check_cuda("poly fused");
 }
 
+// K2r launcher (same schedule, maps and buffer protocol as K2)
+template <typename T, int EM, bool HA, int S>
+static int poly_r_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
+    constexpr int BX = 32, BY = 8;
+    using G = Geo<T, BX, BY>;
+    using U = GeoU<T, BX, BY>;
+    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 3 * 3 * U::RU) * sizeof(T) + 8 * S + 16;
+    const Grid &g = *ka.g;
+    auto kern = pair_r_kernel<T, EM, HA, BX, BY, S>;
+    static const int per_sm = resident_per_sm(kern, U::NTHR, smem);
+    if (per_sm < 1) return fail(PARAEXP_ECUDA, "pair_r kernel does not fit on an SM");
+    const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
+    const int grid = std::min(sch.units, per_sm * num_sms());
+    auto D = make_dev<T>(g);
+    auto cf = make_coef<T, EM, HA>(g, plan.sigma);
+    CUtensorMap tmE, tmH;
+    int rc;
+    if (EM == 2 && (rc = make_map<T>(&tmE, g, g.d_cE_arr, 3, G::WX, G::HY))) return rc;
+    if (HA && (rc = make_map<T>(&tmH, g, g.d_cH_arr, 3, G::WX, G::HY))) return rc;
+    cudaStream_t s = (cudaStream_t)ka.stream;
+    T *w = (T *)bufs[0], *yy = (T *)bufs[1], *sp = (T *)bufs[2], *sp2 = (T *)bufs[3];
+    CUtensorMap tmW, tmS;
+    if ((rc = make_map<T>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
+    if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
+    int init = 1;
+    for (const Op &op : plan.ops) {
+        kern<<<grid, U::NTHR, smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, sch, T(op.a), T(op.b), T(op.e2), T(op.c),
+                                          init, op.kind);
+        ++*ka.launches;
+        if (op.kind == 0) {
+            std::swap(w, sp);
+            std::swap(tmW, tmS);
+        }
+        init = 0;
+    }
+    bufs[0] = yy;
+    bufs[1] = w;
+    bufs[2] = sp;
+    bufs[3] = sp2;
+    return check_cuda("poly_r");
+}
+
 int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     return with_types(*ka.g, plan.sigma, [&](auto tT, auto tEM, auto tHA) {
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
+        if (!kernels_v1()) {
+            if (pair_stages(sizeof(T) == 8) == 4) return poly_r_V<T, EM, HA, 4>(ka, plan, bufs);
+            return poly_r_V<T, EM, HA, 3>(ka, plan, bufs);
+        }
         if (onebar()) return poly_fused_V<T, EM, HA, 4, true>(ka, plan, bufs);
         switch (pair_stages(sizeof(T) == 8)) {
             case 2: return poly_fused_V<T, EM, HA, 2, false>(ka, plan, bufs);
