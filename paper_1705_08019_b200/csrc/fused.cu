@@ -548,7 +548,10 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
     uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(UH + NR * 3 * G::RP) + 15) & ~uintptr_t(15));
     const int tid = threadIdx.x;
     const bool hasA = tid < G::RP;
-    const int ii = tid % G::EX, jj = tid / G::EX;
+    // row-aligned phase-A mapping: warps cover whole 32-wide rows, the +1 halo column last
+    constexpr int MAIN = BX * G::EY;
+    const int ii = tid < MAIN ? tid % BX : BX, jj = tid < MAIN ? tid / BX : tid - MAIN;
+    const int rA = jj * G::EX + ii;                       // ring index of the phase-A point
     const int sE = (jj + 1) * G::WX + ii + G::OX;         // stage index of the u_e point
     const int sH = jj * G::WX + ii - 1 + G::OX;           // stage index of the u_h point
     const bool hasB = tid < G::NT;
@@ -638,9 +641,9 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
                         u1 = (lyE && vk && kp) ? bE1 * c1 : T(0);
                         u2 = (lzE && vk) ? bE2 * c2 : T(0);
                     }
-                    UE1[tid] = u0;
-                    UE1[G::RP + tid] = u1;
-                    UE1[2 * G::RP + tid] = u2;
+                    UE1[rA] = u0;
+                    UE1[G::RP + rA] = u1;
+                    UE1[2 * G::RP + rA] = u2;
                 }
                 // u_h(k) = -bH .* C w_e
                 {
@@ -658,9 +661,9 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
                         u1 = (lyH && vk) ? -(bH1 * c1) : T(0);
                         u2 = (inH && vk && k > 0) ? -(bH2 * c2) : T(0);
                     }
-                    UH0[tid] = u0;
-                    UH0[G::RP + tid] = u1;
-                    UH0[2 * G::RP + tid] = u2;
+                    UH0[rA] = u0;
+                    UH0[G::RP + rA] = u1;
+                    UH0[2 * G::RP + rA] = u2;
                 }
             }
             __syncthreads();
@@ -772,7 +775,7 @@ struct GeoU {
 };
 
 template <typename T, int EM, bool HA, int BX, int BY, int S>
-__global__ void __launch_bounds__(GeoU<T, BX, BY>::NTHR) pair_r_kernel(
+__global__ void __launch_bounds__(GeoU<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) pair_r_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
     T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode) {
@@ -1297,6 +1300,15 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     return check_cuda("poly fused");
 }
 
+static bool pair_r_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PARAEXP_PAIR_R");
+        v = (e && atoi(e) != 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
 // K2r launcher (same schedule, maps and buffer protocol as K2)
 template <typename T, int EM, bool HA, int S>
 static int poly_r_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
@@ -1344,7 +1356,9 @@ int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
-        if (!kernels_v1()) {
+        // K2r measured slower than K2 on B200 (fp64 306 vs 289 us per A-application: barrier
+        // stalls -- the frame threads idle through phase B); opt-in with PARAEXP_PAIR_R=1
+        if (pair_r_enabled()) {
             if (pair_stages(sizeof(T) == 8) == 4) return poly_r_V<T, EM, HA, 4>(ka, plan, bufs);
             return poly_r_V<T, EM, HA, 3>(ka, plan, bufs);
         }
