@@ -59,7 +59,7 @@ extern "C" {
 enum { PARAEXP_F64 = 0, PARAEXP_F32 = 1 };
 enum { PARAEXP_SRC_ZERO = 0, PARAEXP_SRC_GAUSS_PAPER = 1, PARAEXP_SRC_GAUSS_SINE = 2,
        PARAEXP_SRC_SINE = 3 };
-enum { PARAEXP_TAYLOR = 0, PARAEXP_LEJA = 1 };
+enum { PARAEXP_TAYLOR = 0, PARAEXP_LEJA = 1, PARAEXP_KRYLOV = 2 };
 enum { PARAEXP_TAIL_EXP = 0, PARAEXP_TAIL_LEAPFROG = 1 };
 enum { PARAEXP_MAT_SCALAR = 0, PARAEXP_MAT_ZTABLE = 1, PARAEXP_MAT_ARRAY = 2 };
 enum { PARAEXP_KERNELS_AUTO = 0, PARAEXP_KERNELS_UNFUSED = 1, PARAEXP_KERNELS_FUSED = 2 };
@@ -212,7 +212,12 @@ int paraexp_leapfrog_trace(paraexp_grid *grid, const paraexp_source *src, int32_
 /* ---- exp(tau A) v (a5, a6) -------------------------------------------------------- */
 /* Options:
  *   method   PARAEXP_LEJA (Newton form on Leja points of i[-a,a], a = 1.05 h rho,
- *            reading 14) or PARAEXP_TAYLOR (truncated Taylor)
+ *            reading 14), PARAEXP_TAYLOR (truncated Taylor) or
+ *            PARAEXP_KRYLOV (Arnoldi with sigma = infinity, SURVEY 8(f) f3:
+ *            per substep h = tau/s an l = m dimensional Krylov space of X = hA in the
+ *            energy inner product, modified Gram-Schmidt applied twice, result
+ *            ||b|| V_l exp(H_l) e_1; m = l in 1..100 any parity; s = 0 => s = ceil(2 rho tau / l)
+ *            (rho h <= l/2, reading 31); eps_A unused; stops early on a happy breakdown)
  *   m, s     fixed degree (1 or even, <= 100) and substep count; m = 0 => choose (m, s)
  *            minimising m*s subject to the per-substep criterion of reading 16 at eps_A;
  *            m > 0 with s = 0 => s from the criterion at that m

@@ -490,6 +490,62 @@ def expmv_pairs(g: Grid, plan: Plan, e, h, dtype: str = "f64"):
     return be, bh
 
 
+def expmv_krylov(g: Grid, l: int, s: int, tau: float, e, h, dtype: Optional[str] = None):
+    """Krylov approximation of exp(tau A) v (Arnoldi with sigma = infinity, PAPER:383-402;
+    SURVEY 8(f) f3), step by step: for each of s substeps of h = tau/s,
+        beta = ||b||, v_1 = b / beta; for j = 1..l: w = X v_j (X = h A_orig),
+        h_ij = <v_i, w>, w -= h_ij v_i (i = 1..j, the sweep done twice: modified
+        Gram-Schmidt with one reorthogonalisation), h_{j+1,j} = ||w||, v_{j+1} = w / h_{j+1,j},
+        b <- beta V_l expm(H_l) e_1,
+    in the energy inner product <x, y> = sum_e x y / cE_T + sum_h x y / cH_T over live DOFs
+    (proportional to <e,e>_eps + <h,h>_mu).  A happy breakdown
+    (h_{j+1,j} <= 1e-12 max|h|) ends the space early (reading 31).  Returns (e, h, A-applications)."""
+    import scipy.linalg
+    dtype = dtype or g.dtype
+    n3 = 3 * g.Np
+    we = np.where(g.cE_T != 0, 1.0 / np.where(g.cE_T != 0, g.cE_T, 1.0), 0.0)
+    wh = np.where(g.cH_T != 0, 1.0 / np.where(g.cH_T != 0, g.cH_T, 1.0), 0.0)
+    wgt = np.concatenate([we, wh])
+
+    def dot(x, y):
+        return float(np.dot(x * wgt, y))
+
+    b = np.concatenate([np.asarray(e, float), np.asarray(h, float)])
+    if tau == 0.0:
+        return b[:n3].copy(), b[n3:].copy(), 0
+    X = ScaledOp(g, (tau / s) / g.dt, dtype)
+    apps = 0
+    for _ in range(s):
+        beta = math.sqrt(max(dot(b, b), 0.0))
+        if beta == 0.0:
+            break
+        V = [b / beta]
+        H = np.zeros((l, l))
+        lr, hmax = l, 0.0
+        for j in range(l):
+            xe, xh = X(V[j][:n3], V[j][n3:])
+            apps += 1
+            w = np.concatenate([xe, xh])
+            for _pass in range(2):
+                for i in range(j + 1):
+                    hij = dot(V[i], w)
+                    H[i, j] += hij
+                    hmax = max(hmax, abs(hij))
+                    w = w - hij * V[i]
+            if j + 1 == l:
+                break
+            hn = math.sqrt(max(dot(w, w), 0.0))
+            hmax = max(hmax, hn)
+            if not hn > 1e-12 * hmax:
+                lr = j + 1
+                break
+            H[j + 1, j] = hn
+            V.append(w / hn)
+        c = scipy.linalg.expm(H[:lr, :lr])[:, 0]
+        b = beta * sum(c[i] * V[i] for i in range(lr))
+    return b[:n3].copy(), b[n3:].copy(), apps
+
+
 def expmv(g: Grid, plan: Plan, e, h, mode: str = "pairs", dtype: Optional[str] = None):
     if plan.tau == 0.0:
         return np.array(e, float), np.array(h, float)

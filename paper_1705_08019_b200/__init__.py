@@ -14,7 +14,7 @@ import numpy as np
 
 from . import abi
 from .abi import (EDIVERGED, EINVAL, ENOTSUP, EOVERFLOW, F32, F64, KERNELS_AUTO, KERNELS_FUSED,  # noqa
-                  KERNELS_UNFUSED, LEJA, TAIL_EXP, TAIL_LEAPFROG, TAYLOR, ParaexpError, check)
+                  KERNELS_UNFUSED, KRYLOV, LEJA, TAIL_EXP, TAIL_LEAPFROG, TAYLOR, ParaexpError, check)
 
 __all__ = ["Grid", "Comm", "leapfrog", "leapfrog_trace", "expmv", "expmv_plan", "solve", "solve_trace",
            "partition", "schedule",
@@ -23,7 +23,8 @@ __all__ = ["Grid", "Comm", "leapfrog", "leapfrog_trace", "expmv", "expmv_plan", 
 _DT = {"f64": F64, "f32": F32}
 _KER = {"auto": KERNELS_AUTO, "unfused": KERNELS_UNFUSED, "fused": KERNELS_FUSED}
 _SRC_KIND = {"zero": 0, "gauss_paper": 1, "gauss_sine": 2, "sine": 3}
-_METHOD = {"taylor": TAYLOR, "leja": LEJA}
+_METHOD = {"taylor": TAYLOR, "leja": LEJA, "krylov": KRYLOV}
+_METHOD_NAME = {v: k for k, v in _METHOD.items()}
 
 
 def version() -> str:
@@ -216,7 +217,7 @@ def expmv(grid: Grid, tau: float, e, h, method="leja", m=0, s=0, eps_A=1e-12, rh
 
 def _plan_dict(p):
     m = p.m
-    return {"method": "leja" if p.method == LEJA else "taylor", "m": m, "s": p.s, "tau": p.tau,
+    return {"method": _METHOD_NAME[p.method], "m": m, "s": p.s, "tau": p.tau,
             "rho": p.rho, "a": p.a, "gamma": p.gamma, "sigma": p.sigma, "n_ops": p.n_ops,
             "xi": list(p.xi[:m + 1]), "d": [complex(p.d_re[k], p.d_im[k]) for k in range(m + 1)]}
 

@@ -22,7 +22,7 @@ OK, EINVAL, ENOMEM, ECUDA, ENCCL, EDIVERGED, EOVERFLOW, ENOTSUP = 0, -1, -2, -3,
 WCFL = 1
 F64, F32 = 0, 1
 SRC_ZERO, SRC_GAUSS_PAPER, SRC_GAUSS_SINE, SRC_SINE = 0, 1, 2, 3
-TAYLOR, LEJA = 0, 1
+TAYLOR, LEJA, KRYLOV = 0, 1, 2
 TAIL_EXP, TAIL_LEAPFROG = 0, 1
 MAT_SCALAR, MAT_ZTABLE, MAT_ARRAY = 0, 1, 2
 KERNELS_AUTO, KERNELS_UNFUSED, KERNELS_FUSED = 0, 1, 2

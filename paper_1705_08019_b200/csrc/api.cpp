@@ -317,10 +317,129 @@ struct Events {
     }
 };
 
+// ---- f3: Krylov (Arnoldi, sigma = infinity) ---------------------------------
+// exp(H) e_1 of a small real matrix (l <= 100): scaling and squaring of a Taylor series in
+// long double.
+static void expm_first_column(const std::vector<long double> &H, int l, std::vector<double> &c) {
+    long double nrm = 0;
+    for (int i = 0; i < l; ++i) {
+        long double r = 0;
+        for (int j = 0; j < l; ++j) r += std::fabs(H[i * l + j]);
+        nrm = std::max(nrm, r);
+    }
+    int sq = 0;
+    while (nrm > 0.25L) {
+        nrm *= 0.5L;
+        ++sq;
+    }
+    const long double scale = std::ldexp(1.0L, -sq);
+    std::vector<long double> A(l * l), E(l * l, 0.0L), T(l * l), N(l * l);
+    for (int q = 0; q < l * l; ++q) A[q] = H[q] * scale;
+    for (int i = 0; i < l; ++i) E[i * l + i] = 1.0L;
+    T = E;
+    for (int k = 1; k <= 30; ++k) {           // T <- T A / k ; E += T
+        for (int i = 0; i < l; ++i)
+            for (int j = 0; j < l; ++j) {
+                long double acc = 0;
+                for (int q = 0; q < l; ++q) acc += T[i * l + q] * A[q * l + j];
+                N[i * l + j] = acc / k;
+            }
+        T = N;
+        for (int q = 0; q < l * l; ++q) E[q] += T[q];
+    }
+    for (int r = 0; r < sq; ++r) {            // E <- E^2
+        for (int i = 0; i < l; ++i)
+            for (int j = 0; j < l; ++j) {
+                long double acc = 0;
+                for (int q = 0; q < l; ++q) acc += E[i * l + q] * E[q * l + j];
+                N[i * l + j] = acc;
+            }
+        E = N;
+    }
+    c.resize(l);
+    for (int i = 0; i < l; ++i) c[i] = (double)E[i * l + 0];
+}
+
+// One Krylov substep in place on bufs[0]: b <- ||b|| V_l exp(H_l) e_1, Arnoldi in the energy
+// inner product <x,y> = sum x y / cE + sum x y / cH (k_dot_M), modified Gram-Schmidt applied
+// twice.  Returns the realised dimension (happy breakdown stops early).
+static int krylov_substep(const KernelArgs &ka, Grid &G, const Plan &plan, void *b, int *l_out) {
+    const int l = plan.m;
+    const size_t bytes = (size_t)G.L.state_elems() * G.esize();
+    while ((int)G.kry.size() < l + 1) {
+        void *q = nullptr;
+        int rc = dev_alloc(&q, bytes);
+        if (rc) return rc;
+        if ((rc = dev_memset_async(q, 0, bytes, nullptr)) || (rc = dev_sync(nullptr))) return rc;
+        G.kry.push_back(q);
+        G.device_bytes += bytes;
+    }
+    int rc;
+    double bb;
+    if ((rc = k_dot_M(ka, b, b, &bb))) return rc;
+    const double beta0 = std::sqrt(std::max(bb, 0.0));
+    *l_out = 0;
+    if (!(beta0 > 0)) return PARAEXP_OK;              // exp(X) 0 = 0
+    std::vector<void *> V(G.kry.begin(), G.kry.begin() + l + 1);
+    if ((rc = k_lincomb(ka, V[0], b, b, 1.0 / beta0, 0.0, 0.0))) return rc;
+    std::vector<long double> H((size_t)l * l, 0.0L);
+    int lr = l;
+    double hmax = 0;
+    for (int j = 0; j < l; ++j) {
+        void *w = V[j + 1];
+        if ((rc = k_apply_A(ka, V[j], w, plan.sigma))) return rc;     // w = X v_j
+        for (int pass = 0; pass < 2; ++pass)
+            for (int i = 0; i <= j; ++i) {
+                double hij;
+                if ((rc = k_dot_M(ka, V[i], w, &hij))) return rc;
+                H[(size_t)i * l + j] += hij;
+                hmax = std::max(hmax, std::fabs(hij));
+                if ((rc = k_lincomb(ka, w, V[i], V[i], -hij, 0.0, 1.0))) return rc;
+            }
+        if (j + 1 == l) break;                                        // h_{l+1,l} unused
+        double ww;
+        if ((rc = k_dot_M(ka, w, w, &ww))) return rc;
+        const double hn = std::sqrt(std::max(ww, 0.0));
+        hmax = std::max(hmax, hn);
+        if (!(hn > 1e-12 * hmax)) {                                   // happy breakdown:
+            lr = j + 1;                                               // K_{j+1} is invariant
+            break;
+        }
+        H[(size_t)(j + 1) * l + j] = hn;
+        if ((rc = k_lincomb(ka, w, w, w, 1.0 / hn, 0.0, 0.0))) return rc;
+    }
+    std::vector<long double> Hr((size_t)lr * lr);
+    for (int i = 0; i < lr; ++i)
+        for (int j = 0; j < lr; ++j) Hr[(size_t)i * lr + j] = H[(size_t)i * l + j];
+    std::vector<double> c;
+    expm_first_column(Hr, lr, c);
+    if ((rc = k_lincomb(ka, b, V[0], V[0], beta0 * c[0], 0.0, 0.0))) return rc;
+    for (int i = 1; i < lr; ++i)
+        if ((rc = k_lincomb(ka, b, V[i], V[i], beta0 * c[i], 0.0, 1.0))) return rc;
+    *l_out = lr;
+    return PARAEXP_OK;
+}
+
 // apply the propagator p(X)^s in place: bufs[0] in/out.  Kernel time is attributed to
 // phase 6 (ms_poly_kernels) when an Events recorder is given.
 static int run_plan(const KernelArgs &ka, const Plan &plan, void *bufs[4], paraexp_stats *st,
                     Events *ev = nullptr) {
+    if (plan.method == PARAEXP_KRYLOV) {
+        const int id = ev && plan.s > 0 ? ev->open(6) : -1;
+        int64_t apps = 0;
+        for (int q = 0; q < plan.s; ++q) {
+            int lr = 0;
+            int rc = krylov_substep(ka, *const_cast<Grid *>(ka.g), plan, bufs[0], &lr);
+            if (rc) return rc;
+            apps += lr;
+        }
+        if (id >= 0) ev->close(id);
+        if (st) {
+            st->a_applications += apps;
+            st->substeps += plan.s;
+        }
+        return PARAEXP_OK;
+    }
     const int id = ev && plan.s > 0 ? ev->open(6) : -1;
     for (int q = 0; q < plan.s; ++q) {
         int rc = k_poly_substep(ka, plan, bufs);

@@ -60,6 +60,7 @@ struct Grid {
     std::vector<SrcDev> h_src;  // host copy of the current source descriptors
     void *d_q = nullptr;        // source amplitude table
     void *d_canon[2] = {nullptr, nullptr};   // canonical-layout staging of host-pointer fields
+    std::vector<void *> kry;    // Krylov basis vectors (f3), allocated on first use
     int64_t d_q_cap = 0;
     int64_t device_bytes = 0;
     size_t esize() const { return dtype == PARAEXP_F64 ? 8 : 4; }

@@ -277,7 +277,7 @@ __global__ void lincomb_kernel(T *__restrict__ z, const T *__restrict__ x,
                                const T *__restrict__ y, T al, T be, T ga, int64_t n) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
          q += (int64_t)gridDim.x * blockDim.x)
-        z[q] = al * x[q] + be * y[q] + ga * z[q];
+        z[q] = al * x[q] + (be != T(0) ? be * y[q] : T(0)) + (ga != T(0) ? ga * z[q] : T(0));
 }
 template <typename T>
 __global__ void finite_kernel(const T *__restrict__ x, int64_t n, int *flag) {

@@ -229,6 +229,27 @@ static void build_ops(Plan &p) {
 
 int make_plan(int method, int m, int s, double eps_A, double tau, double rho, double dt,
               Plan &out) {
+    if (method == PARAEXP_KRYLOV) {
+        // f3: Krylov plan = subspace dimension l = m and substeps s (reading 31)
+        if (!(tau >= 0) || !std::isfinite(tau)) return fail(PARAEXP_EINVAL, "tau must be >= 0");
+        if (!(rho >= 0) || !std::isfinite(rho)) return fail(PARAEXP_EINVAL, "rho must be >= 0");
+        if (m < 1 || m > PARAEXP_MAX_DEGREE) return fail(PARAEXP_EINVAL, "Krylov dimension m must be in 1..100");
+        if (s < 0) return fail(PARAEXP_EINVAL, "s must be >= 0");
+        out = Plan();
+        out.method = method;
+        out.tau = tau;
+        out.rho = rho;
+        out.m = m;
+        out.gamma = 1.0;
+        if (tau == 0.0) {
+            out.s = 0;
+            out.sigma = 0;
+            return PARAEXP_OK;
+        }
+        out.s = s > 0 ? s : (int)std::max(1.0, std::ceil(2.0 * rho * tau / m));
+        out.sigma = (tau / out.s) / dt;      // X = h A_orig through the stencil scale sigma*dt
+        return PARAEXP_OK;
+    }
     if (method != PARAEXP_LEJA && method != PARAEXP_TAYLOR) return fail(PARAEXP_EINVAL, "bad method");
     if (!(tau >= 0) || !std::isfinite(tau)) return fail(PARAEXP_EINVAL, "tau must be >= 0");
     if (!(rho >= 0) || !std::isfinite(rho)) return fail(PARAEXP_EINVAL, "rho must be >= 0");

@@ -257,3 +257,44 @@ def test_solve_trace(dtype):
     ref = fit.paraexp(og, src, 1e-12, nsteps, p, lambda tau: fit.make_plan("leja", m, s, tau, rho),
                       u0=u0, rho=rho, dtype=dtype)
     assert_parity((eo.double().cpu().numpy(), ho.double().cpu().numpy()), ref, dtype, "solve_trace output")
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("kind", ["vacuum", "random"])
+@pytest.mark.parametrize("l,s", [(12, 2), (30, 1), (5, 3)])
+def test_expmv_krylov(dtype, kind, l, s):
+    """f3: Krylov (Arnoldi, sigma = infinity) on the GPU vs the oracle's step-by-step Arnoldi
+    in the same energy inner product."""
+    n = (21, 19, 13)
+    og, lg = _grids(n, kind, dtype, "auto")
+    e, h = inputs(og, *random_fields(*n, seed=17))
+    tau = 9 * og.dt
+    ref_e, ref_h, apps = fit.expmv_krylov(og, l, s, tau, e, h, dtype=dtype)
+    ge, gh, st = lib_expmv(lg, tau, e, h, method="krylov", m=l, s=s, rho=og.rho_cfl)
+    assert_parity((ge, gh), (ref_e, ref_h), dtype, f"krylov l={l} s={s} {kind}")
+    assert st["a_applications"] == apps
+
+
+def test_solve_krylov_tails():
+    """ParaExp with Krylov tails (the paper's third propagator) vs the oracle."""
+    n = (19, 17, 9)
+    og, lg = _grids(n, "random", "f64", "auto")
+    u0 = inputs(og, *random_fields(*n, seed=79))
+    src = _sources(og, n)
+    rho = og.rho_cfl
+    # oracle: Algorithm 1 sequentially with Krylov propagators E_i (Horner over the
+    # sub-intervals, as paraexp() does for polynomial plans), then the dt/2 Taylor shift
+    S = fit.partition(40, 4)
+    We, Wh = og.clean(*u0)
+    parts = []
+    for i in range(1, 5):
+        z = og.zeros()
+        parts.append(fit.leapfrog(og, z[0], z[1], S[i] - S[i - 1], src, 0.0, S[i - 1]))
+    for i in range(1, 5):
+        We, Wh, _ = fit.expmv_krylov(og, 16, 2, (S[i] - S[i - 1]) * og.dt, We, Wh)
+        if i < 4:
+            ei, hi = parts[i - 1]
+            We, Wh = We + ei, Wh + fit.sync_h(og, ei, hi)
+    ref = fit.paraexp_finish(og, parts[-1], (We, Wh), rho)
+    ge, gh, st = lib_solve(lg, 40, 4, src, u0=u0, method="krylov", m=16, s=2, rho=rho)
+    assert_parity((ge, gh), ref, "f64", "solve krylov")
