@@ -223,13 +223,19 @@ int paraexp_leapfrog_trace(paraexp_grid *grid, const paraexp_source *src, int32_
  *            m > 0 with s = 0 => s from the criterion at that m
  *   eps_A    relative backward-error tolerance in (1e-14, 1)
  *   rho      spectral bound of A; 0 => min(rho_cfl, 1.05*rho_pow) (reading 17)
- *   early_term  must be 0 (reserved)                                                   */
+ *   early_term  Taylor/Leja: != 0 ends a substep's Newton sum once two consecutive increments
+ *            satisfy ||delta y|| <= eps_A ||y|| in the energy norm ("early
+ *            termination", reading 18); the skipped ops launch and return at once;
+ *            stats.a_applications reports the A-applications actually performed
+ *   beta     with eps_A == 0 and beta > 0: eps_A = eps_A* = beta dt^2 / rho
+ *            (eq:tolerance_leja_2; see paraexp_optimal_tolerance)          */
 typedef struct {
     int32_t method;
     int32_t m, s;
     double eps_A;
     double rho;
     int32_t early_term;
+    double beta;
 } paraexp_expmv_opts;
 
 /* Plan export (reading 25: parity is defined at a fixed plan). */
@@ -309,6 +315,13 @@ int paraexp_leja_points(int32_t count, double *xi);
 /* Plan without a grid: tau and rho given, dt used only for sigma (may be 1). */
 int paraexp_plan_host(int32_t method, int32_t m, int32_t s, double eps_A, double tau,
                       double rho, double dt, paraexp_plan_info *out);
+/* eq:tolerance_leja_2: eps_A* = beta dt^2 / ||A||_2, the Leja
+ * tolerance that balances the exponential's backward error against the leapfrog truncation
+ * error eps_B = beta dt^2 (kappa_exp(A) = ||A||_2 for normal A).  Taken literally (reading 30:
+ * the paper gives neither beta's value nor its units; beta carries s^-3 for SI dt and ||A||),
+ * clamped to [1e-14, 0.1]; *clamped (may be NULL) is set to 1 if the clamp applied.
+ * Returns 0.1 for non-positive or non-finite input. */
+double paraexp_optimal_tolerance(double dt, double beta, double norm_A, int32_t *clamped);
 /* theta_m(eps_A): largest theta with max_{|x|<=theta} |p(ix) - e^{ix}| <= eps_A theta
  * (reading 16), method TAYLOR or LEJA.  Cached. */
 double paraexp_theta(int32_t method, int32_t m, double eps_A);

@@ -458,6 +458,50 @@ def pair_constants(plan: Plan, dtype: str = "f64"):
     return out
 
 
+def expmv_pairs_et(g: Grid, plan: Plan, e, h, eps: float, dtype: str = "f64"):
+    """expmv_pairs with the early termination of the Newton sum (PAPER:449-450; reading 18;
+    SURVEY 8(f) f2): within a substep, before op k >= 2, stop if the two previous ops both
+    had ||delta y|| <= eps ||y|| (delta y = the op's increment of y), norms in the energy
+    inner product <x,y> = sum_e x y / cE_T + sum_h x y / cH_T.  Returns (e, h, A-applications
+    performed)."""
+    X = ScaledOp(g, (plan.tau / plan.s) / (plan.gamma * g.dt), dtype)
+    consts = pair_constants(plan, dtype)
+    we = np.where(g.cE_T != 0, 1.0 / np.where(g.cE_T != 0, g.cE_T, 1.0), 0.0)
+    wh = np.where(g.cH_T != 0, 1.0 / np.where(g.cH_T != 0, g.cH_T, 1.0), 0.0)
+
+    def n2(xe, xh):
+        return float(np.dot(xe * we, xe) + np.dot(xh * wh, xh))
+
+    be = np.array(e, dtype=np.float64, copy=True)
+    bh = np.array(h, dtype=np.float64, copy=True)
+    apps = 0
+    for _ in range(plan.s):
+        we_, wh_ = be, bh
+        ye = np.zeros_like(be)
+        yh = np.zeros_like(bh)
+        small = []
+        for k, (kind, a, b, e2, c) in enumerate(consts):
+            if k >= 2 and small[k - 1] and small[k - 2]:
+                break
+            apps += 1 if kind == "half" else 2
+            ue, uh = X(we_, wh_)
+            ne = ye + a * we_ + b * ue
+            nh = yh + a * wh_ + b * uh
+            if kind != "half":
+                xe, xh = X(ue, uh)
+                we2 = xe + e2 * we_
+                wh2 = xh + e2 * wh_
+                if kind == "last":
+                    ne = ne + c * we2
+                    nh = nh + c * wh2
+                else:
+                    we_, wh_ = we2, wh2
+            small.append(n2(ne - ye, nh - yh) <= eps * eps * n2(ne, nh))
+            ye, yh = ne, nh
+        be, bh = ye, yh
+    return be, bh, apps
+
+
 def expmv_pairs(g: Grid, plan: Plan, e, h, dtype: str = "f64"):
     """The same polynomial in real arithmetic, conjugate pairs folded (readings 28-29):
         pair: u = X w; y += a w + b u; w = X u + e2 w

@@ -17,6 +17,7 @@ from .abi import (EDIVERGED, EINVAL, ENOTSUP, EOVERFLOW, F32, F64, KERNELS_AUTO,
                   KERNELS_UNFUSED, KRYLOV, LEJA, TAIL_EXP, TAIL_LEAPFROG, TAYLOR, ParaexpError, check)
 
 __all__ = ["Grid", "Comm", "leapfrog", "leapfrog_trace", "expmv", "expmv_plan", "solve", "solve_trace",
+           "optimal_tolerance",
            "partition", "schedule",
            "leja_points", "plan_host", "theta", "version", "make_sources", "ParaexpError"]
 
@@ -150,11 +151,20 @@ def make_sources(sources: Optional[Iterable]) -> tuple:
     return arr, len(srcs)
 
 
-def _opts(method="leja", m=0, s=0, eps_A=1e-12, rho=0.0):
+def _opts(method="leja", m=0, s=0, eps_A=1e-12, rho=0.0, early_term=False, beta=0.0):
     o = abi.paraexp_expmv_opts()
     o.method = _METHOD[method] if isinstance(method, str) else int(method)
-    o.m, o.s, o.eps_A, o.rho, o.early_term = int(m), int(s), float(eps_A), float(rho or 0.0), 0
+    o.m, o.s, o.eps_A, o.rho = int(m), int(s), float(eps_A), float(rho or 0.0)
+    o.early_term, o.beta = int(bool(early_term)), float(beta or 0.0)
     return o
+
+
+def optimal_tolerance(dt: float, beta: float, norm_A: float) -> tuple:
+    """paraexp_optimal_tolerance: eps_A* = beta dt^2 / ||A||_2 (eq:tolerance_leja_2), clamped
+    to [1e-14, 0.1]; returns (eps_A*, clamped)."""
+    c = C.c_int32()
+    v = abi.lib.paraexp_optimal_tolerance(float(dt), float(beta), float(norm_A), C.byref(c))
+    return v, bool(c.value)
 
 
 def leapfrog(grid: Grid, e, h, nsteps: int, sources=None, t0: float = 0.0,
@@ -205,9 +215,9 @@ def leapfrog_trace(grid: Grid, e, h, nsteps: int, sources=None, t0: float = 0.0,
 
 
 def expmv(grid: Grid, tau: float, e, h, method="leja", m=0, s=0, eps_A=1e-12, rho=0.0,
-          stream=None) -> dict:
+          stream=None, early_term=False, beta=0.0) -> dict:
     """paraexp_expmv: (h, e) <- exp(tau A_orig)(h, e) in place."""
-    o = _opts(method, m, s, eps_A, rho)
+    o = _opts(method, m, s, eps_A, rho, early_term, beta)
     st = abi.paraexp_stats()
     check(abi.lib.paraexp_expmv(grid.handle, float(tau), C.byref(o), _field(e, grid, "e"),
                                 _field(h, grid, "h"), _stream(stream, grid), C.byref(st)),
@@ -222,8 +232,9 @@ def _plan_dict(p):
             "xi": list(p.xi[:m + 1]), "d": [complex(p.d_re[k], p.d_im[k]) for k in range(m + 1)]}
 
 
-def expmv_plan(grid: Grid, tau: float, method="leja", m=0, s=0, eps_A=1e-12, rho=0.0) -> dict:
-    o = _opts(method, m, s, eps_A, rho)
+def expmv_plan(grid: Grid, tau: float, method="leja", m=0, s=0, eps_A=1e-12, rho=0.0,
+               beta=0.0) -> dict:
+    o = _opts(method, m, s, eps_A, rho, False, beta)
     p = abi.paraexp_plan_info()
     check(abi.lib.paraexp_expmv_plan(grid.handle, float(tau), C.byref(o), C.byref(p)),
           "paraexp_expmv_plan")
@@ -304,10 +315,11 @@ class Comm:
 
 def solve(grid: Grid, nsteps: int, p: int, sources=None, t0: float = 0.0, method="leja", m=0,
           s=0, eps_A=1e-12, rho=0.0, tail_mode=TAIL_EXP, u0=None, e_out=None, h_out=None,
-          comm: Optional[Comm] = None, broadcast_out=False, stream=None) -> dict:
+          comm: Optional[Comm] = None, broadcast_out=False, stream=None, early_term=False,
+          beta=0.0) -> dict:
     """paraexp_solve (Algorithm 1): returns the stats dict; output in e_out/h_out."""
     arr, n = make_sources(sources)
-    o = _opts(method, m, s, eps_A, rho)
+    o = _opts(method, m, s, eps_A, rho, early_term, beta)
     st = abi.paraexp_stats()
     e0 = h0 = C.c_void_p(0)
     if u0 is not None:

@@ -73,7 +73,7 @@ class paraexp_stats(C.Structure):
 
 class paraexp_expmv_opts(C.Structure):
     _fields_ = [("method", C.c_int32), ("m", C.c_int32), ("s", C.c_int32), ("eps_A", C.c_double),
-                ("rho", C.c_double), ("early_term", C.c_int32)]
+                ("rho", C.c_double), ("early_term", C.c_int32), ("beta", C.c_double)]
 
 
 class paraexp_plan_info(C.Structure):
@@ -122,6 +122,7 @@ _sigs = {
     "paraexp_plan_host": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                     C.c_double, C.c_double, C.POINTER(paraexp_plan_info)]),
     "paraexp_theta": (C.c_double, [C.c_int32, C.c_int32, C.c_double]),
+    "paraexp_optimal_tolerance": (C.c_double, [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_int32)]),
     "paraexp_strerror": (C.c_char_p, [C.c_int]),
     "paraexp_last_error": (C.c_char_p, []),
     "paraexp_version": (C.c_char_p, []),

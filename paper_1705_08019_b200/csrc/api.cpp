@@ -441,6 +441,40 @@ static int run_plan(const KernelArgs &ka, const Plan &plan, void *bufs[4], parae
         return PARAEXP_OK;
     }
     const int id = ev && plan.s > 0 ? ev->open(6) : -1;
+    if (plan.early_term && plan.s > 0) {
+        // f2: per substep the op norms and the done flag are reset; the kernels count the
+        // A-applications they actually perform (reading 18)
+        Grid &G = *const_cast<Grid *>(ka.g);
+        const size_t nops = plan.ops.size();
+        const size_t bytes = (2 * nops) * sizeof(double) + 2 * sizeof(int) + 16;
+        if (!G.d_et) {
+            int rc = dev_alloc(&G.d_et, (2 * (PARAEXP_MAX_DEGREE + 2)) * sizeof(double) + 64);
+            if (rc) return rc;
+        }
+        EtDev et;
+        et.norms = (double *)G.d_et;
+        et.done = (int *)((char *)G.d_et + 2 * (PARAEXP_MAX_DEGREE + 2) * sizeof(double));
+        et.count = et.done + 1;
+        et.eps2 = plan.eps_A * plan.eps_A;
+        KernelArgs kb = ka;
+        kb.et = &et;
+        int rc = dev_memset_async(et.count, 0, sizeof(int), ka.stream);
+        for (int q = 0; q < plan.s && !rc; ++q) {
+            if ((rc = dev_memset_async(et.norms, 0, 2 * nops * sizeof(double), ka.stream))) break;
+            if ((rc = dev_memset_async(et.done, 0, sizeof(int), ka.stream))) break;
+            rc = k_poly_substep(kb, plan, bufs);
+        }
+        if (rc) return rc;
+        (void)bytes;
+        if (id >= 0) ev->close(id);
+        int count = 0;
+        if ((rc = dev_memcpy_d2h(&count, et.count, sizeof(int), ka.stream))) return rc;
+        if (st) {
+            st->a_applications += count;
+            st->substeps += plan.s;
+        }
+        return PARAEXP_OK;
+    }
     for (int q = 0; q < plan.s; ++q) {
         int rc = k_poly_substep(ka, plan, bufs);
         if (rc) return rc;
@@ -454,10 +488,20 @@ static int run_plan(const KernelArgs &ka, const Plan &plan, void *bufs[4], parae
 }
 
 static int opts_plan(Grid &G, double tau, const paraexp_expmv_opts *o, double rho, Plan &plan) {
-    paraexp_expmv_opts def{PARAEXP_LEJA, 0, 0, 1e-12, 0.0, 0};
+    paraexp_expmv_opts def{PARAEXP_LEJA, 0, 0, 1e-12, 0.0, 0, 0.0};
     if (!o) o = &def;
-    if (o->early_term) return fail(PARAEXP_EINVAL, "early_term is reserved (must be 0)");
-    return make_plan(o->method, o->m, o->s, o->eps_A, tau, rho, G.dt, plan);
+    double eps = o->eps_A;
+    if (eps == 0.0 && o->beta > 0) {   // eq:tolerance_leja_2 (f2, reading 30)
+        int clamped = 0;
+        eps = paraexp_optimal_tolerance(G.dt, o->beta, rho, &clamped);
+    }
+    if (o->early_term && !(eps >= 1e-14 && eps < 1)) return fail(PARAEXP_EINVAL, "early termination needs eps_A in [1e-14, 1)");
+    if (o->early_term && o->method == PARAEXP_KRYLOV) return fail(PARAEXP_EINVAL, "early termination applies to Taylor/Leja");
+    int rc = make_plan(o->method, o->m, o->s, eps, tau, rho, G.dt, plan);
+    if (rc) return rc;
+    plan.early_term = o->early_term != 0;
+    plan.eps_A = eps;
+    return PARAEXP_OK;
 }
 
 }  // namespace pe

@@ -537,8 +537,10 @@ template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
 __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
-    T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode) {
+    T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
     using G = Geo<T, BX, BY>;
+    if (et.norms && et_skip(et)) return;                  // early termination (f2)
+    double dacc = 0.0, yacc = 0.0;                        // ||delta y||^2, ||y||^2 (energy norm)
     using SL = StageL<T, EM, HA, G>;
     constexpr int NR = ONEBAR ? 3 : 2;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -736,6 +738,28 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
                     y4 = y4 + cl * wn4;
                     y5 = y5 + cl * wn5;
                 }
+                if (et.norms) {   // energy weights 1/(cE sigma), 1/(cH sigma) at the own point
+                    T g[6] = {bEk0, bEk1, bEk2, bH0, bH1, bH2};
+                    if (EM == 2) {
+                        g[0] = P0[SL::ST + sB] * cf.sig;
+                        g[1] = P0[SL::ST + G::PL + sB] * cf.sig;
+                        g[2] = P0[SL::ST + 2 * G::PL + sB] * cf.sig;
+                    }
+                    if (HA) {
+                        const int ch = SL::ST + SL::CE;
+                        g[3] = P0[ch + sB] * cf.sig;
+                        g[4] = P0[ch + G::PL + sB] * cf.sig;
+                        g[5] = P0[ch + 2 * G::PL + sB] * cf.sig;
+                    }
+                    const T yn[6] = {y0, y1, y2, y3, y4, y5}, yo6[6] = {yv0, yv1, yv2, yv3, yv4, yv5};
+#pragma unroll
+                    for (int c = 0; c < 6; ++c)
+                        if (g[c] != T(0)) {
+                            const double d = (double)yn[c] - (double)yo6[c], v = (double)yn[c];
+                            dacc += d * d / (double)g[c];
+                            yacc += v * v / (double)g[c];
+                        }
+                }
                 T *yo = y + go;
                 yo[0] = y0;
                 yo[D.cs] = y1;
@@ -755,6 +779,15 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
         }
         if (ONEBAR) __syncthreads();
         lcount += nplanes;
+    }
+    if (et.norms) {
+        const double ds = block_sum(dacc);
+        __syncthreads();
+        const double ys = block_sum(yacc);
+        if (tid == 0) {
+            atomicAdd(et.norms + 2 * et.op, ds);
+            atomicAdd(et.norms + 2 * et.op + 1, ys);
+        }
     }
 }
 
@@ -1283,9 +1316,14 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     if ((rc = make_map<T>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
     if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
     int init = 1;
+    EtDev et;
+    if (ka.et) et = *ka.et;
+    int opi = 0;
     for (const Op &op : plan.ops) {
+        et.op = opi++;
+        et.apps = op.kind == 1 ? 1 : 2;
         kern<<<grid, G::NTHR, Cfg::pair_smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, sch, T(op.a), T(op.b),
-                                                   T(op.e2), T(op.c), init, op.kind);
+                                                   T(op.e2), T(op.c), init, op.kind, et);
         ++*ka.launches;
         if (op.kind == 0) {
             std::swap(w, sp);
@@ -1358,7 +1396,7 @@ int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
         constexpr bool HA = decltype(tHA)::value;
         // K2r measured slower than K2 on B200 (fp64 306 vs 289 us per A-application: barrier
         // stalls -- the frame threads idle through phase B); opt-in with PARAEXP_PAIR_R=1
-        if (pair_r_enabled()) {
+        if (pair_r_enabled() && !ka.et) {   // K2r has no early-termination path
             if (pair_stages(sizeof(T) == 8) == 4) return poly_r_V<T, EM, HA, 4>(ka, plan, bufs);
             return poly_r_V<T, EM, HA, 3>(ka, plan, bufs);
         }

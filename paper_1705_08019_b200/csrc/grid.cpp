@@ -230,6 +230,8 @@ void grid_free_device(Grid &G) {
     dev_free(G.d_red);
     dev_free(G.d_src);
     dev_free(G.d_q);
+    dev_free(G.d_et);
+    G.d_et = nullptr;
     for (void *q : G.kry) dev_free(q);
     G.kry.clear();
     dev_free(G.d_canon[0]);

@@ -61,6 +61,7 @@ struct Grid {
     void *d_q = nullptr;        // source amplitude table
     void *d_canon[2] = {nullptr, nullptr};   // canonical-layout staging of host-pointer fields
     std::vector<void *> kry;    // Krylov basis vectors (f3), allocated on first use
+    void *d_et = nullptr;       // early-termination norms / flags (f2)
     int64_t d_q_cap = 0;
     int64_t device_bytes = 0;
     size_t esize() const { return dtype == PARAEXP_F64 ? 8 : 4; }
@@ -86,6 +87,8 @@ struct Plan {
     std::vector<double> node_im;   // Im of capacity-scaled nodes 2*xi (Leja), empty (Taylor)
     std::vector<double> d_re, d_im;
     std::vector<Op> ops;
+    bool early_term = false;       // f2: stop a substep on two small consecutive increments
+    double eps_A = 0;
 };
 int make_plan(int method, int m, int s, double eps_A, double tau, double rho, double dt,
               Plan &out);
@@ -104,10 +107,23 @@ int dev_set_device(int device);
 int dev_sync(void *stream);
 int check_cuda(const char *what);
 
+// early termination of the Newton sum (f2; reading 18): per op the kernels accumulate the
+// energy norms ||delta y||^2 and ||y||^2 into norms[2 op], norms[2 op + 1]; a launch whose two
+// predecessors both had ||delta|| <= eps ||y|| sets *done and returns, as do all later launches
+// of the substep; *count accumulates the A-applications actually performed.
+struct EtDev {
+    double *norms = nullptr;   // nullptr = early termination off
+    int *done = nullptr;
+    int *count = nullptr;
+    double eps2 = 0;
+    int op = 0, apps = 0;
+};
+
 struct KernelArgs {
     const Grid *g;
     void *stream;
     int64_t *launches;
+    const EtDev *et = nullptr;   // per-call early-termination buffers (op/apps set per launch)
 };
 
 // per-step trace outputs of a leapfrog sequence (f1): device pointers at the row of the

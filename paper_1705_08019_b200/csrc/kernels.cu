@@ -232,34 +232,54 @@ __global__ void __launch_bounds__(256) pair_update_kernel(Dev<T> D, Coef<T, EM, 
                                                           T *__restrict__ w,
                                                           const T *__restrict__ u,
                                                           T *__restrict__ y, T a, T b, T e2, T cl,
-                                                          int init, int mode) {
+                                                          int init, int mode, EtDev et) {
+    if (et.norms && et_skip(et)) return;                  // early termination (f2)
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y * blockDim.y + threadIdx.y;
     const int k = blockIdx.z;
-    if (i >= D.nx || j >= D.ny) return;
-    const int64_t idx = D.idx(i, j, k);
-    T xu[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
-    if (mode != 1) {
-        T a0, a1, a2, b0, b1, b2;
-        curlT_at(D, u + 3 * D.cs, u + 4 * D.cs, u + 5 * D.cs, i, j, k, idx, a0, a1, a2);
-        curl_at(D, u, u + D.cs, u + 2 * D.cs, i, j, k, idx, b0, b1, b2);
-        xu[0] = D.e_live(0, i, j, k) ? cf.bE(0, k, idx) * a0 : T(0);
-        xu[1] = D.e_live(1, i, j, k) ? cf.bE(1, k, idx) * a1 : T(0);
-        xu[2] = D.e_live(2, i, j, k) ? cf.bE(2, k, idx) * a2 : T(0);
-        xu[3] = D.h_live(0, i, j, k) ? -(cf.bH(0, idx) * b0) : T(0);
-        xu[4] = D.h_live(1, i, j, k) ? -(cf.bH(1, idx) * b1) : T(0);
-        xu[5] = D.h_live(2, i, j, k) ? -(cf.bH(2, idx) * b2) : T(0);
-    }
+    double dacc = 0.0, yacc = 0.0;
+    if (i < D.nx && j < D.ny) {
+        const int64_t idx = D.idx(i, j, k);
+        T xu[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
+        if (mode != 1) {
+            T a0, a1, a2, b0, b1, b2;
+            curlT_at(D, u + 3 * D.cs, u + 4 * D.cs, u + 5 * D.cs, i, j, k, idx, a0, a1, a2);
+            curl_at(D, u, u + D.cs, u + 2 * D.cs, i, j, k, idx, b0, b1, b2);
+            xu[0] = D.e_live(0, i, j, k) ? cf.bE(0, k, idx) * a0 : T(0);
+            xu[1] = D.e_live(1, i, j, k) ? cf.bE(1, k, idx) * a1 : T(0);
+            xu[2] = D.e_live(2, i, j, k) ? cf.bE(2, k, idx) * a2 : T(0);
+            xu[3] = D.h_live(0, i, j, k) ? -(cf.bH(0, idx) * b0) : T(0);
+            xu[4] = D.h_live(1, i, j, k) ? -(cf.bH(1, idx) * b1) : T(0);
+            xu[5] = D.h_live(2, i, j, k) ? -(cf.bH(2, idx) * b2) : T(0);
+        }
 #pragma unroll
-    for (int c = 0; c < 6; ++c) {
-        const int64_t q = c * D.cs + idx;
-        const T wv = w[q];
-        const T uv = u[q];
-        const T y0 = init ? T(0) : y[q];
-        T yn = (y0 + a * wv) + b * uv;
-        if (mode == 2) yn = yn + cl * (xu[c] + e2 * wv);
-        y[q] = yn;
-        if (mode == 0) w[q] = xu[c] + e2 * wv;
+        for (int c = 0; c < 6; ++c) {
+            const int64_t q = c * D.cs + idx;
+            const T wv = w[q];
+            const T uv = u[q];
+            const T y0 = init ? T(0) : y[q];
+            T yn = (y0 + a * wv) + b * uv;
+            if (mode == 2) yn = yn + cl * (xu[c] + e2 * wv);
+            y[q] = yn;
+            if (mode == 0) w[q] = xu[c] + e2 * wv;
+            if (et.norms) {
+                const T g = c < 3 ? cf.bE(c, k, idx) : cf.bH(c - 3, idx);
+                if (g != T(0)) {
+                    const double d = (double)yn - (double)y0, v = (double)yn;
+                    dacc += d * d / (double)g;
+                    yacc += v * v / (double)g;
+                }
+            }
+        }
+    }
+    if (et.norms) {
+        const double ds = block_sum(dacc);
+        __syncthreads();
+        const double ys = block_sum(yacc);
+        if (threadIdx.x == 0 && threadIdx.y == 0) {
+            atomicAdd(et.norms + 2 * et.op, ds);
+            atomicAdd(et.norms + 2 * et.op + 1, ys);
+        }
     }
 }
 
@@ -454,10 +474,15 @@ int k_poly_substep_unfused(const KernelArgs &ka, const Plan &plan, void *bufs[4]
         cudaStream_t s = (cudaStream_t)ka.stream;
         T *w = (T *)bufs[0], *yy = (T *)bufs[1], *uu = (T *)bufs[2];
         int init = 1;
+        EtDev et;
+        if (ka.et) et = *ka.et;
+        int opi = 0;
         for (const Op &op : plan.ops) {
+            et.op = opi++;
+            et.apps = op.kind == 1 ? 1 : 2;
             applyX_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, w, uu);
             pair_update_kernel<T, EM, HA><<<grid, kBlock, 0, s>>>(D, cf, w, uu, yy, T(op.a), T(op.b), T(op.e2),
-                                                                  T(op.c), init, op.kind);
+                                                                  T(op.c), init, op.kind, et);
             *ka.launches += 2;
             init = 0;
         }

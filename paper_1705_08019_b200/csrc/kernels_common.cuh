@@ -141,6 +141,28 @@ __device__ __forceinline__ double block_sum(double v) {
     return r;   // valid in thread 0
 }
 
+// Early termination (f2): called by every thread at kernel start; true => return at once.
+// Thread 0 of each block evaluates the criterion on the norms of the two previous ops (all
+// blocks see the same values, so they agree); block 0 records the decision / the count.
+__device__ __forceinline__ bool et_skip(const EtDev &et) {
+    __shared__ int s_skip;
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        int skip = *(volatile int *)et.done;
+        if (!skip && et.op >= 2) {
+            const double d1 = et.norms[2 * (et.op - 1)], y1 = et.norms[2 * (et.op - 1) + 1];
+            const double d2 = et.norms[2 * (et.op - 2)], y2 = et.norms[2 * (et.op - 2) + 1];
+            if (d1 <= et.eps2 * y1 && d2 <= et.eps2 * y2) skip = 1;
+        }
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+            if (skip) *et.done = 1;
+            else atomicAdd(et.count, et.apps);
+        }
+        s_skip = skip;
+    }
+    __syncthreads();
+    return s_skip != 0;
+}
+
 // Dispatch on (dtype, material mode, h-array):  fn(T{}, integral_constant<EM>, bool_constant<HA>)
 template <typename Fn>
 int with_types(const Grid &g, double /*sigma*/, Fn &&fn) {

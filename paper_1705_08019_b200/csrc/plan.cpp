@@ -255,7 +255,7 @@ int make_plan(int method, int m, int s, double eps_A, double tau, double rho, do
     if (!(rho >= 0) || !std::isfinite(rho)) return fail(PARAEXP_EINVAL, "rho must be >= 0");
     if (m < 0 || m > PARAEXP_MAX_DEGREE || (m > 1 && m % 2)) return fail(PARAEXP_EINVAL, "degree m must be 1 or even and <= 100");
     if (s < 0) return fail(PARAEXP_EINVAL, "s must be >= 0");
-    if ((m == 0 || s == 0) && !(eps_A > 1e-14 && eps_A < 1)) return fail(PARAEXP_EINVAL, "eps_A must lie in (1e-14, 1)");
+    if ((m == 0 || s == 0) && !(eps_A >= 1e-14 && eps_A < 1)) return fail(PARAEXP_EINVAL, "eps_A must lie in [1e-14, 1)");
     out = Plan();
     out.method = method;
     out.tau = tau;
@@ -343,6 +343,20 @@ int paraexp_leja_points(int32_t count, double *xi) {
     pe::leja_sequence(count, v);
     std::copy(v.begin(), v.end(), xi);
     return PARAEXP_OK;
+}
+
+double paraexp_optimal_tolerance(double dt, double beta, double norm_A, int32_t *clamped) {
+    if (clamped) *clamped = 0;
+    const double v = beta * dt * dt / norm_A;
+    if (!(dt > 0) || !(beta > 0) || !(norm_A > 0) || !std::isfinite(v)) {
+        if (clamped) *clamped = 1;
+        return 0.1;
+    }
+    if (v < 1e-14 || v > 0.1) {
+        if (clamped) *clamped = 1;
+        return v < 1e-14 ? 1e-14 : 0.1;
+    }
+    return v;
 }
 
 double paraexp_theta(int32_t method, int32_t m, double eps_A) {

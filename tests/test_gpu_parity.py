@@ -298,3 +298,24 @@ def test_solve_krylov_tails():
     ref = fit.paraexp_finish(og, parts[-1], (We, Wh), rho)
     ge, gh, st = lib_solve(lg, 40, 4, src, u0=u0, method="krylov", m=16, s=2, rho=rho)
     assert_parity((ge, gh), ref, "f64", "solve krylov")
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("kind", ["layered", "random"])
+@pytest.mark.parametrize("kernels", KERNELS)
+def test_expmv_early_termination(dtype, kind, kernels):
+    """f2: the device-side early termination (fused block-reduced energy norms + skip flag)
+    makes the same stop decisions as the oracle and gives the same result."""
+    n = (21, 19, 13)
+    og, lg = _grids(n, kind, dtype, kernels)
+    e, h = inputs(og, *random_fields(*n, seed=19))
+    rho = og.rho_cfl
+    tau = 1.0 * og.dt
+    eps = 1e-6 if dtype == "f32" else 1e-9
+    plan = fit.make_plan("leja", 60, 2, tau, rho)
+    ref_e, ref_h, apps = fit.expmv_pairs_et(og, plan, e, h, eps, dtype=dtype)
+    assert apps < 120
+    ge, gh, st = lib_expmv(lg, tau, e, h, method="leja", m=60, s=2, rho=rho, eps_A=eps,
+                           early_term=True)
+    assert st["a_applications"] == apps
+    assert_parity((ge, gh), (ref_e, ref_h), dtype, f"expmv early-term {kind}")

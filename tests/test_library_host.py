@@ -139,3 +139,16 @@ def test_host_only_grid_has_no_compute():
     rc = abi.lib.paraexp_leapfrog(g.handle, None, 0, 0.0, 1, abi.C.c_void_p(8), abi.C.c_void_p(8),
                                   0, None, abi.C.byref(st))
     assert rc == pe.ENOTSUP
+
+
+def test_optimal_tolerance_spec_examples():
+    """eq:tolerance_leja_2 through the library's host helper: SPEC's worked
+    examples (beta = 1, dt = 1e-9, ||A|| = 1e9 -> 1e-27 clamped to the 1e-14 floor; quadrupling
+    dt multiplies eps* by 16; halving ||A|| doubles it)."""
+    import paper_1705_08019_b200 as pe
+    v, cl = pe.optimal_tolerance(1e-9, 1.0, 1e9)
+    assert v == 1e-14 and cl
+    a, _ = pe.optimal_tolerance(1e-12, 1e30, 1e12)
+    b, _ = pe.optimal_tolerance(4e-12, 1e30, 1e12)
+    c, _ = pe.optimal_tolerance(1e-12, 1e30, 0.5e12)
+    assert abs(a - 1e-6) < 1e-20 and abs(b / a - 16) < 1e-12 and abs(c / a - 2) < 1e-12

@@ -190,3 +190,26 @@ def test_fp32_constant_recipe_close_to_fp64():
     for x, y in zip(a, b):
         r = np.linalg.norm(x - y) / np.linalg.norm(x)
         assert 1e-10 < r < 1e-5
+
+
+def test_early_termination_oracle():
+    """f2 (reading 18): with a degree much larger than the substep needs, the
+    early-terminated Newton sum stops after fewer A-applications and stays within ~eps of the
+    full sum (and of the dense exponential)."""
+    n = (4, 4, 3)
+    g = fit.Grid(*n, d0=1e-3, eps_r=np.random.default_rng(5).uniform(1, 4, 48), dt_frac=0.9)
+    e, h = _state(g, 3)
+    tau = 1.0 * g.dt
+    rho = g.rho_cfl
+    plan = fit.make_plan("leja", 60, 2, tau, rho)
+    fe, fh = fit.expmv(g, plan, e, h)
+    for eps in (1e-6, 1e-10):
+        te, th, apps = fit.expmv_pairs_et(g, plan, e, h, eps)
+        assert apps < 60 * 2
+        full = np.concatenate([fe, fh])
+        err = np.linalg.norm(np.concatenate([te, th]) - full) / np.linalg.norm(full)
+        assert err <= 10 * eps
+    # eps tiny: no early stop possible before the end -> identical to the plain sum
+    te, th, apps = fit.expmv_pairs_et(g, fit.make_plan("leja", 8, 3, 10 * g.dt, rho), e, h, 1e-15)
+    pe_, ph_ = fit.expmv(g, fit.make_plan("leja", 8, 3, 10 * g.dt, rho), e, h)
+    assert apps == 24 and np.array_equal(te, pe_) and np.array_equal(th, ph_)
