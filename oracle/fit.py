@@ -139,7 +139,8 @@ class Grid:
 
     @classmethod
     def from_workload(cls, w, dtype=None):
-        return cls(w.nx, w.ny, w.nz, d0=w.d0, eps_r=w.eps_r, pec_cell=w.pec_cell,
+        return cls(w.nx, w.ny, w.nz, d0=w.d0, dx=getattr(w, "dx", None), dy=getattr(w, "dy", None),
+                   dz=getattr(w, "dz", None), eps_r=w.eps_r, pec_cell=w.pec_cell,
                    dt_frac=w.dt_frac, dtype=dtype or w.dtype)
 
     def cfl(self):
@@ -774,6 +775,35 @@ def paraexp_finish(g: Grid, P, W, rho, mode: str = "pairs", dtype: Optional[str]
 def cost_proc(nt: int, p: int, n_leja: int) -> float:
     """eq:tot_cost, PAPER:474-477: C_proc = (2/p) n_t + n_Leja + 2."""
     return 2.0 * nt / p + n_leja + 2
+
+
+def norm_A(g: Grid, tol: float = 1e-10) -> float:
+    """||A||_2 of the normal A = T A_orig T^-1 (lambda_max = ||A||_2), as the
+    square root of the largest eigenvalue of the symmetric PSD operator -A^2 = A^T A on the
+    live DOFs, from scipy's ARPACK (eigsh) on a LinearOperator that applies A_orig through the
+    oracle's own stencil (X = dt A_orig, then / dt).  T = sqrt(M_eps) on e, sqrt(M_mu) on h."""
+    from scipy.sparse.linalg import LinearOperator, eigsh
+    n3 = 3 * g.Np
+    X = ScaledOp(g, 1.0, "f64")
+    Te = np.where(g.live_e, np.sqrt(np.where(g.live_e, g.Meps, 1.0)), 0.0)
+    Mmu = g.M_mu_w()
+    Th = np.where(g.live_h, np.sqrt(np.where(g.live_h, Mmu, 1.0)), 0.0)
+    Ti = np.concatenate([np.where(Te > 0, 1.0 / np.where(Te > 0, Te, 1.0), 0.0),
+                         np.where(Th > 0, 1.0 / np.where(Th > 0, Th, 1.0), 0.0)])
+    T = np.concatenate([Te, Th])
+
+    def mv(x):
+        x = np.asarray(x, float).reshape(-1)
+        u = Ti * x
+        ae, ah = X(u[:n3], u[n3:])
+        ae, ah = X(ae, ah)
+        return -(T * np.concatenate([ae, ah]))
+
+    op = LinearOperator((2 * n3, 2 * n3), matvec=mv, dtype=np.float64)
+    # seeded random start on the live DOFs (a symmetric start can be orthogonal to the top mode)
+    v0 = np.random.default_rng(12345).uniform(-1, 1, 2 * n3) * np.concatenate([g.live_e, g.live_h])
+    lam = eigsh(op, k=1, which="LA", tol=tol, v0=v0, return_eigenvectors=False)[0]
+    return math.sqrt(max(lam, 0.0)) / g.dt
 
 
 # ---------------------------------------------------------------------------

@@ -76,7 +76,8 @@ class Grid:
 
     @classmethod
     def from_workload(cls, w, device=0, dtype=None, kernels="auto"):
-        return cls(w.nx, w.ny, w.nz, d0=w.d0, eps_r=w.eps_r, pec_cell=w.pec_cell,
+        return cls(w.nx, w.ny, w.nz, d0=w.d0, dx=getattr(w, "dx", None), dy=getattr(w, "dy", None),
+                   dz=getattr(w, "dz", None), eps_r=w.eps_r, pec_cell=w.pec_cell,
                    dtype=dtype or w.dtype, device=device, dt_frac=w.dt_frac, kernels=kernels)
 
     @property

@@ -81,6 +81,10 @@ class Workload:
     s: int = 0                          # fixed substeps per propagator (0 = auto)
     eps_A: float = 1e-12
     note: str = ""
+    dx: Optional[np.ndarray] = None     # per-cell spacings (non-uniform meshes); None = d0
+    dy: Optional[np.ndarray] = None
+    dz: Optional[np.ndarray] = None
+    t_end: Optional[float] = None        # interval length T when nsteps follows from dt
 
     @property
     def cells(self) -> int:
@@ -235,3 +239,26 @@ def config_c5(n=128, dtype="f32", nsteps=1024, p=8) -> Workload:
     """C5: uniform vacuum n^3, 1 mm, random e/h (seed 5+n, DESIGN reading 26), no source."""
     return Workload(f"C5-{n}-{dtype}", n, n, n, 1e-3, dtype, 0.95, nsteps, p,
                     u0_seed=5 + n, method="leja", m=64, s=1, eps_A=1e-12)
+
+
+def config_wave2d(n_pts=41, k=1.0, nsteps=None, p=8, dt_frac=0.99, dtype="f64") -> Workload:
+    """The paper's two-dimensional cylindrical wave (Fig. 2): vacuum PEC box
+    L_x = L_y = 20 m, L_z = 1 m ("L_y = 1 m" read as L_z, reading 21), n_x = n_y =
+    n_pts points (41: Leapfrog/Leja, 121: reference), n_z = 2 points (one cell layer), line
+    current in z at the centre, eq:line_current with i_max = 1 A, sigma_t = 2e-8 s, T = 2e-7 s.
+    k > 1: the R(k) study: one element shrunk so that biggest/smallest element
+    size = k -- here the centre column and row of cells get dx = dy = Delta/k (reading 32;
+    the rest of the mesh is unchanged).  nsteps = None leaves n_t to the consumer:
+    n_t = ceil(T / dt) with its own dt (t_end = T)."""
+    nc = n_pts - 1
+    d = 20.0 / nc
+    dx = np.full(nc, d)
+    dy = np.full(nc, d)
+    dz = np.full(1, 1.0)
+    c = nc // 2
+    if k != 1.0:
+        dx[c] = d / k
+        dy[c] = d / k
+    src = [Source(2, c, c, 0, "gauss_paper", 1.0, 2e-8)]
+    return Workload(f"wave2d-{n_pts}-k{k:g}", nc, nc, 1, d, dtype, dt_frac, nsteps or 0, p,
+                    sources=src, method="leja", eps_A=1e-2, dx=dx, dy=dy, dz=dz, t_end=2e-7)

@@ -319,3 +319,59 @@ def test_expmv_early_termination(dtype, kind, kernels):
                            early_term=True)
     assert st["a_applications"] == apps
     assert_parity((ge, gh), (ref_e, ref_h), dtype, f"expmv early-term {kind}")
+
+
+@pytest.mark.parametrize("kernels", KERNELS)
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_nonuniform_mesh(kernels, dtype):
+    """f4: non-uniform spacings dx, dy, dz (per-edge cE and per-face cH arrays) -- leapfrog
+    and expmv vs the oracle."""
+    n = (23, 17, 9)
+    rng = np.random.default_rng(8)
+    dx, dy, dz = (rng.uniform(0.3e-3, 1.5e-3, k) for k in n)
+    kw = dict(dx=dx, dy=dy, dz=dz, dt_frac=0.95, dtype=dtype)
+    og = fit.Grid(*n, **kw)
+    lg = pe.Grid(*n, kernels=kernels, **kw)
+    assert lg.info()["material_mode"] == pe.abi.MAT_ARRAY
+    e, h = inputs(og, *random_fields(*n, seed=23))
+    src = _sources(og, n)
+    ref = fit.leapfrog(og, e, h, 200, src)
+    ge, gh, _ = lib_leapfrog(lg, e, h, 200, src)
+    assert_parity((ge, gh), ref, dtype, "non-uniform leapfrog")
+    plan = fit.make_plan("leja", 32, 3, 20 * og.dt, og.rho_cfl)
+    ref2 = fit.expmv(og, plan, *ref, dtype=dtype)
+    ge2, gh2, _ = lib_expmv(lg, 20 * og.dt, *ref, m=32, s=3, rho=og.rho_cfl)
+    assert_parity((ge2, gh2), ref2, dtype, "non-uniform expmv")
+
+
+@pytest.mark.parametrize("k", [1, 10])
+def test_wave2d_solve(k):
+    """The paper's 2-D cylindrical wave (41 x 41 x 2) over its full interval
+    T = 2e-7 s, with one small element of ratio k (the R(k) study mesh): ParaExp p = 8 vs the
+    oracle at a fixed Leja plan."""
+    from synth import config_wave2d
+    w = config_wave2d(41, k)
+    og = fit.Grid.from_workload(w)
+    lg = pe.Grid.from_workload(w)
+    nt = math.ceil(w.t_end / og.dt)
+    nt += (-nt) % 8
+    rho = 1.05 * fit.norm_A(og)
+    S = fit.partition(nt, 8)
+    s = _fixed_s("leja", 40, 1e-10, (S[1] - S[0]) * og.dt, rho)
+    ref = fit.paraexp(og, w.sources, 0.0, nt, 8, lambda tau: fit.make_plan("leja", 40, s, tau, rho),
+                      rho=rho)
+    ge, gh, st = lib_solve(lg, nt, 8, w.sources, method="leja", m=40, s=s, rho=rho)
+    assert_parity((ge, gh), ref, "f64", f"wave2d k={k}")
+    assert np.linalg.norm(ref[0]) > 0
+
+
+@pytest.mark.parametrize("k", [1, 5, 20])
+def test_rho_pow_vs_oracle_norm(k):
+    """K5 (library Lanczos) vs the oracle's ARPACK ||A||_2 on the R(k) meshes (SPEC: 1e-3)."""
+    from synth import config_wave2d
+    w = config_wave2d(41, k)
+    og = fit.Grid.from_workload(w)
+    lg = pe.Grid.from_workload(w)
+    rp = lg.info(compute_rho_pow=True)["rho_pow"]
+    ref = fit.norm_A(og)
+    assert abs(rp - ref) <= 1e-3 * ref, (rp, ref)
