@@ -128,7 +128,7 @@ def test_solve_c1():
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("p", [1, 3, 4])
+@pytest.mark.parametrize("p", [1, 3, 4, 61])
 @pytest.mark.parametrize("kernels", KERNELS)
 def test_solve_random_u0(dtype, p, kernels):
     n = (19, 17, 9)
