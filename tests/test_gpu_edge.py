@@ -151,3 +151,21 @@ def test_host_pointer_fields(pinned):
     torch.cuda.synchronize()
     assert torch.equal(eo_d.cpu(), eo_h) and torch.equal(ho_d.cpu(), ho_h)
     assert eo_h.abs().max() > 0
+
+
+def test_c_example_runs(tmp_path):
+    """examples/cavity_solve.c through the C ABI from plain C with host buffers: runs, and the
+    ParaExp (exp tails) vs serial leapfrog gap on C1 is small but nonzero (O(dt^2) tails)."""
+    import os
+    import re
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_1705_08019_b200")
+    exe = tmp_path / "cavity_solve"
+    subprocess.check_call(["gcc", "-std=c11", "-O2", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "examples", "cavity_solve.c"), "-L", libdir,
+                           "-l:libparaexp.so", f"-Wl,-rpath,{libdir}", "-lm", "-o", str(exe)])
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    rel = float(re.search(r"= ([0-9.e+-]+)\s*$", out.stdout.strip()).group(1))
+    assert 0 < rel < 0.2, out.stdout

@@ -152,3 +152,16 @@ def test_optimal_tolerance_spec_examples():
     b, _ = pe.optimal_tolerance(4e-12, 1e30, 1e12)
     c, _ = pe.optimal_tolerance(1e-12, 1e30, 0.5e12)
     assert abs(a - 1e-6) < 1e-20 and abs(b / a - 16) < 1e-12 and abs(c / a - 2) < 1e-12
+
+
+def test_c_example_compiles_and_links(tmp_path):
+    """The ABI is plain C: examples/cavity_solve.c (no Python, no CUDA headers) compiles with
+    gcc -std=c11 against include/paraexp.h and links against libparaexp.so."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_1705_08019_b200")
+    exe = tmp_path / "cavity_solve"
+    subprocess.check_call(["gcc", "-std=c11", "-O2", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "examples", "cavity_solve.c"), "-L", libdir,
+                           "-l:libparaexp.so", f"-Wl,-rpath,{libdir}", "-lm", "-o", str(exe)])
+    assert exe.exists()
