@@ -544,8 +544,8 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_r_kernel(
 // ---------------------------------------------------------------------------------------
 // Phase A of iteration k: u_e(k+1) on the +1 halo and u_h(k) on the -1 halo; phase B: the
 // tile's w'(k) and y(k).  Ring depth 2 (two barriers per plane) or 3 (ONEBAR).
-template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
-__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
+template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR, int MINB = 1>
+__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, MINB) pair_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
     T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
@@ -1313,13 +1313,13 @@ int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const 
     });
 }
 
-template <typename T, int EM, bool HA, int S, bool ONEBAR>
+template <typename T, int EM, bool HA, int S, bool ONEBAR, int MINB = 1>
 static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     constexpr int BX = 32, BY = 8;
     using Cfg = FusedCfg<T, EM, HA, BX, BY, S, ONEBAR>;
     using G = Geo<T, BX, BY>;
     const Grid &g = *ka.g;
-    auto kern = pair_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR>;
+    auto kern = pair_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR, MINB>;
     static const int per_sm = resident_per_sm(kern, G::NTHR, Cfg::pair_smem);
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "fused pair kernel does not fit on an SM");
     const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
@@ -1421,6 +1421,8 @@ int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
             return poly_r_V<T, EM, HA, 3>(ka, plan, bufs);
         }
         if (onebar()) return poly_fused_V<T, EM, HA, 4, true>(ka, plan, bufs);
+        if (getenv("PARAEXP_PAIR_OCC3"))   // experiment: 2 stages, 3 CTAs/SM register budget
+            return poly_fused_V<T, EM, HA, 2, false, 3>(ka, plan, bufs);
         switch (pair_stages(sizeof(T) == 8)) {
             case 2: return poly_fused_V<T, EM, HA, 2, false>(ka, plan, bufs);
             case 4: return poly_fused_V<T, EM, HA, 4, false>(ka, plan, bufs);
