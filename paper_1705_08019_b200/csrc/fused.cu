@@ -404,12 +404,6 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_r_kernel(
         // carried own-point values: h(k) (x, y, z) and e'(k) (x, y, z) of the previous plane
         T hxk = T(0), hyk = T(0), hzk = T(0), ek0 = T(0), ek1 = T(0), ek2 = T(0);
         T g0 = bH0, g1 = bH1, g2 = bH2;                    // cH at the own point, plane k (HA)
-        T nE0 = bE0, nE1 = bE1, nE2 = bE2;                // ztable: coefficients of the next plane
-        if (EM == 1) {
-            nE0 = __ldg(cf.tab + kb) * cf.sig;
-            nE1 = __ldg(cf.tab + D.nz + kb) * cf.sig;
-            nE2 = __ldg(cf.tab + 2 * D.nz + kb) * cf.sig;
-        }
         if (tid == 0)
             for (int p = 0; p < min(S, nplanes); ++p) {
                 const uint32_t L = lcount + p;
@@ -425,15 +419,10 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_r_kernel(
             const T *P1 = stages + (L1 % S) * SL::SZ;
             T *R1 = ring + (kk & 1) * 3 * G::RP;
             const T *R0 = ring + (k & 1) * 3 * G::RP;
-            if (EM == 1) {                                // plane kk: prefetched one iteration ago
-                bE0 = nE0;
-                bE1 = nE1;
-                bE2 = nE2;
-                if (kk + 1 < D.nz) {
-                    nE0 = __ldg(cf.tab + kk + 1) * cf.sig;
-                    nE1 = __ldg(cf.tab + D.nz + kk + 1) * cf.sig;
-                    nE2 = __ldg(cf.tab + 2 * D.nz + kk + 1) * cf.sig;
-                }
+            if (EM == 1 && kk < D.nz) {
+                bE0 = __ldg(cf.tab + kk) * cf.sig;
+                bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
+                bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
             }
             if (p == 0 && hasA) {                         // h(kb-1) at the own point
                 hxk = P0[3 * G::PL + sA];
@@ -544,8 +533,8 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_r_kernel(
 // ---------------------------------------------------------------------------------------
 // Phase A of iteration k: u_e(k+1) on the +1 halo and u_h(k) on the -1 halo; phase B: the
 // tile's w'(k) and y(k).  Ring depth 2 (two barriers per plane) or 3 (ONEBAR).
-template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR, int MINB = 1>
-__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, MINB) pair_fused_kernel(
+template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
+__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
     T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
@@ -598,17 +587,6 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, MINB) pair_fused_kernel(
         const bool lxBe = jB > 0, lyBe = iB > 0, lzBe = iB > 0 && jB > 0;
         const bool lxBh = iB > 0, lyBh = jB > 0;
         const int64_t gB = D.idx(inB ? iB : 0, inB ? jB : 0, 0);
-        T nE0 = bE0, nE1 = bE1, nE2 = bE2;                // ztable: coefficients of the next plane
-        if (EM == 1) {
-            if (kb >= 1) {
-                bE0 = __ldg(cf.tab + kb - 1) * cf.sig;
-                bE1 = __ldg(cf.tab + D.nz + kb - 1) * cf.sig;
-                bE2 = __ldg(cf.tab + 2 * D.nz + kb - 1) * cf.sig;
-            }
-            nE0 = __ldg(cf.tab + kb) * cf.sig;
-            nE1 = __ldg(cf.tab + D.nz + kb) * cf.sig;
-            nE2 = __ldg(cf.tab + 2 * D.nz + kb) * cf.sig;
-        }
         if (tid == 0)
             for (int p = 0; p < min(S, nplanes); ++p) {
                 const uint32_t L = lcount + p;
@@ -637,14 +615,16 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, MINB) pair_fused_kernel(
             T *UE1 = UE + (kk % NR) * 3 * G::RP;           // u_e(k+1)
             T *UH0 = UH + ((k + NR) % NR) * 3 * G::RP;    // u_h(k)
             T bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;         // coefficients at plane k (phase B)
-            if (EM == 1) {                                // plane kk: prefetched one iteration ago
-                bE0 = nE0;
-                bE1 = nE1;
-                bE2 = nE2;
-                if (kk + 1 < D.nz) {
-                    nE0 = __ldg(cf.tab + kk + 1) * cf.sig;
-                    nE1 = __ldg(cf.tab + D.nz + kk + 1) * cf.sig;
-                    nE2 = __ldg(cf.tab + 2 * D.nz + kk + 1) * cf.sig;
+            if (EM == 1) {
+                if (kk < D.nz) {
+                    bE0 = __ldg(cf.tab + kk) * cf.sig;
+                    bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
+                    bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
+                }
+                if (k >= 0) {
+                    bEk0 = __ldg(cf.tab + k) * cf.sig;
+                    bEk1 = __ldg(cf.tab + D.nz + k) * cf.sig;
+                    bEk2 = __ldg(cf.tab + 2 * D.nz + k) * cf.sig;
                 }
             }
             if (hasA) {
@@ -1313,13 +1293,13 @@ int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const 
     });
 }
 
-template <typename T, int EM, bool HA, int S, bool ONEBAR, int MINB = 1>
+template <typename T, int EM, bool HA, int S, bool ONEBAR>
 static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     constexpr int BX = 32, BY = 8;
     using Cfg = FusedCfg<T, EM, HA, BX, BY, S, ONEBAR>;
     using G = Geo<T, BX, BY>;
     const Grid &g = *ka.g;
-    auto kern = pair_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR, MINB>;
+    auto kern = pair_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR>;
     static const int per_sm = resident_per_sm(kern, G::NTHR, Cfg::pair_smem);
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "fused pair kernel does not fit on an SM");
     const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
@@ -1421,8 +1401,6 @@ int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
             return poly_r_V<T, EM, HA, 3>(ka, plan, bufs);
         }
         if (onebar()) return poly_fused_V<T, EM, HA, 4, true>(ka, plan, bufs);
-        if (getenv("PARAEXP_PAIR_OCC3"))   // experiment: 2 stages, 3 CTAs/SM register budget
-            return poly_fused_V<T, EM, HA, 2, false, 3>(ka, plan, bufs);
         switch (pair_stages(sizeof(T) == 8)) {
             case 2: return poly_fused_V<T, EM, HA, 2, false>(ka, plan, bufs);
             case 4: return poly_fused_V<T, EM, HA, 4, false>(ka, plan, bufs);
