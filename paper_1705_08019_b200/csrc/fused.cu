@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
 //    neighbours of e'(k) are read from shared memory), and phase A carries h(k) at its own
 //    point from the previous plane (only h(k+1) and its i-1 / j-1 neighbours are read).
 template <typename T, int EM, bool HA, int BX, int BY, int S, bool TR>
-__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_r_kernel(
+__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ out,
     Sched sch, SrcList src, const T *__restrict__ q, const __grid_constant__ TraceDev tr) {
@@ -533,8 +533,10 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_r_kernel(
 // ---------------------------------------------------------------------------------------
 // Phase A of iteration k: u_e(k+1) on the +1 halo and u_h(k) on the -1 halo; phase B: the
 // tile's w'(k) and y(k).  Ring depth 2 (two barriers per plane) or 3 (ONEBAR).
+// min 2 CTAs/SM: the measured K2 rate depends on two resident CTAs per SM (a register
+// growth to > 102 per thread halves the occupancy: 376 vs 288 us per A-application)
 template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
-__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) pair_fused_kernel(
+__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 2) pair_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
     T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {

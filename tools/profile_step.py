@@ -1,6 +1,6 @@
 """Small driver for ncu captures: the bench workload's kernels (C3 256^3 layered fp64) on a
 short run -- a few fused leapfrog steps and one degree-100 Leja substep (the planner's choice
-for the bench's sub-intervals).  Usage: python tools/profile_step.py [f64|f32] [lf_steps]"""
+for the bench's sub-intervals).  Usage: python tools/profile_step.py [f64|f32] [lf_steps] [n]"""
 import os
 import sys
 
@@ -15,7 +15,8 @@ from synth import config_c3  # noqa: E402
 def main():
     dtype = sys.argv[1] if len(sys.argv) > 1 else "f64"
     nlf = int(sys.argv[2]) if len(sys.argv) > 2 else 6
-    w = config_c3(dtype)
+    n = int(sys.argv[3]) if len(sys.argv) > 3 else 256
+    w = config_c3(dtype, n=n)
     g = pe.Grid.from_workload(w)
     td = g.torch_dtype()
     e = torch.rand(3 * g.npts, dtype=td, device="cuda:0")
