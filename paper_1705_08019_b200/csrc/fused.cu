@@ -86,7 +86,24 @@ struct Geo {
 
 struct Sched {
     int tiles_x, tiles_y, ntiles, chunk, nchunks, units;
+    // dynamic unit order (ctr != nullptr): CTAs grab units from a grid-owned monotone counter,
+    // so the units in flight are always a contiguous window of the chunk-major sequence and
+    // x/y-neighbour tiles run within a fraction of a unit of each other (their halo planes
+    // stay in L2 however many waves a launch has).  Each launch advances the counter by
+    // exactly units + gridDim (every CTA ends with one failing grab); base is its start.
+    unsigned long long *ctr;
+    unsigned long long base;
 };
+
+// unit loop: static stride (ctr == nullptr) or dynamic grabs; uniform per CTA
+__device__ __forceinline__ int grab_unit(const Sched &sch, int prev) {
+    if (!sch.ctr) return prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
+    __shared__ int s_unit;
+    __syncthreads();                                      // previous s_unit consumed
+    if (threadIdx.x == 0) s_unit = (int)(atomicAdd(sch.ctr, 1ull) - sch.base);
+    __syncthreads();
+    return s_unit;
+}
 
 struct SrcList {
     int n;
@@ -204,7 +221,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
     __syncthreads();
     uint32_t lcount = 0;   // planes loaded by this CTA so far (ring position)
     double eacc = 0.0;     // TR: this thread's energy contributions
-    for (int unit = blockIdx.x; unit < sch.units; unit += gridDim.x) {
+    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
         const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
@@ -385,7 +402,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
     __syncthreads();
     uint32_t lcount = 0;
     double eacc = 0.0;
-    for (int unit = blockIdx.x; unit < sch.units; unit += gridDim.x) {
+    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
         const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
@@ -536,7 +553,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
 // min 2 CTAs/SM: the measured K2 rate depends on two resident CTAs per SM (a register
 // growth to > 102 per thread halves the occupancy: 376 vs 288 us per A-application)
 template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
-__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 2) pair_fused_kernel(
+__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) pair_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
     T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
@@ -571,7 +588,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 2) pair_fused_kernel(
     }
     __syncthreads();
     uint32_t lcount = 0;
-    for (int unit = blockIdx.x; unit < sch.units; unit += gridDim.x) {
+    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
         const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
@@ -847,7 +864,7 @@ __global__ void __launch_bounds__(GeoU<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3)
     }
     __syncthreads();
     uint32_t lcount = 0;
-    for (int unit = blockIdx.x; unit < sch.units; unit += gridDim.x) {
+    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
         const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
@@ -1124,7 +1141,28 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
     s.chunk = bc;
     s.nchunks = (g.nz + bc - 1) / bc;
     s.units = s.ntiles * s.nchunks;
+    s.ctr = nullptr;
+    s.base = 0;
     return s;
+}
+
+// dynamic scheduling (default; PARAEXP_STATIC_SCHED=1 keeps the static stride)
+static bool dynamic_sched() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PARAEXP_STATIC_SCHED");
+        v = (e && atoi(e) != 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+// per-launch Sched with the grid's unit counter; advances the host shadow of the counter
+static Sched launch_sched(const Grid &g, Sched sch, int grid) {
+    Grid &G = const_cast<Grid &>(g);
+    if (!dynamic_sched() || !G.d_sched) return sch;
+    sch.ctr = (unsigned long long *)G.d_sched;
+    sch.base = G.sched_base;
+    G.sched_base += (unsigned long long)sch.units + (unsigned long long)grid;
+    return sch;
 }
 
 template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
@@ -1209,7 +1247,7 @@ static int leapfrog_fused_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps,
             if (!trm.probe) trm.np = 0;
         }
         kern<<<grid, G::NTHR, Cfg::lf_smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf,
-                                                 (T *)(even ? bufs[1] : bufs[0]), sch, sl,
+                                                 (T *)(even ? bufs[1] : bufs[0]), launch_sched(g, sch, grid), sl,
                                                  nsrc ? (const T *)q_dev + m * nsrc : nullptr, trm);
         ++*ka.launches;
     }
@@ -1256,7 +1294,8 @@ static int leapfrog_r_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int
             trm.probe = tr->probe ? tr->probe + m * tr->np : nullptr;
             if (!trm.probe) trm.np = 0;
         }
-        kern<<<grid, G::NTHR, smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf, (T *)(even ? bufs[1] : bufs[0]), sch,
+        kern<<<grid, G::NTHR, smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf, (T *)(even ? bufs[1] : bufs[0]),
+                                          launch_sched(g, sch, grid),
                                           sl, nsrc ? (const T *)q_dev + m * nsrc : nullptr, trm);
         ++*ka.launches;
     }
@@ -1324,7 +1363,7 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     for (const Op &op : plan.ops) {
         et.op = opi++;
         et.apps = op.kind == 1 ? 1 : 2;
-        kern<<<grid, G::NTHR, Cfg::pair_smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, sch, T(op.a), T(op.b),
+        kern<<<grid, G::NTHR, Cfg::pair_smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a), T(op.b),
                                                    T(op.e2), T(op.c), init, op.kind, et);
         ++*ka.launches;
         if (op.kind == 0) {
@@ -1375,7 +1414,7 @@ static int poly_r_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
     int init = 1;
     for (const Op &op : plan.ops) {
-        kern<<<grid, U::NTHR, smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, sch, T(op.a), T(op.b), T(op.e2), T(op.c),
+        kern<<<grid, U::NTHR, smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a), T(op.b), T(op.e2), T(op.c),
                                           init, op.kind);
         ++*ka.launches;
         if (op.kind == 0) {

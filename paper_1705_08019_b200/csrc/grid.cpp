@@ -216,7 +216,11 @@ static int upload(Grid &G) {
     if (rc) return rc;
     rc = dev_alloc(&G.d_src, sizeof(SrcDev) * PARAEXP_MAX_SOURCES);
     if (rc) return rc;
-    G.device_bytes += 8192 + sizeof(SrcDev) * PARAEXP_MAX_SOURCES;
+    // dynamic-schedule unit counter of the fused kernels (starts at 0; see fused.cu Sched)
+    if ((rc = dev_alloc(&G.d_sched, 256))) return rc;
+    if ((rc = dev_memset_async(G.d_sched, 0, 256, nullptr)) || (rc = dev_sync(nullptr))) return rc;
+    G.sched_base = 0;
+    G.device_bytes += 8192 + 256 + sizeof(SrcDev) * PARAEXP_MAX_SOURCES;
     return PARAEXP_OK;
 }
 
@@ -232,6 +236,9 @@ void grid_free_device(Grid &G) {
     dev_free(G.d_q);
     dev_free(G.d_et);
     G.d_et = nullptr;
+    dev_free(G.d_sched);
+    G.d_sched = nullptr;
+    G.sched_base = 0;
     for (void *q : G.kry) dev_free(q);
     G.kry.clear();
     dev_free(G.d_canon[0]);

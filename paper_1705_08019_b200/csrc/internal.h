@@ -62,6 +62,8 @@ struct Grid {
     void *d_canon[2] = {nullptr, nullptr};   // canonical-layout staging of host-pointer fields
     std::vector<void *> kry;    // Krylov basis vectors (f3), allocated on first use
     void *d_et = nullptr;       // early-termination norms / flags (f2)
+    void *d_sched = nullptr;    // monotone unit counter of the fused kernels' dynamic schedule
+    unsigned long long sched_base = 0;   // host shadow: value of *d_sched before the next launch
     int64_t d_q_cap = 0;
     int64_t device_bytes = 0;
     size_t esize() const { return dtype == PARAEXP_F64 ? 8 : 4; }
