@@ -100,7 +100,10 @@ __device__ __forceinline__ int grab_unit(const Sched &sch, int prev) {
     if (!sch.ctr) return prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
     __shared__ int s_unit;
     __syncthreads();                                      // previous s_unit consumed
-    if (threadIdx.x == 0) s_unit = (int)(atomicAdd(sch.ctr, 1ull) - sch.base);
+    if (threadIdx.x == 0) {
+        const long long d = (long long)(atomicAdd(sch.ctr, 1ull) - sch.base);
+        s_unit = (d < 0 || d > 0x7fffffffLL) ? 0x7fffffff : (int)d;   // never loop on a bad count
+    }
     __syncthreads();
     return s_unit;
 }
@@ -558,7 +561,13 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
     T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
     using G = Geo<T, BX, BY>;
-    if (et.norms && et_skip(et)) return;                  // early termination (f2)
+    if (et.norms && et_skip(et)) {                        // early termination (f2)
+        // a skipped launch still advances the dynamic-schedule counter by units + gridDim,
+        // the amount the host's shadow base assumed
+        if (sch.ctr && blockIdx.x == 0 && threadIdx.x == 0)
+            atomicAdd(sch.ctr, (unsigned long long)sch.units + gridDim.x);
+        return;
+    }
     double dacc = 0.0, yacc = 0.0;                        // ||delta y||^2, ||y||^2 (energy norm)
     using SL = StageL<T, EM, HA, G>;
     constexpr int NR = ONEBAR ? 3 : 2;
