@@ -1133,9 +1133,15 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
     s.ntiles = s.tiles_x * s.tiles_y;
     double best = 1e300;
     int bc = g.nz;
+    // L2 reuse: in the dynamic unit order a y-neighbour tile (tiles_x units later) starts
+    // about tiles_x * chunk / resident planes later; keep that within ~4 planes so its halo
+    // rows are still in L2 (measured at 768^3 fp64: chunk 48-64 beats the unconstrained 154
+    // by 4%)
+    const int cap = std::max(8, (int)(4.0 * resident / std::max(1, s.tiles_x)));
     for (int ch = 1; ch <= g.nz; ++ch) {
         const int nch = (g.nz + ch - 1) / ch;
         if (ch < std::min(g.nz, 8) && nch > 1) continue;
+        if (ch > cap && ch > 8) continue;
         const double units = (double)s.ntiles * nch;
         const double waves = units / resident;
         const double eff_waves = std::ceil(waves);
