@@ -848,8 +848,17 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
     S.root = root;
     const bool has_u0 = e0 != nullptr;
 
-    const double rho = default_rho(G, opts, stream, &S.kernel_launches, &rc);
+    double rho = default_rho(G, opts, stream, &S.kernel_launches, &rc);
     if (rc) return rc;
+    if (comm && world > 1 && !(opts && opts->rho > 0)) {
+        // every rank must build the same plans: the K5 estimate (atomics) can differ in the
+        // last bits between ranks, so all ranks take rank 0's value
+        double *d = (double *)G.d_red;
+        if ((rc = dev_memcpy_h2d_async(d, &rho, sizeof(double), stream))) return rc;
+        if ((rc = nccl_check(g_nccl.Broadcast(d, d, 1, kNcclF64, 0, comm->comm, (cudaStream_t)stream),
+                             "ncclBroadcast(rho)"))) return rc;
+        if ((rc = dev_memcpy_d2h(&rho, d, sizeof(double), stream))) return rc;
+    }
     S.rho = rho;
     // one plan per distinct sub-interval length, plus the dt/2 shift plan
     std::map<int64_t, Plan> plans;
