@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <mutex>
 
 #include "internal.h"
@@ -538,6 +539,264 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
                 const uint32_t L = lcount + p + S;
                 issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
                                           &tm_cH, x0, y0, kb - 1 + p + S);
+            }
+        }
+        lcount += nplanes;
+    }
+    if (TR && tr.energy) {
+        const double sum = block_sum(eacc);
+        if (tid == 0 && sum != 0.0) atomicAdd(tr.energy, sum * tr.dt);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1v: fp32 leapfrog step, two x-adjacent points per thread (float2 shared/global accesses)
+// ---------------------------------------------------------------------------------------
+// fp32 moves half the bytes of fp64 through the same per-point instruction stream, so K1r
+// is issue/latency-bound there.  K1v is K1r with a 64 x 8 tile and each thread owning the
+// pair (i, i+1): own values, j-neighbours and stores are float2; the i-1 neighbour of the
+// left point is one scalar load and the i-1 neighbour of the right point is the left own
+// value (phase A), the i+1 neighbour of the left point is the right own value (phase B).
+// Phase-A points: 32 pair-threads per row for rows y0 .. y0+BY (the +1 halo row) and one
+// single-point thread per row for the +1 halo column x0+64.  Ring rows have an even pitch so
+// float2 accesses stay 8-byte aligned.
+template <int BY>
+struct GeoV {
+    static constexpr int BX = 64;                          // points per tile row
+    static constexpr int OX = 4;                           // TMA x start = x0 - 4 (16 B aligned)
+    static constexpr int WX = 72;                          // box width (>= OX + BX + 1, 16 B multiple)
+    static constexpr int HY = BY + 2;
+    static constexpr int PL = WX * HY;
+    static constexpr int EY = BY + 1;
+    static constexpr int RX = 66;                          // ring row pitch (>= 65, even)
+    static constexpr int RP = RX * EY;
+    static constexpr int MAIN = 32 * EY;                   // pair threads (tile + halo row)
+    static constexpr int NA = MAIN + EY;                   // + halo-column threads
+    static constexpr int NTHR = ((NA + 31) / 32) * 32;
+    static constexpr int NT = 32 * BY;                     // phase-B pair threads
+};
+
+template <int EM, bool HA, int BY, int S, bool TR>
+__global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
+    const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
+    const __grid_constant__ CUtensorMap tm_cH, Dev<float> D, Coef<float, EM, HA> cf, float *__restrict__ out,
+    Sched sch, SrcList src, const float *__restrict__ q, const __grid_constant__ TraceDev tr) {
+    using G = GeoV<BY>;
+    using SL = StageL<float, EM, HA, G>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *stages = reinterpret_cast<float *>(smem_raw);
+    float *ring = stages + S * SL::SZ;                     // [2][3][RP]
+    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(ring + 2 * 3 * G::RP) + 15) & ~uintptr_t(15));
+    const int tid = threadIdx.x;
+    const bool hasA = tid < G::NA;
+    const bool pair = tid < G::MAIN;
+    const int ii = pair ? 2 * (tid % 32) : G::BX;          // local x of the (left) point
+    const int jj = pair ? tid / 32 : tid - G::MAIN;
+    const int rA = jj * G::RX + ii;
+    const int sA = (jj + 1) * G::WX + ii + G::OX;
+    const bool tileA = pair && jj < BY;                    // == phase-B thread of the same pair
+    float bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
+    const float bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
+    if (tid == 0) {
+        for (int s2 = 0; s2 < S; ++s2) mbar_init(&bars[s2], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    auto ld2 = [](const float *p) { return *reinterpret_cast<const float2 *>(p); };
+    auto st2 = [](float *p, float a, float b) { *reinterpret_cast<float2 *>(p) = make_float2(a, b); };
+    uint32_t lcount = 0;
+    double eacc = 0.0;
+    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
+        const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
+        const int x0 = (tile % sch.tiles_x) * G::BX, y0 = (tile / sch.tiles_x) * BY;
+        const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
+        const int nplanes = ke - kb + 2;
+        const int ia = x0 + ii, jA = y0 + jj, ib = ia + 1;
+        const bool rowA = hasA && jA < D.ny;
+        const bool inA = rowA && ia < D.nx, inB = pair && rowA && ib < D.nx;
+        // liveness (reading 5): e_x: j>0 (k>0); e_y: i>0 (k>0); e_z: i>0 && j>0
+        const bool lxa = inA && jA > 0, lya = inA && ia > 0, lza = inA && ia > 0 && jA > 0;
+        const bool lxb = inB && jA > 0, lyb = inB, lzb = inB && jA > 0;
+        const bool wrA = inA && tileA;
+        uint32_t sma = 0, smb = 0, pma = 0, pmb = 0;
+        for (int r = 0; r < src.n; ++r) {
+            if (inA && src.i[r] == ia && src.j[r] == jA) sma |= 1u << r;
+            if (inB && src.i[r] == ib && src.j[r] == jA) smb |= 1u << r;
+        }
+        if (TR)
+            for (int r = 0; r < tr.np; ++r) {
+                if (wrA && tr.i[r] == ia && tr.j[r] == jA) pma |= 1u << r;
+                if (wrA && inB && tr.i[r] == ib && tr.j[r] == jA) pmb |= 1u << r;
+            }
+        float *oA = out + D.idx(wrA ? ia : 0, wrA ? jA : 0, 0);
+        // carried own values of plane k: h (x, y, z) and e' (x, y, z), left (a) and right (b)
+        float hxa = 0.f, hxb = 0.f, hya = 0.f, hyb = 0.f, hza = 0.f, hzb = 0.f;
+        float ea0 = 0.f, eb0 = 0.f, ea1 = 0.f, eb1 = 0.f, ea2 = 0.f, eb2 = 0.f;
+        float g0a = bH0, g1a = bH1, g2a = bH2, g0b = bH0, g1b = bH1, g2b = bH2;
+        if (tid == 0)
+            for (int p = 0; p < min(S, nplanes); ++p) {
+                const uint32_t L = lcount + p;
+                issue_plane<float, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                              &tm_cH, x0, y0, kb - 1 + p);
+            }
+        for (int p = 0; p + 1 < nplanes; ++p) {
+            const int k = kb - 1 + p, kk = k + 1;
+            const uint32_t L0 = lcount + p, L1 = L0 + 1;
+            if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
+            mbar_wait(&bars[L1 % S], (L1 / S) & 1);
+            const float *P0 = stages + (L0 % S) * SL::SZ;
+            const float *P1 = stages + (L1 % S) * SL::SZ;
+            float *R1 = ring + (kk & 1) * 3 * G::RP;
+            const float *R0 = ring + (k & 1) * 3 * G::RP;
+            if (EM == 1 && kk < D.nz) {
+                bE0 = __ldg(cf.tab + kk) * cf.sig;
+                bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
+                bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
+            }
+            if (p == 0 && hasA) {                           // h(kb-1) at the own points
+                if (pair) {
+                    const float2 x = ld2(P0 + 3 * G::PL + sA), y = ld2(P0 + 4 * G::PL + sA);
+                    hxa = x.x; hxb = x.y; hya = y.x; hyb = y.y;
+                } else {
+                    hxa = P0[3 * G::PL + sA];
+                    hya = P0[4 * G::PL + sA];
+                }
+            }
+            float na0 = 0.f, nb0 = 0.f, na1 = 0.f, nb1 = 0.f, na2 = 0.f, nb2 = 0.f;   // e'(k+1)
+            float h1xa = 0.f, h1xb = 0.f, h1ya = 0.f, h1yb = 0.f, h1za = 0.f, h1zb = 0.f;
+            // ---- phase A: e'(k+1) ----
+            if (hasA) {
+                const float *hx = P1 + 3 * G::PL, *hy = P1 + 4 * G::PL, *hz = P1 + 5 * G::PL;
+                const bool vk = kk < D.nz, kp = kk > 0;
+                float wa0 = bE0, wa1 = bE1, wa2 = bE2, wb0 = bE0, wb1 = bE1, wb2 = bE2;
+                if (pair) {
+                    const float2 X = ld2(hx + sA), Y = ld2(hy + sA), Z = ld2(hz + sA);
+                    const float2 Zjm = ld2(hz + sA - G::WX), Xjm = ld2(hx + sA - G::WX);
+                    const float zim = hz[sA - 1], yim = hy[sA - 1];
+                    h1xa = X.x; h1xb = X.y; h1ya = Y.x; h1yb = Y.y; h1za = Z.x; h1zb = Z.y;
+                    const float c0a = ((Z.x - Zjm.x) - Y.x) + hya, c0b = ((Z.y - Zjm.y) - Y.y) + hyb;
+                    const float c1a = ((X.x - hxa) - Z.x) + zim, c1b = ((X.y - hxb) - Z.y) + Z.x;
+                    const float c2a = ((Y.x - yim) - X.x) + Xjm.x, c2b = ((Y.y - Y.x) - X.y) + Xjm.y;
+                    if (EM == 2) {
+                        const float2 A0 = ld2(P1 + SL::ST + sA), A1 = ld2(P1 + SL::ST + G::PL + sA);
+                        const float2 A2 = ld2(P1 + SL::ST + 2 * G::PL + sA);
+                        wa0 = A0.x * cf.sig; wb0 = A0.y * cf.sig;
+                        wa1 = A1.x * cf.sig; wb1 = A1.y * cf.sig;
+                        wa2 = A2.x * cf.sig; wb2 = A2.y * cf.sig;
+                    }
+                    const float2 E0 = ld2(P1 + sA), E1 = ld2(P1 + G::PL + sA), E2 = ld2(P1 + 2 * G::PL + sA);
+                    na0 = (lxa && vk && kp) ? E0.x + wa0 * c0a : 0.f;
+                    nb0 = (lxb && vk && kp) ? E0.y + wb0 * c0b : 0.f;
+                    na1 = (lya && vk && kp) ? E1.x + wa1 * c1a : 0.f;
+                    nb1 = (lyb && vk && kp) ? E1.y + wb1 * c1b : 0.f;
+                    na2 = (lza && vk) ? E2.x + wa2 * c2a : 0.f;
+                    nb2 = (lzb && vk) ? E2.y + wb2 * c2b : 0.f;
+                } else {
+                    const float X = hx[sA], Y = hy[sA], Z = hz[sA];
+                    h1xa = X; h1ya = Y; h1za = Z;
+                    const float c0 = ((Z - hz[sA - G::WX]) - Y) + hya;
+                    const float c1 = ((X - hxa) - Z) + hz[sA - 1];
+                    const float c2 = ((Y - hy[sA - 1]) - X) + hx[sA - G::WX];
+                    if (EM == 2) {
+                        wa0 = P1[SL::ST + sA] * cf.sig;
+                        wa1 = P1[SL::ST + G::PL + sA] * cf.sig;
+                        wa2 = P1[SL::ST + 2 * G::PL + sA] * cf.sig;
+                    }
+                    na0 = (lxa && vk && kp) ? P1[sA] + wa0 * c0 : 0.f;
+                    na1 = (lya && vk && kp) ? P1[G::PL + sA] + wa1 * c1 : 0.f;
+                    na2 = (lza && vk) ? P1[2 * G::PL + sA] + wa2 * c2 : 0.f;
+                }
+                if ((sma | smb) && vk)
+                    for (int r = 0; r < src.n; ++r) {
+                        if (src.k[r] != kk) continue;
+                        const int sc = src.c[r];
+                        const float qv = q[r];
+                        if ((sma >> r) & 1u) {
+                            if (sc == 0) na0 -= qv;
+                            if (sc == 1) na1 -= qv;
+                            if (sc == 2) na2 -= qv;
+                        }
+                        if ((smb >> r) & 1u) {
+                            if (sc == 0) nb0 -= qv;
+                            if (sc == 1) nb1 -= qv;
+                            if (sc == 2) nb2 -= qv;
+                        }
+                    }
+                if (pair) {
+                    st2(R1 + rA, na0, nb0);
+                    st2(R1 + G::RP + rA, na1, nb1);
+                    st2(R1 + 2 * G::RP + rA, na2, nb2);
+                } else {
+                    R1[rA] = na0;
+                    R1[G::RP + rA] = na1;
+                    R1[2 * G::RP + rA] = na2;
+                }
+                if (wrA && vk && kk >= kb && kk < ke) {
+                    float *o = oA + (int64_t)kk * D.plane;
+                    st2(o, na0, nb0);                     // b beyond nx lands in the zero x-padding
+                    st2(o + D.cs, na1, nb1);
+                    st2(o + 2 * D.cs, na2, nb2);
+                    if (TR) {
+                        if (wa0 != 0.f) eacc += (double)na0 * na0 / (double)wa0;
+                        if (wa1 != 0.f) eacc += (double)na1 * na1 / (double)wa1;
+                        if (wa2 != 0.f) eacc += (double)na2 * na2 / (double)wa2;
+                        if (inB) {
+                            if (wb0 != 0.f) eacc += (double)nb0 * nb0 / (double)wb0;
+                            if (wb1 != 0.f) eacc += (double)nb1 * nb1 / (double)wb1;
+                            if (wb2 != 0.f) eacc += (double)nb2 * nb2 / (double)wb2;
+                        }
+                        if (pma | pmb)
+                            for (int r = 0; r < tr.np; ++r) {
+                                if (tr.k[r] != kk) continue;
+                                const int c = tr.c[r];
+                                if ((pma >> r) & 1u) tr.probe[r] = (double)(c == 0 ? na0 : (c == 1 ? na1 : na2));
+                                if ((pmb >> r) & 1u) tr.probe[r] = (double)(c == 0 ? nb0 : (c == 1 ? nb1 : nb2));
+                            }
+                    }
+                }
+            }
+            __syncthreads();
+            // ---- phase B: h'(k) on the tile pair ----
+            if (k >= kb && wrA) {
+                const float2 Zj = ld2(R0 + 2 * G::RP + rA + G::RX), Xj = ld2(R0 + rA + G::RX);
+                const float zip = R0[2 * G::RP + rA + 2], yip = R0[G::RP + rA + 2];
+                // point a: i+1 neighbours are the own right values; point b: from the ring
+                const float c0a = ((ea1 + Zj.x) - na1) - ea2, c0b = ((eb1 + Zj.y) - nb1) - eb2;
+                const float c1a = ((ea2 + na0) - eb2) - ea0, c1b = ((eb2 + nb0) - zip) - eb0;
+                const float c2a = ((ea0 + eb1) - Xj.x) - ea1, c2b = ((eb0 + yip) - Xj.y) - eb1;
+                if (HA) {
+                    const int ch = SL::ST + SL::CE;
+                    const float2 A0 = ld2(P0 + ch + sA), A1 = ld2(P0 + ch + G::PL + sA), A2 = ld2(P0 + ch + 2 * G::PL + sA);
+                    g0a = A0.x * cf.sig; g0b = A0.y * cf.sig;
+                    g1a = A1.x * cf.sig; g1b = A1.y * cf.sig;
+                    g2a = A2.x * cf.sig; g2b = A2.y * cf.sig;
+                }
+                const bool lxA2 = ia > 0, lyA2 = jA > 0, kp = k > 0;
+                const float nxa = lxA2 ? hxa - g0a * c0a : hxa, nxb = hxb - g0b * c0b;
+                const float nya = lyA2 ? hya - g1a * c1a : hya, nyb = lyA2 ? hyb - g1b * c1b : hyb;
+                const float nza = kp ? hza - g2a * c2a : hza, nzb = kp ? hzb - g2b * c2b : hzb;
+                float *o = oA + (int64_t)k * D.plane + 3 * D.cs;
+                st2(o, nxa, inB ? nxb : 0.f);
+                st2(o + D.cs, nya, inB ? nyb : 0.f);
+                st2(o + 2 * D.cs, nza, inB ? nzb : 0.f);
+                if (TR) {
+                    if (lxA2 && g0a != 0.f) eacc += (double)hxa * nxa / (double)g0a;
+                    if (lyA2 && g1a != 0.f) eacc += (double)hya * nya / (double)g1a;
+                    if (kp && g2a != 0.f) eacc += (double)hza * nza / (double)g2a;
+                    if (inB) {
+                        if (g0b != 0.f) eacc += (double)hxb * nxb / (double)g0b;
+                        if (lyA2 && g1b != 0.f) eacc += (double)hyb * nyb / (double)g1b;
+                        if (kp && g2b != 0.f) eacc += (double)hzb * nzb / (double)g2b;
+                    }
+                }
+            }
+            hxa = h1xa; hxb = h1xb; hya = h1ya; hyb = h1yb; hza = h1za; hzb = h1zb;
+            ea0 = na0; eb0 = nb0; ea1 = na1; eb1 = nb1; ea2 = na2; eb2 = nb2;
+            __syncthreads();
+            if (tid == 0 && p + S < nplanes) {
+                const uint32_t L = lcount + p + S;
+                issue_plane<float, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                              &tm_cH, x0, y0, kb - 1 + p + S);
             }
         }
         lcount += nplanes;
@@ -1318,6 +1577,63 @@ static int leapfrog_r_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int
     return check_cuda("leapfrog_r");
 }
 
+// K1v launcher (fp32, 64 x 8 tiles, two points per thread)
+template <int EM, bool HA, int S, bool TR>
+static int leapfrog_v_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int nsrc, const void *q_dev,
+                        const std::vector<SrcDev> &hsrc, const TraceDev *tr) {
+    constexpr int BY = 8;
+    using G = GeoV<BY>;
+    constexpr size_t smem = (size_t)(S * StageL<float, EM, HA, G>::SZ + 2 * 3 * G::RP) * sizeof(float) + 8 * S + 16;
+    const Grid &g = *ka.g;
+    auto kern = leapfrog_v_kernel<EM, HA, BY, S, TR>;
+    static const int per_sm = resident_per_sm(kern, G::NTHR, smem);
+    if (per_sm < 1) return fail(PARAEXP_ECUDA, "leapfrog_v kernel does not fit on an SM");
+    const Sched sch = make_sched(g, G::BX, BY, per_sm * num_sms());
+    const int grid = std::min(sch.units, per_sm * num_sms());
+    auto D = make_dev<float>(g);
+    auto cf = make_coef<float, EM, HA>(g, 1.0);
+    CUtensorMap tmE, tmH, tmA, tmB;
+    int rc;
+    if (EM == 2 && (rc = make_map<float>(&tmE, g, g.d_cE_arr, 3, G::WX, G::HY))) return rc;
+    if (HA && (rc = make_map<float>(&tmH, g, g.d_cH_arr, 3, G::WX, G::HY))) return rc;
+    if ((rc = make_map<float>(&tmA, g, bufs[0], 6, G::WX, G::HY))) return rc;
+    if ((rc = make_map<float>(&tmB, g, bufs[1], 6, G::WX, G::HY))) return rc;
+    SrcList sl;
+    sl.n = nsrc;
+    for (int r = 0; r < nsrc && r < 16; ++r) {
+        sl.c[r] = hsrc[r].comp;
+        sl.i[r] = hsrc[r].i;
+        sl.j[r] = hsrc[r].j;
+        sl.k[r] = hsrc[r].k;
+    }
+    cudaStream_t s = (cudaStream_t)ka.stream;
+    TraceDev trm;
+    if (TR) trm = *tr;
+    for (int64_t m = 0; m < nsteps; ++m) {
+        const bool even = (m % 2) == 0;
+        if (TR) {
+            trm.energy = tr->energy ? tr->energy + m : nullptr;
+            trm.probe = tr->probe ? tr->probe + m * tr->np : nullptr;
+            if (!trm.probe) trm.np = 0;
+        }
+        kern<<<grid, G::NTHR, smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf, (float *)(even ? bufs[1] : bufs[0]),
+                                          launch_sched(g, sch, grid), sl,
+                                          nsrc ? (const float *)q_dev + m * nsrc : nullptr, trm);
+        ++*ka.launches;
+    }
+    if (nsteps % 2) std::swap(bufs[0], bufs[1]);
+    return check_cuda("leapfrog_v");
+}
+
+static bool lf_vec_enabled() {   // K1v for fp32 (default); PARAEXP_LF_VEC=0 selects K1r
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PARAEXP_LF_VEC");
+        v = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // kernel generation: r (row-aligned, register-carried; default) or the first fused kernels
 // (PARAEXP_KERNEL_V1=1)
 static bool kernels_v1() {
@@ -1339,6 +1655,12 @@ int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const 
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
         if (!kernels_v1()) {
+            if constexpr (std::is_same<T, float>::value) {
+                if (lf_vec_enabled()) {
+                    if (trace) return leapfrog_v_V<EM, HA, 3, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
+                    return leapfrog_v_V<EM, HA, 3, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
+                }
+            }
             if (trace) return leapfrog_r_V<T, EM, HA, 3, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
             return leapfrog_r_V<T, EM, HA, 3, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
         }
