@@ -591,11 +591,43 @@ def expmv_krylov(g: Grid, l: int, s: int, tau: float, e, h, dtype: Optional[str]
     return b[:n3].copy(), b[n3:].copy(), apps
 
 
+def expmv_horner(g: Grid, plan: Plan, e, h, dtype: str = "f64"):
+    """The same polynomial as expmv_pairs in nested (Horner) order (DESIGN reading 33):
+    with the pair blocks (a_k + b_k X) and the factors (X^2 + e2_k) of pair_constants,
+        p(X) b = sum_k (a_k + b_k X) prod_{j<k} (X^2 + e2_j) b  +  c prod_{j<K} (X^2 + e2_j) b,
+    evaluated from the innermost block out:
+        r = b, s = c;  for k = K-1 .. 0:  r <- (a_k b + b_k (X b)) + s (X (X r) + e2_k r),  s = 1
+    ('half', m = 1: r = a b + b_k X b).  Arithmetic fp64, constants rounded to `dtype`."""
+    X = ScaledOp(g, (plan.tau / plan.s) / (plan.gamma * g.dt), dtype)
+    consts = pair_constants(plan, dtype)
+    be = np.array(e, dtype=np.float64, copy=True)
+    bh = np.array(h, dtype=np.float64, copy=True)
+    for _ in range(plan.s):
+        xbe, xbh = X(be, bh)
+        re_, rh_ = be, bh
+        scale = consts[-1][4]
+        for k in range(len(consts) - 1, -1, -1):
+            kind, a, bk, e2, _c = consts[k]
+            ne = a * be + bk * xbe
+            nh = a * bh + bk * xbh
+            if kind != "half":
+                ue, uh = X(re_, rh_)
+                x2e, x2h = X(ue, uh)
+                ne = ne + scale * (x2e + e2 * re_)
+                nh = nh + scale * (x2h + e2 * rh_)
+            re_, rh_ = ne, nh
+            scale = 1.0
+        be, bh = re_, rh_
+    return be, bh
+
+
 def expmv(g: Grid, plan: Plan, e, h, mode: str = "pairs", dtype: Optional[str] = None):
     if plan.tau == 0.0:
         return np.array(e, float), np.array(h, float)
     if mode == "complex":
         return expmv_newton_complex(g, plan, e, h)
+    if mode == "horner":
+        return expmv_horner(g, plan, e, h, dtype or g.dtype)
     return expmv_pairs(g, plan, e, h, dtype or g.dtype)
 
 

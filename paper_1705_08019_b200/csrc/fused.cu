@@ -1079,6 +1079,198 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
 }
 
 // ---------------------------------------------------------------------------------------
+// K2H: one nested (Horner) step of the pair-block polynomial (DESIGN reading 33)
+// ---------------------------------------------------------------------------------------
+//   r' = (a b + beta X b) + s (X (X r) + e2 r)          (s = c for the innermost step, else 1)
+// Inputs b (the substep's start vector) and r (the running nest) are both TMA-staged with the
+// same 1-cell halo box; X r -> X(X r) runs as in K2 (u_e(k+1), u_h(k) rings, then X u on the
+// tile) and X b is evaluated at the own point straight from the b stage.  HBM per step: read
+// b, r, write r' = 18 values per two A-applications (K2: read w, y, write w', y = 24), paid
+// for with one extra stencil evaluation (X b) per step.  Scalar / z-table materials only.
+template <typename T, int BX, int BY>
+struct StageH {
+    static constexpr int A = 128 / (int)sizeof(T);
+    static constexpr int ST = ((6 * Geo<T, BX, BY>::PL + A - 1) / A) * A;   // one 6-component box
+    static constexpr int SZ = 2 * ST;                                        // r box | b box
+};
+
+template <typename T, int EM, int BX, int BY, int S>
+__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 2) horner_fused_kernel(
+    const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_b, Dev<T> D,
+    Coef<T, EM, false> cf, T *__restrict__ rout, Sched sch, T a, T beta, T e2, T sc, int mode) {
+    using G = Geo<T, BX, BY>;
+    using SH = StageH<T, BX, BY>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T *stages = reinterpret_cast<T *>(smem_raw);
+    T *UE = stages + S * SH::SZ;                         // [2][3][RP]
+    T *UH = UE + 2 * 3 * G::RP;                          // [2][3][RP]
+    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(UH + 2 * 3 * G::RP) + 15) & ~uintptr_t(15));
+    const int tid = threadIdx.x;
+    const bool hasA = tid < G::RP;
+    constexpr int MAIN = BX * G::EY;
+    const int ii = tid < MAIN ? tid % BX : BX, jj = tid < MAIN ? tid / BX : tid - MAIN;
+    const int rA = jj * G::EX + ii;
+    const int sE = (jj + 1) * G::WX + ii + G::OX;
+    const int sH = jj * G::WX + ii - 1 + G::OX;
+    const bool hasB = tid < G::NT;
+    const int tx = tid % BX, ty = tid / BX;
+    const int re = ty * G::EX + tx;
+    const int rh = (ty + 1) * G::EX + (tx + 1);
+    const int sB = (ty + 1) * G::WX + tx + G::OX;
+    T bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
+    const T bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
+    constexpr uint32_t BYTES = (uint32_t)(2 * 6 * G::PL * sizeof(T));
+    auto issue = [&](int slot, uint32_t L, int x0, int y0, int kz) {
+        T *dst = stages + slot * SH::SZ;
+        mbar_expect_tx(&bars[slot], BYTES);
+        tma_load_4d(dst, &tm_r, &bars[slot], x0 - G::OX, y0 - 1, kz, 0);
+        tma_load_4d(dst + SH::ST, &tm_b, &bars[slot], x0 - G::OX, y0 - 1, kz, 0);
+        (void)L;
+    };
+    if (tid == 0) {
+        for (int s2 = 0; s2 < S; ++s2) mbar_init(&bars[s2], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    uint32_t lcount = 0;
+    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
+        const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
+        const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
+        const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
+        const int nplanes = ke - kb + 2;
+        const int iE = x0 + ii, jE = y0 + jj;
+        const bool inE = hasA && iE < D.nx && jE < D.ny;
+        const bool lxE = inE && jE > 0, lyE = inE && iE > 0, lzE = inE && iE > 0 && jE > 0;
+        const int iH = iE - 1, jH = jE - 1;
+        const bool inH = hasA && iH >= 0 && jH >= 0 && iH < D.nx && jH < D.ny;
+        const bool lxH = inH && iH > 0, lyH = inH && jH > 0;
+        const int iB = x0 + tx, jB = y0 + ty;
+        const bool inB = hasB && iB < D.nx && jB < D.ny;
+        const bool lxBe = jB > 0, lyBe = iB > 0, lzBe = iB > 0 && jB > 0;
+        const bool lxBh = iB > 0, lyBh = jB > 0;
+        const int64_t gB = D.idx(inB ? iB : 0, inB ? jB : 0, 0);
+        T bhxk = T(0), bhyk = T(0);                       // b_h(k-1) at the own point (carried)
+        if (tid == 0)
+            for (int p = 0; p < min(S, nplanes); ++p) {
+                const uint32_t L = lcount + p;
+                issue((int)(L % S), L, x0, y0, kb - 1 + p);
+            }
+        for (int p = 0; p + 1 < nplanes; ++p) {
+            const int k = kb - 1 + p, kk = k + 1;
+            const uint32_t L0 = lcount + p, L1 = L0 + 1;
+            const bool doB = k >= kb && inB;
+            if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
+            mbar_wait(&bars[L1 % S], (L1 / S) & 1);
+            const T *P0 = stages + (L0 % S) * SH::SZ;    // r plane k
+            const T *P1 = stages + (L1 % S) * SH::SZ;    // r plane k+1
+            const T *B0 = P0 + SH::ST, *B1 = P1 + SH::ST; // b planes k, k+1
+            T *UE1 = UE + (kk & 1) * 3 * G::RP;
+            T *UH0 = UH + (k & 1) * 3 * G::RP;
+            T bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;
+            if (EM == 1) {
+                if (kk < D.nz) {
+                    bE0 = __ldg(cf.tab + kk) * cf.sig;
+                    bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
+                    bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
+                }
+                if (k >= 0) {
+                    bEk0 = __ldg(cf.tab + k) * cf.sig;
+                    bEk1 = __ldg(cf.tab + D.nz + k) * cf.sig;
+                    bEk2 = __ldg(cf.tab + 2 * D.nz + k) * cf.sig;
+                }
+            }
+            if (mode != 1 && hasA) {
+                {   // u_e(k+1) = bE .* C^T r_h
+                    T c0, c1, c2;
+                    curlT_stage<T, G>(P1, P0, sE, c0, c1, c2);
+                    const bool vk = kk < D.nz, kp = kk > 0;
+                    UE1[rA] = (lxE && vk && kp) ? bE0 * c0 : T(0);
+                    UE1[G::RP + rA] = (lyE && vk && kp) ? bE1 * c1 : T(0);
+                    UE1[2 * G::RP + rA] = (lzE && vk) ? bE2 * c2 : T(0);
+                }
+                {   // u_h(k) = -bH .* C r_e
+                    T c0, c1, c2;
+                    curl_stage<T, G>(P0, P1, sH, c0, c1, c2);
+                    const bool vk = k >= 0 && k < D.nz;
+                    UH0[rA] = (lxH && vk) ? -(bH0 * c0) : T(0);
+                    UH0[G::RP + rA] = (lyH && vk) ? -(bH1 * c1) : T(0);
+                    UH0[2 * G::RP + rA] = (inH && vk && k > 0) ? -(bH2 * c2) : T(0);
+                }
+            }
+            __syncthreads();
+            if (p == 0 && inB) {                          // b_h(kb-1) own for the first X b
+                bhxk = B0[3 * G::PL + sB];
+                bhyk = B0[4 * G::PL + sB];
+            }
+            if (doB) {
+                const T *UE0 = UE + (k & 1) * 3 * G::RP;
+                const T *UHm = UH + ((k - 1) & 1) * 3 * G::RP;
+                const bool kp = k > 0;
+                // X b at the own point (plane k)
+                T xb[6];
+                {
+                    const T *bhx = B0 + 3 * G::PL, *bhy = B0 + 4 * G::PL, *bhz = B0 + 5 * G::PL;
+                    const T hx0 = bhx[sB], hy0 = bhy[sB], hz0 = bhz[sB];
+                    const T d0 = ((hz0 - bhz[sB - G::WX]) - hy0) + bhyk;
+                    const T d1 = ((hx0 - bhxk) - hz0) + bhz[sB - 1];
+                    const T d2 = ((hy0 - bhy[sB - 1]) - hx0) + bhx[sB - G::WX];
+                    xb[0] = (lxBe && kp) ? bEk0 * d0 : T(0);
+                    xb[1] = (lyBe && kp) ? bEk1 * d1 : T(0);
+                    xb[2] = lzBe ? bEk2 * d2 : T(0);
+                    bhxk = hx0;
+                    bhyk = hy0;
+                    const T *bex = B0, *bey = B0 + G::PL, *bez = B0 + 2 * G::PL;
+                    const T ex0 = bex[sB], ey0 = bey[sB], ez0 = bez[sB];
+                    const T c0 = ((ey0 + bez[sB + G::WX]) - B1[G::PL + sB]) - ez0;
+                    const T c1 = ((ez0 + B1[sB]) - bez[sB + 1]) - ex0;
+                    const T c2 = ((ex0 + bey[sB + 1]) - bex[sB + G::WX]) - ey0;
+                    xb[3] = lxBh ? -(bH0 * c0) : T(0);
+                    xb[4] = lyBh ? -(bH1 * c1) : T(0);
+                    xb[5] = kp ? -(bH2 * c2) : T(0);
+                }
+                T x2[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
+                if (mode != 1) {                          // X u = X (X r) at the own point
+                    const T ux0 = UE0[re], uy0 = UE0[G::RP + re], uz0 = UE0[2 * G::RP + re];
+                    const T hx0 = UH0[rh], hy0 = UH0[G::RP + rh], hz0 = UH0[2 * G::RP + rh];
+                    const T uz_jp = UE0[2 * G::RP + re + G::EX], ux_jp = UE0[re + G::EX];
+                    const T uz_ip = UE0[2 * G::RP + re + 1], uy_ip = UE0[G::RP + re + 1];
+                    const T ux_kp = UE1[re], uy_kp = UE1[G::RP + re];
+                    const T c0 = ((uy0 + uz_jp) - uy_kp) - uz0;
+                    const T c1 = ((uz0 + ux_kp) - uz_ip) - ux0;
+                    const T c2 = ((ux0 + uy_ip) - ux_jp) - uy0;
+                    const T hz_jm = UH0[2 * G::RP + rh - G::EX], hx_jm = UH0[rh - G::EX];
+                    const T hz_im = UH0[2 * G::RP + rh - 1], hy_im = UH0[G::RP + rh - 1];
+                    const T hy_km = UHm[G::RP + rh], hx_km = UHm[rh];
+                    const T d0 = ((hz0 - hz_jm) - hy0) + hy_km;
+                    const T d1 = ((hx0 - hx_km) - hz0) + hz_im;
+                    const T d2 = ((hy0 - hy_im) - hx0) + hx_jm;
+                    x2[0] = (lxBe && kp) ? bEk0 * d0 : T(0);
+                    x2[1] = (lyBe && kp) ? bEk1 * d1 : T(0);
+                    x2[2] = lzBe ? bEk2 * d2 : T(0);
+                    x2[3] = lxBh ? -(bH0 * c0) : T(0);
+                    x2[4] = lyBh ? -(bH1 * c1) : T(0);
+                    x2[5] = kp ? -(bH2 * c2) : T(0);
+                }
+                T *ro = rout + gB + (int64_t)k * D.plane;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) {
+                    const T bv = B0[c * G::PL + sB];
+                    T v = a * bv + beta * xb[c];
+                    if (mode != 1) v = v + sc * (x2[c] + e2 * P0[c * G::PL + sB]);
+                    ro[c * D.cs] = v;
+                }
+            }
+            __syncthreads();
+            if (tid == 0 && p + S < nplanes) {
+                const uint32_t L = lcount + p + S;
+                issue((int)(L % S), L, x0, y0, kb - 1 + p + S);
+            }
+        }
+        lcount += nplanes;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // K2v: fp32 Newton pair, two x-adjacent points per thread (float2), own values in registers
 // ---------------------------------------------------------------------------------------
 // Tile 64 x 8.  Phase A: thread (pi, jj < BY) computes u_e(k+1) AND u_h(k) on the pair
@@ -2104,6 +2296,59 @@ static int poly_r_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     return check_cuda("poly_r");
 }
 
+// K2H launcher: the ops from the innermost (last) to the outermost; bufs[0] = b is read by
+// every step, the nest ping-pongs between bufs[1] and bufs[2]; on return bufs[0] = result.
+template <typename T, int EM, int S>
+static int poly_horner_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
+    constexpr int BX = 32, BY = 8;
+    using G = Geo<T, BX, BY>;
+    using SH = StageH<T, BX, BY>;
+    constexpr size_t smem = (size_t)(S * SH::SZ + 2 * 2 * 3 * G::RP) * sizeof(T) + 8 * S + 16;
+    const Grid &g = *ka.g;
+    auto kern = horner_fused_kernel<T, EM, BX, BY, S>;
+    static const int per_sm = resident_per_sm(kern, G::NTHR, smem);
+    if (per_sm < 1) return fail(PARAEXP_ECUDA, "horner kernel does not fit on an SM");
+    const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
+    const int grid = std::min(sch.units, per_sm * num_sms());
+    auto D = make_dev<T>(g);
+    auto cf = make_coef<T, EM, false>(g, plan.sigma);
+    cudaStream_t s = (cudaStream_t)ka.stream;
+    void *bb = bufs[0], *r1 = bufs[1], *r2 = bufs[2];
+    CUtensorMap tmB, tm1, tm2;
+    int rc;
+    if ((rc = make_map<T>(&tmB, g, bb, 6, G::WX, G::HY))) return rc;
+    if ((rc = make_map<T>(&tm1, g, r1, 6, G::WX, G::HY))) return rc;
+    if ((rc = make_map<T>(&tm2, g, r2, 6, G::WX, G::HY))) return rc;
+    const int K = (int)plan.ops.size();
+    const CUtensorMap *in = &tmB;
+    void *out = r1;
+    for (int q = K - 1; q >= 0; --q) {
+        const Op &op = plan.ops[q];
+        const T sc = (T)(q == K - 1 ? op.c : 1.0);
+        const int mode = op.kind == 1 ? 1 : 0;
+        kern<<<grid, G::NTHR, smem, s>>>(*in, tmB, D, cf, (T *)out, launch_sched(g, sch, grid), T(op.a), T(op.b),
+                                          T(op.e2), sc, mode);
+        ++*ka.launches;
+        in = out == r1 ? &tm1 : &tm2;
+        out = out == r1 ? r2 : r1;
+    }
+    void *res = out == r1 ? r2 : r1;                     // the last written buffer
+    bufs[0] = res;
+    bufs[1] = bb;
+    bufs[2] = res == r1 ? r2 : r1;
+    return check_cuda("poly horner");
+}
+
+static int horner_stages() {   // 0 = K2H off (PARAEXP_HORNER=0), else the stage count
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PARAEXP_HORNER");
+        v = e ? atoi(e) : 2;
+        if (v != 0 && v != 2 && v != 3) v = 2;
+    }
+    return v;
+}
+
 // K2v launcher (fp32, 64 x 8 tiles, two points per thread; same buffer protocol as K2)
 template <int EM, bool HA, int S>
 static int poly_v_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
@@ -2156,6 +2401,12 @@ int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
+        if constexpr (EM != 2 && !HA && std::is_same<T, double>::value) {
+            // K2H (nested evaluation, 18 instead of 24 values per pair) unless early
+            // termination needs the forward sum
+            if (!ka.et && horner_stages() == 2) return poly_horner_V<T, EM, 2>(ka, plan, bufs);
+            if (!ka.et && horner_stages() == 3) return poly_horner_V<T, EM, 3>(ka, plan, bufs);
+        }
         if constexpr (std::is_same<T, float>::value) {
             if (lf_vec_enabled()) return poly_v_V<EM, HA, 3>(ka, plan, bufs);   // K2v (fp32)
         }

@@ -213,3 +213,20 @@ def test_early_termination_oracle():
     te, th, apps = fit.expmv_pairs_et(g, fit.make_plan("leja", 8, 3, 10 * g.dt, rho), e, h, 1e-15)
     pe_, ph_ = fit.expmv(g, fit.make_plan("leja", 8, 3, 10 * g.dt, rho), e, h)
     assert apps == 24 and np.array_equal(te, pe_) and np.array_equal(th, ph_)
+
+
+@pytest.mark.parametrize("method,m,s", [("leja", 40, 3), ("leja", 1, 5), ("leja", 2, 4), ("leja", 64, 1),
+                                         ("taylor", 16, 6), ("leja", 6, 2)])
+def test_horner_equals_forward_and_complex(method, m, s):
+    """Reading 33: the nested (Horner) evaluation of the real pair-block polynomial equals the
+    forward pair recurrence and the plain complex Newton form (fp64, 1e-12)."""
+    g = fit.Grid(5, 4, 4, d0=1e-3, eps_r=np.random.default_rng(2).uniform(1, 4, 80), dt_frac=0.95)
+    e, h = _state(g, 8)
+    tau = (30 if method == "leja" else 6) * g.dt
+    plan = fit.make_plan(method, m, s, tau, g.rho_cfl)
+    he, hh = fit.expmv(g, plan, e, h, mode="horner")
+    fe, fh = fit.expmv(g, plan, e, h, mode="pairs")
+    ce, ch = fit.expmv(g, plan, e, h, mode="complex")
+    ref = np.concatenate([ce, ch])
+    for got in (np.concatenate([he, hh]), np.concatenate([fe, fh])):
+        assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
