@@ -2339,12 +2339,15 @@ static int poly_horner_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
     return check_cuda("poly horner");
 }
 
-static int horner_stages() {   // 0 = K2H off (PARAEXP_HORNER=0), else the stage count
+// K2H is opt-in (PARAEXP_HORNER=2|3 stages): on B200 fp64 256^3 it measured 304 (2 stages,
+// 2 CTAs/SM) / 298 (3 stages, 1 CTA/SM) vs K2's 284 us per A-application -- the 25% fewer HBM
+// bytes do not pay for the extra X b stencil and the lower occupancy
+static int horner_stages() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("PARAEXP_HORNER");
-        v = e ? atoi(e) : 2;
-        if (v != 0 && v != 2 && v != 3) v = 2;
+        v = e ? atoi(e) : 0;
+        if (v != 0 && v != 2 && v != 3) v = 0;
     }
     return v;
 }
