@@ -446,7 +446,6 @@ static int run_plan(const KernelArgs &ka, const Plan &plan, void *bufs[4], parae
         // A-applications they actually perform (reading 18)
         Grid &G = *const_cast<Grid *>(ka.g);
         const size_t nops = plan.ops.size();
-        const size_t bytes = (2 * nops) * sizeof(double) + 2 * sizeof(int) + 16;
         if (!G.d_et) {
             int rc = dev_alloc(&G.d_et, (2 * (PARAEXP_MAX_DEGREE + 2)) * sizeof(double) + 64);
             if (rc) return rc;
@@ -465,7 +464,6 @@ static int run_plan(const KernelArgs &ka, const Plan &plan, void *bufs[4], parae
             rc = k_poly_substep(kb, plan, bufs);
         }
         if (rc) return rc;
-        (void)bytes;
         if (id >= 0) ev->close(id);
         int count = 0;
         if ((rc = dev_memcpy_d2h(&count, et.count, sizeof(int), ka.stream))) return rc;
