@@ -39,6 +39,23 @@ static int ensure_ws(Grid &G, int n) {
     return PARAEXP_OK;
 }
 
+// ---- dynamic-schedule counter check ---------------------------------------------------------
+// The fused kernels take their units from a grid-owned monotone counter whose expected value
+// the host tracks (fused.cu Sched).  At points where a call synchronises anyway, verify it;
+// on a mismatch (an aborted launch) reset both and report the error instead of letting later
+// launches work on a shifted unit sequence.
+static int sched_check(Grid &G, void *stream) {
+    if (!G.d_sched) return PARAEXP_OK;
+    unsigned long long v = 0;
+    int rc = dev_memcpy_d2h(&v, G.d_sched, sizeof(v), stream);
+    if (rc) return rc;
+    if (v == G.sched_base) return PARAEXP_OK;
+    dev_memset_async(G.d_sched, 0, sizeof(v), stream);
+    dev_sync(stream);
+    G.sched_base = 0;
+    return fail(PARAEXP_ECUDA, "fused-kernel schedule counter out of step (aborted launch?); reset");
+}
+
 // ---- host or device field pointers ---------------------------------------------------------
 // Field arguments may be device pointers (stream-ordered, no copy) or host pointers (pinned or
 // pageable): host fields are staged through canonical-layout device buffers with
@@ -701,6 +718,7 @@ static int leapfrog_impl(paraexp_grid *grid, const paraexp_source *src, int32_t 
         ev.sum(ms);
         S.ms_total = ms[4];
         S.ms_leapfrog_kernels = ms[5];
+        if ((rc = sched_check(G, stream))) return rc;
     }
     return PARAEXP_OK;
 }
@@ -757,6 +775,7 @@ int paraexp_expmv(paraexp_grid *grid, double tau, const paraexp_expmv_opts *opts
     int flag = 0;
     if ((rc = k_check_finite(ka, bufs[0], &flag))) return rc;
     if (flag) return fail(PARAEXP_EOVERFLOW, "exp(tA)v produced non-finite values (use larger s)");
+    if ((rc = sched_check(G, stream))) return rc;
     double ms[7] = {0, 0, 0, 0, 0, 0, 0};
     ev.sum(ms);
     S.ms_total = ms[4];
@@ -1037,6 +1056,7 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
     S.cell_updates = (S.leapfrog_steps + S.a_applications) * cells;
     std::vector<int> flags(p + 2, 0);
     if ((rc = dev_memcpy_d2h(flags.data(), dflag, sizeof(int) * (p + 2), stream))) return rc;
+    if ((rc = sched_check(G, stream))) return rc;
     double ms[7] = {0, 0, 0, 0, 0, 0, 0};
     ev.sum(ms);
     S.ms_particular = ms[0];
