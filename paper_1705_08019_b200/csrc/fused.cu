@@ -1281,13 +1281,35 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 2) horner_fused_kernel(
 // y0-1..y0+BY-1).  Rings (column c stored at c - x0 + 2, even pitch): u_e 2 planes (rows
 // y0..y0+BY), u_h 1 plane (rows y0-1..y0+BY-1, stored at row + 1).  Phase B reads only the
 // j+1 / i+2 neighbours of u_e(k) and the j-1 / i-1 neighbours of u_h(k).
-template <int EM, bool HA, int BY, int S>
-__global__ void __launch_bounds__(GeoV<BY>::NTHR, 2) pair_v_kernel(
+// geometry of the two-points-per-thread pair kernel for T = float / double (64 x BY tiles)
+template <typename T, int BY>
+struct GeoW {
+    static constexpr int BX = 64;
+    static constexpr int VEC = 16 / (int)sizeof(T);
+    static constexpr int OX = VEC;                          // TMA x start x0 - OX (16 B aligned)
+    static constexpr int WX = ((OX + BX + 1 + VEC - 1) / VEC) * VEC;   // covers x0-1 .. x0+64
+    static constexpr int HY = BY + 2;
+    static constexpr int PL = WX * HY;
+    static constexpr int NTHR = ((32 * (BY + 1) + (BY + 1) + 31) / 32) * 32;
+};
+template <typename T> struct Vec2;
+template <> struct Vec2<float> {
+    using type = float2;
+    static __device__ __forceinline__ float2 make(float a, float b) { return make_float2(a, b); }
+};
+template <> struct Vec2<double> {
+    using type = double2;
+    static __device__ __forceinline__ double2 make(double a, double b) { return make_double2(a, b); }
+};
+
+template <typename T, int EM, bool HA, int BY, int S>
+__global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pair_v_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
-    const __grid_constant__ CUtensorMap tm_cH, Dev<float> D, Coef<float, EM, HA> cf, float *__restrict__ wout,
-    float *__restrict__ y, Sched sch, float a, float b, float e2, float cl, int init, int mode, EtDev et) {
-    using G = GeoV<BY>;
-    using SL = StageL<float, EM, HA, G>;
+    const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
+    T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
+    using G = GeoW<T, BY>;
+    using V2 = typename Vec2<T>::type;
+    using SL = StageL<T, EM, HA, G>;
     constexpr int RX = 68, RR = RX * (BY + 1);              // ring row pitch, ring plane
     if (et.norms && et_skip(et)) {                          // early termination (f2)
         if (sch.ctr && blockIdx.x == 0 && threadIdx.x == 0)
@@ -1295,9 +1317,9 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 2) pair_v_kernel(
         return;
     }
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float *stages = reinterpret_cast<float *>(smem_raw);
-    float *UE = stages + S * SL::SZ;                        // [2][3][RR]
-    float *UH = UE + 2 * 3 * RR;                            // [3][RR]
+    T *stages = reinterpret_cast<T *>(smem_raw);
+    T *UE = stages + S * SL::SZ;                        // [2][3][RR]
+    T *UH = UE + 2 * 3 * RR;                            // [3][RR]
     uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(UH + 3 * RR) + 15) & ~uintptr_t(15));
     const int tid = threadIdx.x;
     const bool pair = tid < 32 * (BY + 1);
@@ -1311,15 +1333,15 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 2) pair_v_kernel(
     const int yH = pair ? (jr < BY ? jr : -1) : jr - 1;     // H rows -1..BY-1
     const int sE = (yE + 1) * G::WX + xE + G::OX, sH = (yH + 1) * G::WX + xH + G::OX;
     const int rE = yE * RX + xE + 2, rH = (yH + 1) * RX + xH + 2;
-    float bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
-    const float bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
+    T bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
+    const T bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
     if (tid == 0) {
         for (int s2 = 0; s2 < S; ++s2) mbar_init(&bars[s2], 1);
         fence_barrier_init();
     }
     __syncthreads();
-    auto ld2 = [](const float *p) { return *reinterpret_cast<const float2 *>(p); };
-    auto st2 = [](float *p, float u, float v) { *reinterpret_cast<float2 *>(p) = make_float2(u, v); };
+    auto ld2 = [](const T *p) { return *reinterpret_cast<const V2 *>(p); };
+    auto st2 = [](T *p, T u, T v) { *reinterpret_cast<V2 *>(p) = Vec2<T>::make(u, v); };
     double dacc = 0.0, yacc = 0.0;
     uint32_t lcount = 0;
     for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
@@ -1336,35 +1358,35 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 2) pair_v_kernel(
         const bool doT = own && inEa;                       // tile pair (E point == H point == own)
         const int64_t gB = D.idx(doT ? iEa : 0, doT ? jE : 0, 0);
         // carried own values of plane k
-        float hxa = 0.f, hxb = 0.f, hya = 0.f, hyb = 0.f, hza = 0.f, hzb = 0.f;   // w_h at E point
-        float exa = 0.f, exb = 0.f, eya = 0.f, eyb = 0.f;                         // w_e at H point
-        float uea0 = 0.f, ueb0 = 0.f, uea1 = 0.f, ueb1 = 0.f, uea2 = 0.f, ueb2 = 0.f;   // u_e(k)
-        float uma0 = 0.f, umb0 = 0.f, uma1 = 0.f, umb1 = 0.f, uma2 = 0.f, umb2 = 0.f;   // u_h(k-1)
+        T hxa = T(0), hxb = T(0), hya = T(0), hyb = T(0), hza = T(0), hzb = T(0);   // w_h at E point
+        T exa = T(0), exb = T(0), eya = T(0), eyb = T(0);                         // w_e at H point
+        T uea0 = T(0), ueb0 = T(0), uea1 = T(0), ueb1 = T(0), uea2 = T(0), ueb2 = T(0);   // u_e(k)
+        T uma0 = T(0), umb0 = T(0), uma1 = T(0), umb1 = T(0), uma2 = T(0), umb2 = T(0);   // u_h(k-1)
         if (tid == 0)
             for (int p = 0; p < min(S, nplanes); ++p) {
                 const uint32_t L = lcount + p;
-                issue_plane<float, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
                                               &tm_cH, x0, y0, kb - 1 + p);
             }
         for (int p = 0; p + 1 < nplanes; ++p) {
             const int k = kb - 1 + p, kk = k + 1;
             const uint32_t L0 = lcount + p, L1 = L0 + 1;
             const bool doB = doT && k >= kb;
-            float2 yv[6];
+            V2 yv[6];
 #pragma unroll
-            for (int c = 0; c < 6; ++c) yv[c] = make_float2(0.f, 0.f);
+            for (int c = 0; c < 6; ++c) yv[c] = Vec2<T>::make(T(0), T(0));
             if (doB && !init) {
-                const float *yp = y + gB + (int64_t)k * D.plane;
+                const T *yp = y + gB + (int64_t)k * D.plane;
 #pragma unroll
                 for (int c = 0; c < 6; ++c) yv[c] = ld2(yp + c * D.cs);
             }
             if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
             mbar_wait(&bars[L1 % S], (L1 / S) & 1);
-            const float *P0 = stages + (L0 % S) * SL::SZ;   // plane k
-            const float *P1 = stages + (L1 % S) * SL::SZ;   // plane k+1
-            float *UE1 = UE + (kk & 1) * 3 * RR;
-            const float *UE0 = UE + (k & 1) * 3 * RR;
-            float bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;
+            const T *P0 = stages + (L0 % S) * SL::SZ;   // plane k
+            const T *P1 = stages + (L1 % S) * SL::SZ;   // plane k+1
+            T *UE1 = UE + (kk & 1) * 3 * RR;
+            const T *UE0 = UE + (k & 1) * 3 * RR;
+            T bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;
             if (EM == 1) {
                 if (kk < D.nz) {
                     bE0 = __ldg(cf.tab + kk) * cf.sig;
@@ -1379,7 +1401,7 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 2) pair_v_kernel(
             }
             if (p == 0 && act) {                            // w(kb-1) own values
                 if (pair) {
-                    float2 t = ld2(P0 + 3 * G::PL + sE); hxa = t.x; hxb = t.y;
+                    V2 t = ld2(P0 + 3 * G::PL + sE); hxa = t.x; hxb = t.y;
                     t = ld2(P0 + 4 * G::PL + sE); hya = t.x; hyb = t.y;
                     t = ld2(P0 + 5 * G::PL + sE); hza = t.x; hzb = t.y;
                     t = ld2(P0 + sH); exa = t.x; exb = t.y;
@@ -1390,54 +1412,54 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 2) pair_v_kernel(
                 }
             }
             // ---- phase A ----
-            float ua0 = 0.f, ub0 = 0.f, ua1 = 0.f, ub1 = 0.f, ua2 = 0.f, ub2 = 0.f;   // u_e(k+1)
-            float va0 = 0.f, vb0 = 0.f, va1 = 0.f, vb1 = 0.f, va2 = 0.f, vb2 = 0.f;   // u_h(k)
-            float h1xa = 0.f, h1xb = 0.f, h1ya = 0.f, h1yb = 0.f, h1za = 0.f, h1zb = 0.f;
-            float e1xa = 0.f, e1xb = 0.f, e1ya = 0.f, e1yb = 0.f, ezka = 0.f, ezkb = 0.f;
+            T ua0 = T(0), ub0 = T(0), ua1 = T(0), ub1 = T(0), ua2 = T(0), ub2 = T(0);   // u_e(k+1)
+            T va0 = T(0), vb0 = T(0), va1 = T(0), vb1 = T(0), va2 = T(0), vb2 = T(0);   // u_h(k)
+            T h1xa = T(0), h1xb = T(0), h1ya = T(0), h1yb = T(0), h1za = T(0), h1zb = T(0);
+            T e1xa = T(0), e1xb = T(0), e1ya = T(0), e1yb = T(0), ezka = T(0), ezkb = T(0);
             if (act) {
                 // u_e(k+1) = bE .* C^T w_h(k+1), w_h(k) own carried
                 {
-                    const float *hx = P1 + 3 * G::PL, *hy = P1 + 4 * G::PL, *hz = P1 + 5 * G::PL;
+                    const T *hx = P1 + 3 * G::PL, *hy = P1 + 4 * G::PL, *hz = P1 + 5 * G::PL;
                     const bool vk = kk < D.nz, kp = kk > 0;
-                    float wa0 = bE0, wa1 = bE1, wa2 = bE2, wb0 = bE0, wb1 = bE1, wb2 = bE2;
+                    T wa0 = bE0, wa1 = bE1, wa2 = bE2, wb0 = bE0, wb1 = bE1, wb2 = bE2;
                     if (pair) {
-                        const float2 X = ld2(hx + sE), Y = ld2(hy + sE), Z = ld2(hz + sE);
-                        const float2 Zjm = ld2(hz + sE - G::WX), Xjm = ld2(hx + sE - G::WX);
-                        const float zim = hz[sE - 1], yim = hy[sE - 1];
+                        const V2 X = ld2(hx + sE), Y = ld2(hy + sE), Z = ld2(hz + sE);
+                        const V2 Zjm = ld2(hz + sE - G::WX), Xjm = ld2(hx + sE - G::WX);
+                        const T zim = hz[sE - 1], yim = hy[sE - 1];
                         h1xa = X.x; h1xb = X.y; h1ya = Y.x; h1yb = Y.y; h1za = Z.x; h1zb = Z.y;
                         if (EM == 2) {
-                            const float2 A0 = ld2(P1 + SL::ST + sE), A1 = ld2(P1 + SL::ST + G::PL + sE);
-                            const float2 A2 = ld2(P1 + SL::ST + 2 * G::PL + sE);
+                            const V2 A0 = ld2(P1 + SL::ST + sE), A1 = ld2(P1 + SL::ST + G::PL + sE);
+                            const V2 A2 = ld2(P1 + SL::ST + 2 * G::PL + sE);
                             wa0 = A0.x * cf.sig; wb0 = A0.y * cf.sig;
                             wa1 = A1.x * cf.sig; wb1 = A1.y * cf.sig;
                             wa2 = A2.x * cf.sig; wb2 = A2.y * cf.sig;
                         }
-                        const float c0a = ((Z.x - Zjm.x) - Y.x) + hya, c0b = ((Z.y - Zjm.y) - Y.y) + hyb;
-                        const float c1a = ((X.x - hxa) - Z.x) + zim, c1b = ((X.y - hxb) - Z.y) + Z.x;
-                        const float c2a = ((Y.x - yim) - X.x) + Xjm.x, c2b = ((Y.y - Y.x) - X.y) + Xjm.y;
-                        ua0 = (inEa && jE > 0 && vk && kp) ? wa0 * c0a : 0.f;
-                        ub0 = (inEb && jE > 0 && vk && kp) ? wb0 * c0b : 0.f;
-                        ua1 = (inEa && iEa > 0 && vk && kp) ? wa1 * c1a : 0.f;
-                        ub1 = (inEb && vk && kp) ? wb1 * c1b : 0.f;
-                        ua2 = (inEa && iEa > 0 && jE > 0 && vk) ? wa2 * c2a : 0.f;
-                        ub2 = (inEb && jE > 0 && vk) ? wb2 * c2b : 0.f;
+                        const T c0a = ((Z.x - Zjm.x) - Y.x) + hya, c0b = ((Z.y - Zjm.y) - Y.y) + hyb;
+                        const T c1a = ((X.x - hxa) - Z.x) + zim, c1b = ((X.y - hxb) - Z.y) + Z.x;
+                        const T c2a = ((Y.x - yim) - X.x) + Xjm.x, c2b = ((Y.y - Y.x) - X.y) + Xjm.y;
+                        ua0 = (inEa && jE > 0 && vk && kp) ? wa0 * c0a : T(0);
+                        ub0 = (inEb && jE > 0 && vk && kp) ? wb0 * c0b : T(0);
+                        ua1 = (inEa && iEa > 0 && vk && kp) ? wa1 * c1a : T(0);
+                        ub1 = (inEb && vk && kp) ? wb1 * c1b : T(0);
+                        ua2 = (inEa && iEa > 0 && jE > 0 && vk) ? wa2 * c2a : T(0);
+                        ub2 = (inEb && jE > 0 && vk) ? wb2 * c2b : T(0);
                         st2(UE1 + rE, ua0, ub0);
                         st2(UE1 + RR + rE, ua1, ub1);
                         st2(UE1 + 2 * RR + rE, ua2, ub2);
                     } else {
-                        const float X = hx[sE], Y = hy[sE], Z = hz[sE];
+                        const T X = hx[sE], Y = hy[sE], Z = hz[sE];
                         h1xa = X; h1ya = Y; h1za = Z;
                         if (EM == 2) {
                             wa0 = P1[SL::ST + sE] * cf.sig;
                             wa1 = P1[SL::ST + G::PL + sE] * cf.sig;
                             wa2 = P1[SL::ST + 2 * G::PL + sE] * cf.sig;
                         }
-                        const float c0 = ((Z - hz[sE - G::WX]) - Y) + hya;
-                        const float c1 = ((X - hxa) - Z) + hz[sE - 1];
-                        const float c2 = ((Y - hy[sE - 1]) - X) + hx[sE - G::WX];
-                        ua0 = (inEa && jE > 0 && vk && kp) ? wa0 * c0 : 0.f;
-                        ua1 = (inEa && iEa > 0 && vk && kp) ? wa1 * c1 : 0.f;
-                        ua2 = (inEa && iEa > 0 && jE > 0 && vk) ? wa2 * c2 : 0.f;
+                        const T c0 = ((Z - hz[sE - G::WX]) - Y) + hya;
+                        const T c1 = ((X - hxa) - Z) + hz[sE - 1];
+                        const T c2 = ((Y - hy[sE - 1]) - X) + hx[sE - G::WX];
+                        ua0 = (inEa && jE > 0 && vk && kp) ? wa0 * c0 : T(0);
+                        ua1 = (inEa && iEa > 0 && vk && kp) ? wa1 * c1 : T(0);
+                        ua2 = (inEa && iEa > 0 && jE > 0 && vk) ? wa2 * c2 : T(0);
                         UE1[rE] = ua0;
                         UE1[RR + rE] = ua1;
                         UE1[2 * RR + rE] = ua2;
@@ -1445,36 +1467,36 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 2) pair_v_kernel(
                 }
                 // u_h(k) = -bH .* C w_e(k), w_e(k) x, y own carried
                 {
-                    const float *ex = P0, *ey = P0 + G::PL, *ez = P0 + 2 * G::PL;
+                    const T *ex = P0, *ey = P0 + G::PL, *ez = P0 + 2 * G::PL;
                     const bool vk = k >= 0 && k < D.nz;
-                    float ga0 = bH0, ga1 = bH1, ga2 = bH2, gb0 = bH0, gb1 = bH1, gb2 = bH2;
+                    T ga0 = bH0, ga1 = bH1, ga2 = bH2, gb0 = bH0, gb1 = bH1, gb2 = bH2;
                     if (pair) {
-                        const float2 EZ = ld2(ez + sH), EX1 = ld2(P1 + sH), EY1 = ld2(P1 + G::PL + sH);
-                        const float2 Zjp = ld2(ez + sH + G::WX), Xjp = ld2(ex + sH + G::WX);
-                        const float zip = ez[sH + 2], yip = ey[sH + 2];
+                        const V2 EZ = ld2(ez + sH), EX1 = ld2(P1 + sH), EY1 = ld2(P1 + G::PL + sH);
+                        const V2 Zjp = ld2(ez + sH + G::WX), Xjp = ld2(ex + sH + G::WX);
+                        const T zip = ez[sH + 2], yip = ey[sH + 2];
                         ezka = EZ.x; ezkb = EZ.y;
                         e1xa = EX1.x; e1xb = EX1.y; e1ya = EY1.x; e1yb = EY1.y;
                         if (HA) {
                             const int ch = SL::ST + SL::CE;
-                            const float2 A0 = ld2(P0 + ch + sH), A1 = ld2(P0 + ch + G::PL + sH), A2 = ld2(P0 + ch + 2 * G::PL + sH);
+                            const V2 A0 = ld2(P0 + ch + sH), A1 = ld2(P0 + ch + G::PL + sH), A2 = ld2(P0 + ch + 2 * G::PL + sH);
                             ga0 = A0.x * cf.sig; gb0 = A0.y * cf.sig;
                             ga1 = A1.x * cf.sig; gb1 = A1.y * cf.sig;
                             ga2 = A2.x * cf.sig; gb2 = A2.y * cf.sig;
                         }
-                        const float c0a = ((eya + Zjp.x) - EY1.x) - EZ.x, c0b = ((eyb + Zjp.y) - EY1.y) - EZ.y;
-                        const float c1a = ((EZ.x + EX1.x) - EZ.y) - exa, c1b = ((EZ.y + EX1.y) - zip) - exb;
-                        const float c2a = ((exa + eyb) - Xjp.x) - eya, c2b = ((exb + yip) - Xjp.y) - eyb;
-                        va0 = (inHa && iHa > 0 && vk) ? -(ga0 * c0a) : 0.f;
-                        vb0 = (inHb && vk) ? -(gb0 * c0b) : 0.f;
-                        va1 = (inHa && jH > 0 && vk) ? -(ga1 * c1a) : 0.f;
-                        vb1 = (inHb && jH > 0 && vk) ? -(gb1 * c1b) : 0.f;
-                        va2 = (inHa && vk && k > 0) ? -(ga2 * c2a) : 0.f;
-                        vb2 = (inHb && vk && k > 0) ? -(gb2 * c2b) : 0.f;
+                        const T c0a = ((eya + Zjp.x) - EY1.x) - EZ.x, c0b = ((eyb + Zjp.y) - EY1.y) - EZ.y;
+                        const T c1a = ((EZ.x + EX1.x) - EZ.y) - exa, c1b = ((EZ.y + EX1.y) - zip) - exb;
+                        const T c2a = ((exa + eyb) - Xjp.x) - eya, c2b = ((exb + yip) - Xjp.y) - eyb;
+                        va0 = (inHa && iHa > 0 && vk) ? -(ga0 * c0a) : T(0);
+                        vb0 = (inHb && vk) ? -(gb0 * c0b) : T(0);
+                        va1 = (inHa && jH > 0 && vk) ? -(ga1 * c1a) : T(0);
+                        vb1 = (inHb && jH > 0 && vk) ? -(gb1 * c1b) : T(0);
+                        va2 = (inHa && vk && k > 0) ? -(ga2 * c2a) : T(0);
+                        vb2 = (inHb && vk && k > 0) ? -(gb2 * c2b) : T(0);
                         st2(UH + rH, va0, vb0);
                         st2(UH + RR + rH, va1, vb1);
                         st2(UH + 2 * RR + rH, va2, vb2);
                     } else {
-                        const float EZv = ez[sH], EX1v = P1[sH], EY1v = P1[G::PL + sH];
+                        const T EZv = ez[sH], EX1v = P1[sH], EY1v = P1[G::PL + sH];
                         ezka = EZv;
                         e1xa = EX1v;
                         e1ya = EY1v;
@@ -1484,12 +1506,12 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 2) pair_v_kernel(
                             ga1 = P0[ch + G::PL + sH] * cf.sig;
                             ga2 = P0[ch + 2 * G::PL + sH] * cf.sig;
                         }
-                        const float c0 = ((eya + ez[sH + G::WX]) - EY1v) - EZv;
-                        const float c1 = ((EZv + EX1v) - ez[sH + 1]) - exa;
-                        const float c2 = ((exa + ey[sH + 1]) - ex[sH + G::WX]) - eya;
-                        va0 = (inHa && iHa > 0 && vk) ? -(ga0 * c0) : 0.f;
-                        va1 = (inHa && jH > 0 && vk) ? -(ga1 * c1) : 0.f;
-                        va2 = (inHa && vk && k > 0) ? -(ga2 * c2) : 0.f;
+                        const T c0 = ((eya + ez[sH + G::WX]) - EY1v) - EZv;
+                        const T c1 = ((EZv + EX1v) - ez[sH + 1]) - exa;
+                        const T c2 = ((exa + ey[sH + 1]) - ex[sH + G::WX]) - eya;
+                        va0 = (inHa && iHa > 0 && vk) ? -(ga0 * c0) : T(0);
+                        va1 = (inHa && jH > 0 && vk) ? -(ga1 * c1) : T(0);
+                        va2 = (inHa && vk && k > 0) ? -(ga2 * c2) : T(0);
                         UH[rH] = va0;
                         UH[RR + rH] = va1;
                         UH[2 * RR + rH] = va2;
@@ -1500,54 +1522,54 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 2) pair_v_kernel(
             // ---- phase B: w'(k), y(k) on the own tile pair ----
             if (doB) {
                 const bool inB = inEb;                      // right point inside the grid
-                float wn[12];
+                T wn[12];
 #pragma unroll
-                for (int c = 0; c < 12; ++c) wn[c] = 0.f;
-                const float w_a[6] = {exa, eya, ezka, hxa, hya, hza};
-                const float w_b[6] = {exb, eyb, ezkb, hxb, hyb, hzb};
-                float be[6] = {bEk0, bEk1, bEk2, bEk0, bEk1, bEk2};   // a: 0..2, b: 3..5
-                float bh[6] = {bH0, bH1, bH2, bH0, bH1, bH2};
+                for (int c = 0; c < 12; ++c) wn[c] = T(0);
+                const T w_a[6] = {exa, eya, ezka, hxa, hya, hza};
+                const T w_b[6] = {exb, eyb, ezkb, hxb, hyb, hzb};
+                T be[6] = {bEk0, bEk1, bEk2, bEk0, bEk1, bEk2};   // a: 0..2, b: 3..5
+                T bh[6] = {bH0, bH1, bH2, bH0, bH1, bH2};
                 if (EM == 2) {
-                    const float2 A0 = ld2(P0 + SL::ST + sE), A1 = ld2(P0 + SL::ST + G::PL + sE);
-                    const float2 A2 = ld2(P0 + SL::ST + 2 * G::PL + sE);
+                    const V2 A0 = ld2(P0 + SL::ST + sE), A1 = ld2(P0 + SL::ST + G::PL + sE);
+                    const V2 A2 = ld2(P0 + SL::ST + 2 * G::PL + sE);
                     be[0] = A0.x * cf.sig; be[3] = A0.y * cf.sig;
                     be[1] = A1.x * cf.sig; be[4] = A1.y * cf.sig;
                     be[2] = A2.x * cf.sig; be[5] = A2.y * cf.sig;
                 }
                 if (HA) {
                     const int ch = SL::ST + SL::CE;
-                    const float2 A0 = ld2(P0 + ch + sE), A1 = ld2(P0 + ch + G::PL + sE), A2 = ld2(P0 + ch + 2 * G::PL + sE);
+                    const V2 A0 = ld2(P0 + ch + sE), A1 = ld2(P0 + ch + G::PL + sE), A2 = ld2(P0 + ch + 2 * G::PL + sE);
                     bh[0] = A0.x * cf.sig; bh[3] = A0.y * cf.sig;
                     bh[1] = A1.x * cf.sig; bh[4] = A1.y * cf.sig;
                     bh[2] = A2.x * cf.sig; bh[5] = A2.y * cf.sig;
                 }
                 if (mode != 1) {
                     // C u_e(k): j+1 from the ring (float2), i+1 = own right (a) / ring i+2 (b)
-                    const float2 UZj = ld2(UE0 + 2 * RR + rE + RX), UXj = ld2(UE0 + rE + RX);
-                    const float uzi = UE0[2 * RR + rE + 2], uyi = UE0[RR + rE + 2];
-                    const float c0a = ((uea1 + UZj.x) - ua1) - uea2, c0b = ((ueb1 + UZj.y) - ub1) - ueb2;
-                    const float c1a = ((uea2 + ua0) - ueb2) - uea0, c1b = ((ueb2 + ub0) - uzi) - ueb0;
-                    const float c2a = ((uea0 + ueb1) - UXj.x) - uea1, c2b = ((ueb0 + uyi) - UXj.y) - ueb1;
+                    const V2 UZj = ld2(UE0 + 2 * RR + rE + RX), UXj = ld2(UE0 + rE + RX);
+                    const T uzi = UE0[2 * RR + rE + 2], uyi = UE0[RR + rE + 2];
+                    const T c0a = ((uea1 + UZj.x) - ua1) - uea2, c0b = ((ueb1 + UZj.y) - ub1) - ueb2;
+                    const T c1a = ((uea2 + ua0) - ueb2) - uea0, c1b = ((ueb2 + ub0) - uzi) - ueb0;
+                    const T c2a = ((uea0 + ueb1) - UXj.x) - uea1, c2b = ((ueb0 + uyi) - UXj.y) - ueb1;
                     // C^T u_h(k): j-1 from the ring (float2), i-1 = ring (a) / own left (b)
-                    const float2 HZj = ld2(UH + 2 * RR + rH - RX), HXj = ld2(UH + rH - RX);
-                    const float hzi = UH[2 * RR + rH - 1], hyi = UH[RR + rH - 1];
-                    const float d0a = ((va2 - HZj.x) - va1) + uma1, d0b = ((vb2 - HZj.y) - vb1) + umb1;
-                    const float d1a = ((va0 - uma0) - va2) + hzi, d1b = ((vb0 - umb0) - vb2) + va2;
-                    const float d2a = ((va1 - hyi) - va0) + HXj.x, d2b = ((vb1 - va1) - vb0) + HXj.y;
+                    const V2 HZj = ld2(UH + 2 * RR + rH - RX), HXj = ld2(UH + rH - RX);
+                    const T hzi = UH[2 * RR + rH - 1], hyi = UH[RR + rH - 1];
+                    const T d0a = ((va2 - HZj.x) - va1) + uma1, d0b = ((vb2 - HZj.y) - vb1) + umb1;
+                    const T d1a = ((va0 - uma0) - va2) + hzi, d1b = ((vb0 - umb0) - vb2) + va2;
+                    const T d2a = ((va1 - hyi) - va0) + HXj.x, d2b = ((vb1 - va1) - vb0) + HXj.y;
                     const bool kp = k > 0, jp = jE > 0, ip = iEa > 0;
-                    wn[0] = ((jp && kp) ? be[0] * d0a : 0.f) + e2 * w_a[0];
-                    wn[1] = ((ip && kp) ? be[1] * d1a : 0.f) + e2 * w_a[1];
-                    wn[2] = ((ip && jp) ? be[2] * d2a : 0.f) + e2 * w_a[2];
-                    wn[3] = (ip ? -(bh[0] * c0a) : 0.f) + e2 * w_a[3];
-                    wn[4] = (jp ? -(bh[1] * c1a) : 0.f) + e2 * w_a[4];
-                    wn[5] = (kp ? -(bh[2] * c2a) : 0.f) + e2 * w_a[5];
+                    wn[0] = ((jp && kp) ? be[0] * d0a : T(0)) + e2 * w_a[0];
+                    wn[1] = ((ip && kp) ? be[1] * d1a : T(0)) + e2 * w_a[1];
+                    wn[2] = ((ip && jp) ? be[2] * d2a : T(0)) + e2 * w_a[2];
+                    wn[3] = (ip ? -(bh[0] * c0a) : T(0)) + e2 * w_a[3];
+                    wn[4] = (jp ? -(bh[1] * c1a) : T(0)) + e2 * w_a[4];
+                    wn[5] = (kp ? -(bh[2] * c2a) : T(0)) + e2 * w_a[5];
                     if (inB) {
-                        wn[6] = ((jp && kp) ? be[3] * d0b : 0.f) + e2 * w_b[0];
-                        wn[7] = (kp ? be[4] * d1b : 0.f) + e2 * w_b[1];
-                        wn[8] = (jp ? be[5] * d2b : 0.f) + e2 * w_b[2];
+                        wn[6] = ((jp && kp) ? be[3] * d0b : T(0)) + e2 * w_b[0];
+                        wn[7] = (kp ? be[4] * d1b : T(0)) + e2 * w_b[1];
+                        wn[8] = (jp ? be[5] * d2b : T(0)) + e2 * w_b[2];
                         wn[9] = -(bh[3] * c0b) + e2 * w_b[3];
-                        wn[10] = (jp ? -(bh[4] * c1b) : 0.f) + e2 * w_b[4];
-                        wn[11] = (kp ? -(bh[5] * c2b) : 0.f) + e2 * w_b[5];
+                        wn[10] = (jp ? -(bh[4] * c1b) : T(0)) + e2 * w_b[4];
+                        wn[11] = (kp ? -(bh[5] * c2b) : T(0)) + e2 * w_b[5];
                     }
                 }
                 const int64_t go = gB + (int64_t)k * D.plane;
@@ -1555,26 +1577,26 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 2) pair_v_kernel(
 #pragma unroll
                     for (int c = 0; c < 6; ++c) st2(wout + go + c * D.cs, wn[c], wn[6 + c]);
                 }
-                const float u_a[6] = {uea0, uea1, uea2, va0, va1, va2};
-                const float u_b[6] = {ueb0, ueb1, ueb2, vb0, vb1, vb2};
+                const T u_a[6] = {uea0, uea1, uea2, va0, va1, va2};
+                const T u_b[6] = {ueb0, ueb1, ueb2, vb0, vb1, vb2};
 #pragma unroll
                 for (int c = 0; c < 6; ++c) {
-                    float qa = (yv[c].x + a * w_a[c]) + b * u_a[c];
-                    float qb = (yv[c].y + a * w_b[c]) + b * u_b[c];
+                    T qa = (yv[c].x + a * w_a[c]) + b * u_a[c];
+                    T qb = (yv[c].y + a * w_b[c]) + b * u_b[c];
                     if (mode == 2) {
                         qa = qa + cl * wn[c];
                         qb = qb + cl * wn[6 + c];
                     }
-                    if (!inB) qb = 0.f;
+                    if (!inB) qb = T(0);
                     st2(y + go + c * D.cs, qa, qb);
                     if (et.norms) {
-                        const float ga = c < 3 ? be[c] : bh[c - 3], gb = c < 3 ? be[3 + c] : bh[c];
-                        if (ga != 0.f) {
+                        const T ga = c < 3 ? be[c] : bh[c - 3], gb = c < 3 ? be[3 + c] : bh[c];
+                        if (ga != T(0)) {
                             const double d = (double)qa - (double)yv[c].x;
                             dacc += d * d / (double)ga;
                             yacc += (double)qa * qa / (double)ga;
                         }
-                        if (inB && gb != 0.f) {
+                        if (inB && gb != T(0)) {
                             const double d = (double)qb - (double)yv[c].y;
                             dacc += d * d / (double)gb;
                             yacc += (double)qb * qb / (double)gb;
@@ -1590,7 +1612,7 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 2) pair_v_kernel(
             __syncthreads();
             if (tid == 0 && p + S < nplanes) {
                 const uint32_t L = lcount + p + S;
-                issue_plane<float, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
                                               &tm_cH, x0, y0, kb - 1 + p + S);
             }
         }
@@ -2352,30 +2374,29 @@ static int horner_stages() {
     return v;
 }
 
-// K2v launcher (fp32, 64 x 8 tiles, two points per thread; same buffer protocol as K2)
-template <int EM, bool HA, int S>
+// K2v launcher (64 x BY tiles, two points per thread; same buffer protocol as K2)
+template <typename T, int EM, bool HA, int BY, int S>
 static int poly_v_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
-    constexpr int BY = 8;
-    using G = GeoV<BY>;
+    using G = GeoW<T, BY>;
     constexpr int RR = 68 * (BY + 1);
-    constexpr size_t smem = (size_t)(S * StageL<float, EM, HA, G>::SZ + 3 * 3 * RR) * sizeof(float) + 8 * S + 16;
+    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 3 * 3 * RR) * sizeof(T) + 8 * S + 16;
     const Grid &g = *ka.g;
-    auto kern = pair_v_kernel<EM, HA, BY, S>;
+    auto kern = pair_v_kernel<T, EM, HA, BY, S>;
     static const int per_sm = resident_per_sm(kern, G::NTHR, smem);
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "pair_v kernel does not fit on an SM");
     const Sched sch = make_sched(g, G::BX, BY, per_sm * num_sms());
     const int grid = std::min(sch.units, per_sm * num_sms());
-    auto D = make_dev<float>(g);
-    auto cf = make_coef<float, EM, HA>(g, plan.sigma);
+    auto D = make_dev<T>(g);
+    auto cf = make_coef<T, EM, HA>(g, plan.sigma);
     CUtensorMap tmE, tmH;
     int rc;
-    if (EM == 2 && (rc = make_map<float>(&tmE, g, g.d_cE_arr, 3, G::WX, G::HY))) return rc;
-    if (HA && (rc = make_map<float>(&tmH, g, g.d_cH_arr, 3, G::WX, G::HY))) return rc;
+    if (EM == 2 && (rc = make_map<T>(&tmE, g, g.d_cE_arr, 3, G::WX, G::HY))) return rc;
+    if (HA && (rc = make_map<T>(&tmH, g, g.d_cH_arr, 3, G::WX, G::HY))) return rc;
     cudaStream_t s = (cudaStream_t)ka.stream;
-    float *w = (float *)bufs[0], *yy = (float *)bufs[1], *sp = (float *)bufs[2], *sp2 = (float *)bufs[3];
+    T *w = (T *)bufs[0], *yy = (T *)bufs[1], *sp = (T *)bufs[2], *sp2 = (T *)bufs[3];
     CUtensorMap tmW, tmS;
-    if ((rc = make_map<float>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
-    if ((rc = make_map<float>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
+    if ((rc = make_map<T>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
+    if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
     int init = 1;
     EtDev et;
     if (ka.et) et = *ka.et;
@@ -2383,8 +2404,8 @@ static int poly_v_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     for (const Op &op : plan.ops) {
         et.op = opi++;
         et.apps = op.kind == 1 ? 1 : 2;
-        kern<<<grid, G::NTHR, smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), (float)op.a,
-                                          (float)op.b, (float)op.e2, (float)op.c, init, op.kind, et);
+        kern<<<grid, G::NTHR, smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), (T)op.a,
+                                          (T)op.b, (T)op.e2, (T)op.c, init, op.kind, et);
         ++*ka.launches;
         if (op.kind == 0) {
             std::swap(w, sp);
@@ -2411,7 +2432,7 @@ int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
             if (!ka.et && horner_stages() == 3) return poly_horner_V<T, EM, 3>(ka, plan, bufs);
         }
         if constexpr (std::is_same<T, float>::value) {
-            if (lf_vec_enabled()) return poly_v_V<EM, HA, 3>(ka, plan, bufs);   // K2v (fp32)
+            if (lf_vec_enabled()) return poly_v_V<float, EM, HA, 8, 3>(ka, plan, bufs);   // K2v (fp32)
         }
         // K2r measured slower than K2 on B200 (fp64 306 vs 289 us per A-application: barrier
         // stalls -- the frame threads idle through phase B); opt-in with PARAEXP_PAIR_R=1
