@@ -22,12 +22,6 @@ const double kMu0 = 1.25663706212e-6;
 
 namespace pe {
 
-static bool all_equal(const double *a, int64_t n) {
-    for (int64_t q = 1; q < n; ++q)
-        if (a[q] != a[0]) return false;
-    return true;
-}
-
 static int build_coefficients(Grid &G, const paraexp_grid_desc &d) {
     const int nx = G.nx, ny = G.ny, nz = G.nz;
     std::vector<double> dx(nx), dy(ny), dz(nz);
