@@ -1302,7 +1302,7 @@ template <> struct Vec2<double> {
     static __device__ __forceinline__ double2 make(double a, double b) { return make_double2(a, b); }
 };
 
-template <typename T, int EM, bool HA, int BY, int S>
+template <typename T, int EM, bool HA, int BY, int S, bool ET>
 __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pair_v_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
@@ -1311,7 +1311,7 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
     using V2 = typename Vec2<T>::type;
     using SL = StageL<T, EM, HA, G>;
     constexpr int RX = 68, RR = RX * (BY + 1);              // ring row pitch, ring plane
-    if (et.norms && et_skip(et)) {                          // early termination (f2)
+    if (ET && et.norms && et_skip(et)) {                          // early termination (f2)
         if (sch.ctr && blockIdx.x == 0 && threadIdx.x == 0)
             atomicAdd(sch.ctr, (unsigned long long)sch.units + gridDim.x);
         return;
@@ -1589,7 +1589,7 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
                     }
                     if (!inB) qb = T(0);
                     st2(y + go + c * D.cs, qa, qb);
-                    if (et.norms) {
+                    if (ET && et.norms) {
                         const T ga = c < 3 ? be[c] : bh[c - 3], gb = c < 3 ? be[3 + c] : bh[c];
                         if (ga != T(0)) {
                             const double d = (double)qa - (double)yv[c].x;
@@ -1618,7 +1618,7 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
         }
         lcount += nplanes;
     }
-    if (et.norms) {
+    if (ET && et.norms) {
         const double ds = block_sum(dacc);
         __syncthreads();
         const double ys = block_sum(yacc);
@@ -2381,8 +2381,10 @@ static int poly_v_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     constexpr int RR = 68 * (BY + 1);
     constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 3 * 3 * RR) * sizeof(T) + 8 * S + 16;
     const Grid &g = *ka.g;
-    auto kern = pair_v_kernel<T, EM, HA, BY, S>;
-    static const int per_sm = resident_per_sm(kern, G::NTHR, smem);
+    auto kern = ka.et ? pair_v_kernel<T, EM, HA, BY, S, true> : pair_v_kernel<T, EM, HA, BY, S, false>;
+    static const int per_sm = resident_per_sm(pair_v_kernel<T, EM, HA, BY, S, true>, G::NTHR, smem);
+    static const int per_sm2 = resident_per_sm(pair_v_kernel<T, EM, HA, BY, S, false>, G::NTHR, smem);
+    if (per_sm2 < per_sm) return fail(PARAEXP_ECUDA, "pair_v variants differ in occupancy");
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "pair_v kernel does not fit on an SM");
     const Sched sch = make_sched(g, G::BX, BY, per_sm * num_sms());
     const int grid = std::min(sch.units, per_sm * num_sms());
