@@ -227,8 +227,35 @@ static void build_ops(Plan &p) {
     }
 }
 
-int make_plan(int method, int m, int s, double eps_A, double tau, double rho, double dt,
-              Plan &out) {
+static int make_plan_uncached(int method, int m, int s, double eps_A, double tau, double rho, double dt,
+                              Plan &out);
+
+// Plans are pure functions of their arguments; building the Newton coefficients (quad
+// precision, m up to 100) costs up to ~0.3 s on the host, which a ParaExp solve would
+// otherwise pay on every call while the GPU idles.  Memoise them (bounded).
+int make_plan(int method, int m, int s, double eps_A, double tau, double rho, double dt, Plan &out) {
+    using Key = std::tuple<int, int, int, double, double, double, double>;
+    static std::mutex mu;
+    static std::map<Key, Plan> cache;
+    const Key key{method, m, s, eps_A, tau, rho, dt};
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            out = it->second;
+            return PARAEXP_OK;
+        }
+    }
+    int rc = make_plan_uncached(method, m, s, eps_A, tau, rho, dt, out);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() >= 512) cache.clear();
+    cache.emplace(key, out);
+    return PARAEXP_OK;
+}
+
+static int make_plan_uncached(int method, int m, int s, double eps_A, double tau, double rho, double dt,
+                              Plan &out) {
     if (method == PARAEXP_KRYLOV) {
         // f3: Krylov plan = subspace dimension l = m and substeps s (reading 31)
         if (!(tau >= 0) || !std::isfinite(tau)) return fail(PARAEXP_EINVAL, "tau must be >= 0");
