@@ -338,11 +338,12 @@ def solve(grid: Grid, nsteps: int, p: int, sources=None, t0: float = 0.0, method
 
 def solve_trace(grid: Grid, nsteps: int, p: int, sources=None, t0: float = 0.0, method="leja", m=0,
                 s=0, eps_A=1e-12, rho=0.0, u0=None, e_out=None, h_out=None, probes=None,
-                energy: bool = True, comm: Optional[Comm] = None, broadcast_out=False, stream=None):
+                energy: bool = True, comm: Optional[Comm] = None, broadcast_out=False, stream=None,
+                early_term=False, beta=0.0):
     """paraexp_solve_trace: solve plus the energy / probe rows at the sub-interval boundaries
     T_1..T_p (f1).  Returns (stats, energy[p] or None, probe[p, nprobe] or None)."""
     arr, n = make_sources(sources)
-    o = _opts(method, m, s, eps_A, rho)
+    o = _opts(method, m, s, eps_A, rho, early_term, beta)
     t, en, pr = _trace(grid, p, probes, energy)
     st = abi.paraexp_stats()
     e0 = h0 = C.c_void_p(0)
