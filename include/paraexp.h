@@ -64,7 +64,7 @@ enum { PARAEXP_TAIL_EXP = 0, PARAEXP_TAIL_LEAPFROG = 1 };
 enum { PARAEXP_MAT_SCALAR = 0, PARAEXP_MAT_ZTABLE = 1, PARAEXP_MAT_ARRAY = 2 };
 enum { PARAEXP_KERNELS_AUTO = 0, PARAEXP_KERNELS_UNFUSED = 1, PARAEXP_KERNELS_FUSED = 2 };
 
-#define PARAEXP_MAX_DEGREE 100
+#define PARAEXP_MAX_DEGREE 150
 #define PARAEXP_MAX_SOURCES 64
 
 /* ---- grid ------------------------------------------------------------------------ */
@@ -216,9 +216,9 @@ int paraexp_leapfrog_trace(paraexp_grid *grid, const paraexp_source *src, int32_
  *            PARAEXP_KRYLOV (Arnoldi with sigma = infinity, SURVEY 8(f) f3:
  *            per substep h = tau/s an l = m dimensional Krylov space of X = hA in the
  *            energy inner product, modified Gram-Schmidt applied twice, result
- *            ||b|| V_l exp(H_l) e_1; m = l in 1..100 any parity; s = 0 => s = ceil(2 rho tau / l)
+ *            ||b|| V_l exp(H_l) e_1; m = l in 1..150 any parity; s = 0 => s = ceil(2 rho tau / l)
  *            (rho h <= l/2, reading 31); eps_A unused; stops early on a happy breakdown)
- *   m, s     fixed degree (1 or even, <= 100) and substep count; m = 0 => choose (m, s)
+ *   m, s     fixed degree (1 or even, <= 150, reading 16) and substep count; m = 0 => choose (m, s)
  *            minimising m*s subject to the per-substep criterion of reading 16 at eps_A;
  *            m > 0 with s = 0 => s from the criterion at that m
  *   eps_A    relative backward-error tolerance in (1e-14, 1)

@@ -26,7 +26,7 @@ TAYLOR, LEJA, KRYLOV = 0, 1, 2
 TAIL_EXP, TAIL_LEAPFROG = 0, 1
 MAT_SCALAR, MAT_ZTABLE, MAT_ARRAY = 0, 1, 2
 KERNELS_AUTO, KERNELS_UNFUSED, KERNELS_FUSED = 0, 1, 2
-MAX_DEGREE = 100
+MAX_DEGREE = 150
 MAX_PROBES = 16
 
 _dp = C.POINTER(C.c_double)

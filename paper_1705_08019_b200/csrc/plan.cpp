@@ -260,7 +260,7 @@ static int make_plan_uncached(int method, int m, int s, double eps_A, double tau
         // f3: Krylov plan = subspace dimension l = m and substeps s (reading 31)
         if (!(tau >= 0) || !std::isfinite(tau)) return fail(PARAEXP_EINVAL, "tau must be >= 0");
         if (!(rho >= 0) || !std::isfinite(rho)) return fail(PARAEXP_EINVAL, "rho must be >= 0");
-        if (m < 1 || m > PARAEXP_MAX_DEGREE) return fail(PARAEXP_EINVAL, "Krylov dimension m must be in 1..100");
+        if (m < 1 || m > PARAEXP_MAX_DEGREE) return fail(PARAEXP_EINVAL, "Krylov dimension m must be in 1..150");
         if (s < 0) return fail(PARAEXP_EINVAL, "s must be >= 0");
         out = Plan();
         out.method = method;
@@ -280,7 +280,7 @@ static int make_plan_uncached(int method, int m, int s, double eps_A, double tau
     if (method != PARAEXP_LEJA && method != PARAEXP_TAYLOR) return fail(PARAEXP_EINVAL, "bad method");
     if (!(tau >= 0) || !std::isfinite(tau)) return fail(PARAEXP_EINVAL, "tau must be >= 0");
     if (!(rho >= 0) || !std::isfinite(rho)) return fail(PARAEXP_EINVAL, "rho must be >= 0");
-    if (m < 0 || m > PARAEXP_MAX_DEGREE || (m > 1 && m % 2)) return fail(PARAEXP_EINVAL, "degree m must be 1 or even and <= 100");
+    if (m < 0 || m > PARAEXP_MAX_DEGREE || (m > 1 && m % 2)) return fail(PARAEXP_EINVAL, "degree m must be 1 or even and <= 150");
     if (s < 0) return fail(PARAEXP_EINVAL, "s must be >= 0");
     if ((m == 0 || s == 0) && !(eps_A >= 1e-14 && eps_A < 1)) return fail(PARAEXP_EINVAL, "eps_A must lie in [1e-14, 1)");
     out = Plan();
@@ -296,10 +296,10 @@ static int make_plan_uncached(int method, int m, int s, double eps_A, double tau
     }
     const double tr = tau * rho;
     if (m == 0) {
-        static const int leja_c[] = {8, 12, 16, 20, 24, 32, 40, 48, 56, 64, 72, 80, 88, 100};
+        static const int leja_c[] = {8, 12, 16, 20, 24, 32, 40, 48, 56, 64, 72, 80, 88, 100, 120, 150};
         static const int tay_c[] = {4, 8, 12, 16, 20, 24, 32, 40, 48};
         const int *c = method == PARAEXP_LEJA ? leja_c : tay_c;
-        const int nc = method == PARAEXP_LEJA ? 14 : 9;
+        const int nc = method == PARAEXP_LEJA ? 16 : 9;
         long best = -1;
         for (int q = 0; q < nc; ++q) {
             const double th = theta_m(method, c[q], eps_A);

@@ -77,7 +77,7 @@ def test_leapfrog_ragged(dtype, kind, kernels):
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("method,m,s", [("leja", 40, 3), ("leja", 1, 7), ("leja", 2, 5),
                                          ("leja", 64, 1), ("taylor", 16, 6), ("leja", 6, 2),
-                                         ("leja", 10, 1), ("leja", 4, 3)])
+                                         ("leja", 10, 1), ("leja", 4, 3), ("leja", 150, 1)])
 @pytest.mark.parametrize("kind", ["vacuum", "layered", "random"])
 @pytest.mark.parametrize("kernels", KERNELS)
 def test_expmv_fixed_plan(dtype, method, m, s, kind, kernels):

@@ -86,7 +86,7 @@ def test_auto_plan_minimises_cost():
     tau, rho, tol = 1.0, 300.0, 1e-10
     p = pe.plan_host("leja", 0, 0, tol, tau, rho)
     best = min((mm * max(1, math.ceil(tau * rho / pe.theta("leja", mm, tol))), mm)
-               for mm in [8, 12, 16, 20, 24, 32, 40, 48, 56, 64, 72, 80, 88, 100])
+               for mm in [8, 12, 16, 20, 24, 32, 40, 48, 56, 64, 72, 80, 88, 100, 120, 150])
     assert p["m"] * p["s"] == best[0]
 
 
