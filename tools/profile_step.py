@@ -1,6 +1,6 @@
 """Small driver for ncu captures: the bench workload's kernels (C3 256^3 layered fp64) on a
-short run -- a few fused leapfrog steps and one degree-100 Leja substep (the planner's choice
-for the bench's sub-intervals).  Usage: python tools/profile_step.py [f64|f32] [lf_steps] [n]"""
+short run -- a few fused leapfrog steps and one degree-150 Leja substep (the planner's choice
+for the bench's sub-intervals: m = 150, s = 9).  Usage: python tools/profile_step.py [f64|f32] [lf_steps] [n]"""
 import os
 import sys
 
@@ -22,7 +22,7 @@ def main():
     e = torch.rand(3 * g.npts, dtype=td, device="cuda:0")
     h = torch.rand(3 * g.npts, dtype=td, device="cuda:0") * 1e-3
     st = pe.leapfrog(g, e, h, nlf, w.sources)
-    st2 = pe.expmv(g, 512 * g.dt / 15, e, h, method="leja", m=100, s=1, rho=g.rho_cfl)
+    st2 = pe.expmv(g, 512 * g.dt / 9, e, h, method="leja", m=150, s=1, rho=g.rho_cfl)
     torch.cuda.synchronize()
     print("leapfrog ms", st["ms_leapfrog_kernels"], "expmv ms", st2["ms_poly_kernels"],
           "launches", st["kernel_launches"] + st2["kernel_launches"])
