@@ -1630,169 +1630,6 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
 }
 
 // ---------------------------------------------------------------------------------------
-// K2ws: the Newton pair with warp-specialised phases (scalar / z-table materials)
-// ---------------------------------------------------------------------------------------
-// Warps 0-9 (group A) compute phase A of plane k+1 (u_e(k+2), u_h(k+1)) while warps 10-17
-// (group B) compute phase B of plane k (w'(k), y(k)); one CTA barrier per plane hands the
-// rings over.  Rings are 3 planes deep, the TMA stage ring 4 planes, so the two groups never
-// touch each other's slots between barriers:
-//   A(t) writes u_e(kb+t) -> slot (kb+t)%3 and u_h(kb+t-1) -> slot (kb+t-1)%3,
-//   B(t-1) reads u_e(kb+t-2), u_e(kb+t-1), u_h(kb+t-2), u_h(kb+t-3) and stage plane kb+t-2.
-template <typename T, int EM, int BX, int BY>
-__global__ void __launch_bounds__(((Geo<T, BX, BY>::RP + 31) / 32) * 32 + BX * BY, 1) pair_ws_kernel(
-    const __grid_constant__ CUtensorMap tm_state, Dev<T> D, Coef<T, EM, false> cf, T *__restrict__ wout,
-    T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode) {
-    using G = Geo<T, BX, BY>;
-    using SL = StageL<T, EM, false, G>;
-    constexpr int S = 4, NR = 3;
-    constexpr int NA = ((G::RP + 31) / 32) * 32;          // group A threads
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    T *stages = reinterpret_cast<T *>(smem_raw);
-    T *UE = stages + S * SL::SZ;                          // [3][3][RP]
-    T *UH = UE + NR * 3 * G::RP;                          // [3][3][RP]
-    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(UH + NR * 3 * G::RP) + 15) & ~uintptr_t(15));
-    const int tid = threadIdx.x;
-    const bool grpA = tid < NA;
-    // group A: row-aligned phase-A points
-    constexpr int MAIN = BX * G::EY;
-    const int ii = tid < MAIN ? tid % BX : BX, jj = tid < MAIN ? tid / BX : tid - MAIN;
-    const bool hasA = grpA && tid < G::RP;
-    const int rA = jj * G::EX + ii;
-    const int sE = (jj + 1) * G::WX + ii + G::OX;
-    const int sH = jj * G::WX + ii - 1 + G::OX;
-    // group B: tile points
-    const int bt = tid - NA;
-    const bool hasB = !grpA && bt < G::NT;
-    const int tx = bt % BX, ty = bt / BX;
-    const int re = ty * G::EX + tx;
-    const int rh = (ty + 1) * G::EX + (tx + 1);
-    const int sB = (ty + 1) * G::WX + tx + G::OX;
-    const T bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
-    auto slot3 = [](int q) { return ((q % 3) + 3) % 3; };
-    auto bEat = [&](int c, int k) -> T {
-        if (EM == 1) return __ldg(cf.tab + c * cf.nz + k) * cf.sig;
-        return cf.cEs[c] * cf.sig;
-    };
-    if (tid == 0) {
-        for (int s2 = 0; s2 < S; ++s2) mbar_init(&bars[s2], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    uint32_t lcount = 0;
-    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
-        const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
-        const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
-        const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
-        const int nplanes = ke - kb + 2;
-        const int iE = x0 + ii, jE = y0 + jj;
-        const bool inE = hasA && iE < D.nx && jE < D.ny;
-        const bool lxE = inE && jE > 0, lyE = inE && iE > 0, lzE = inE && iE > 0 && jE > 0;
-        const int iH = iE - 1, jH = jE - 1;
-        const bool inH = hasA && iH >= 0 && jH >= 0 && iH < D.nx && jH < D.ny;
-        const bool lxH = inH && iH > 0, lyH = inH && jH > 0;
-        const int iB = x0 + tx, jB = y0 + ty;
-        const bool inB = hasB && iB < D.nx && jB < D.ny;
-        const bool lxBe = jB > 0, lyBe = iB > 0, lzBe = iB > 0 && jB > 0;
-        const bool lxBh = iB > 0, lyBh = jB > 0;
-        const int64_t gB = D.idx(inB ? iB : 0, inB ? jB : 0, 0);
-        if (tid == 0)
-            for (int q = 0; q < min(S, nplanes); ++q) {
-                const uint32_t L = lcount + q;
-                issue_plane<T, EM, false, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, nullptr, nullptr,
-                                             x0, y0, kb - 1 + q);
-            }
-        for (int t = 0; t < nplanes; ++t) {
-            if (grpA) {
-                if (t <= nplanes - 2 && hasA) {            // A(t): planes k = kb-1+t, kk = k+1
-                    const int k = kb - 1 + t, kk = k + 1;
-                    const uint32_t L0 = lcount + t, L1 = L0 + 1;
-                    if (t == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
-                    mbar_wait(&bars[L1 % S], (L1 / S) & 1);
-                    const T *P0 = stages + (L0 % S) * SL::SZ, *P1 = stages + (L1 % S) * SL::SZ;
-                    T *UE1 = UE + slot3(kk) * 3 * G::RP;
-                    T *UH0 = UH + slot3(k) * 3 * G::RP;
-                    {
-                        T c0, c1, c2;
-                        curlT_stage<T, G>(P1, P0, sE, c0, c1, c2);
-                        const bool vk = kk < D.nz, kp = kk > 0;
-                        UE1[rA] = (lxE && vk && kp) ? bEat(0, kk) * c0 : T(0);
-                        UE1[G::RP + rA] = (lyE && vk && kp) ? bEat(1, kk) * c1 : T(0);
-                        UE1[2 * G::RP + rA] = (lzE && vk) ? bEat(2, kk) * c2 : T(0);
-                    }
-                    {
-                        T c0, c1, c2;
-                        curl_stage<T, G>(P0, P1, sH, c0, c1, c2);
-                        const bool vk = k >= 0 && k < D.nz;
-                        UH0[rA] = (lxH && vk) ? -(bH0 * c0) : T(0);
-                        UH0[G::RP + rA] = (lyH && vk) ? -(bH1 * c1) : T(0);
-                        UH0[2 * G::RP + rA] = (inH && vk && k > 0) ? -(bH2 * c2) : T(0);
-                    }
-                }
-            } else if (t >= 2 && inB) {                   // B(t-1): plane k = kb + t - 2
-                const int k = kb + t - 2;
-                const uint32_t L0 = lcount + t - 1;
-                T yv[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
-                const int64_t go = gB + (int64_t)k * D.plane;
-                if (!init) {
-#pragma unroll
-                    for (int c = 0; c < 6; ++c) yv[c] = y[go + c * D.cs];
-                }
-                mbar_wait(&bars[L0 % S], (L0 / S) & 1);   // completed long ago: visibility only
-                const T *P0 = stages + (L0 % S) * SL::SZ;
-                const T *UE0 = UE + slot3(k) * 3 * G::RP, *UE1 = UE + slot3(k + 1) * 3 * G::RP;
-                const T *UH0 = UH + slot3(k) * 3 * G::RP, *UHm = UH + slot3(k - 1) * 3 * G::RP;
-                const T ux0 = UE0[re], uy0 = UE0[G::RP + re], uz0 = UE0[2 * G::RP + re];
-                const T hx0 = UH0[rh], hy0 = UH0[G::RP + rh], hz0 = UH0[2 * G::RP + rh];
-                T w[6];
-#pragma unroll
-                for (int c = 0; c < 6; ++c) w[c] = P0[c * G::PL + sB];
-                T wn[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
-                if (mode != 1) {
-                    const T uz_jp = UE0[2 * G::RP + re + G::EX], ux_jp = UE0[re + G::EX];
-                    const T uz_ip = UE0[2 * G::RP + re + 1], uy_ip = UE0[G::RP + re + 1];
-                    const T ux_kp = UE1[re], uy_kp = UE1[G::RP + re];
-                    const T c0 = ((uy0 + uz_jp) - uy_kp) - uz0;
-                    const T c1 = ((uz0 + ux_kp) - uz_ip) - ux0;
-                    const T c2 = ((ux0 + uy_ip) - ux_jp) - uy0;
-                    const T hz_jm = UH0[2 * G::RP + rh - G::EX], hx_jm = UH0[rh - G::EX];
-                    const T hz_im = UH0[2 * G::RP + rh - 1], hy_im = UH0[G::RP + rh - 1];
-                    const T hy_km = UHm[G::RP + rh], hx_km = UHm[rh];
-                    const T d0 = ((hz0 - hz_jm) - hy0) + hy_km;
-                    const T d1 = ((hx0 - hx_km) - hz0) + hz_im;
-                    const T d2 = ((hy0 - hy_im) - hx0) + hx_jm;
-                    const bool kp = k > 0;
-                    wn[0] = ((lxBe && kp) ? bEat(0, k) * d0 : T(0)) + e2 * w[0];
-                    wn[1] = ((lyBe && kp) ? bEat(1, k) * d1 : T(0)) + e2 * w[1];
-                    wn[2] = (lzBe ? bEat(2, k) * d2 : T(0)) + e2 * w[2];
-                    wn[3] = (lxBh ? -(bH0 * c0) : T(0)) + e2 * w[3];
-                    wn[4] = (lyBh ? -(bH1 * c1) : T(0)) + e2 * w[4];
-                    wn[5] = (kp ? -(bH2 * c2) : T(0)) + e2 * w[5];
-                    if (mode == 0) {
-#pragma unroll
-                        for (int c = 0; c < 6; ++c) wout[go + c * D.cs] = wn[c];
-                    }
-                }
-                const T u[6] = {ux0, uy0, uz0, hx0, hy0, hz0};
-#pragma unroll
-                for (int c = 0; c < 6; ++c) {
-                    T v = (yv[c] + a * w[c]) + b * u[c];
-                    if (mode == 2) v = v + cl * wn[c];
-                    y[go + c * D.cs] = v;
-                }
-            }
-            __syncthreads();
-            // the stage slot of plane kb+t-2 (load t-1) is free: load plane kb-1+(t-1+S)
-            if (tid == 0 && t >= 1 && t - 1 + S < nplanes) {
-                const uint32_t L = lcount + t - 1 + S;
-                issue_plane<T, EM, false, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, nullptr, nullptr,
-                                             x0, y0, kb - 1 + t - 1 + S);
-            }
-        }
-        lcount += nplanes;
-    }
-}
-
-// ---------------------------------------------------------------------------------------
 // K2r: the Newton pair with one point set and register-carried own values
 // ---------------------------------------------------------------------------------------
 // Every thread owns one point of U = [x0-1, x0+BX] x [y0-1, y0+BY] ((BX+2) x (BY+2)) and
@@ -2481,54 +2318,6 @@ static int poly_r_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     return check_cuda("poly_r");
 }
 
-// K2ws launcher (same schedule, maps and buffer protocol as K2)
-template <typename T, int EM>
-static int poly_ws_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
-    constexpr int BX = 32, BY = 8, S = 4;
-    using G = Geo<T, BX, BY>;
-    constexpr int NTHR = ((G::RP + 31) / 32) * 32 + BX * BY;
-    constexpr size_t smem = (size_t)(S * StageL<T, EM, false, G>::SZ + 2 * 3 * 3 * G::RP) * sizeof(T) + 8 * S + 16;
-    const Grid &g = *ka.g;
-    auto kern = pair_ws_kernel<T, EM, BX, BY>;
-    static const int per_sm = resident_per_sm(kern, NTHR, smem);
-    if (per_sm < 1) return fail(PARAEXP_ECUDA, "pair_ws kernel does not fit on an SM");
-    const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
-    const int grid = std::min(sch.units, per_sm * num_sms());
-    auto D = make_dev<T>(g);
-    auto cf = make_coef<T, EM, false>(g, plan.sigma);
-    cudaStream_t s = (cudaStream_t)ka.stream;
-    T *w = (T *)bufs[0], *yy = (T *)bufs[1], *sp = (T *)bufs[2], *sp2 = (T *)bufs[3];
-    CUtensorMap tmW, tmS;
-    int rc;
-    if ((rc = make_map<T>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
-    if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
-    int init = 1;
-    for (const Op &op : plan.ops) {
-        kern<<<grid, NTHR, smem, s>>>(tmW, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a), T(op.b), T(op.e2),
-                                       T(op.c), init, op.kind);
-        ++*ka.launches;
-        if (op.kind == 0) {
-            std::swap(w, sp);
-            std::swap(tmW, tmS);
-        }
-        init = 0;
-    }
-    bufs[0] = yy;
-    bufs[1] = w;
-    bufs[2] = sp;
-    bufs[3] = sp2;
-    return check_cuda("poly ws");
-}
-
-static bool pair_ws_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PARAEXP_PAIR_WS");
-        v = (e && atoi(e) != 0) ? 1 : 0;
-    }
-    return v == 1;
-}
-
 // K2H launcher: the ops from the innermost (last) to the outermost; bufs[0] = b is read by
 // every step, the nest ping-pongs between bufs[1] and bufs[2]; on return bufs[0] = result.
 template <typename T, int EM, int S>
@@ -2639,7 +2428,6 @@ int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
         if constexpr (EM != 2 && !HA && std::is_same<T, double>::value) {
-            if (!ka.et && pair_ws_enabled()) return poly_ws_V<T, EM>(ka, plan, bufs);
             // K2H (nested evaluation, 18 instead of 24 values per pair) unless early
             // termination needs the forward sum
             if (!ka.et && horner_stages() == 2) return poly_horner_V<T, EM, 2>(ka, plan, bufs);
