@@ -39,6 +39,15 @@ static int ensure_ws(Grid &G, int n) {
     return PARAEXP_OK;
 }
 
+// ---- concurrent particular sweeps ------------------------------------------------------------
+// On by default for grids of at most 2^19 cells (64^3: one fused sweep covers ~128 (tile, chunk)
+// units, far fewer than the ~444 resident CTAs); PARAEXP_CONCURRENT=0/1 forces it off/on.
+static bool concurrent_sweeps(const Grid &G) {
+    const char *e = getenv("PARAEXP_CONCURRENT");
+    if (e) return atoi(e) != 0;
+    return (int64_t)G.nx * G.ny * G.nz <= (1 << 19);
+}
+
 // ---- dynamic-schedule counter check ---------------------------------------------------------
 // The fused kernels take their units from a grid-owned monotone counter whose expected value
 // the host tracks (fused.cu Sched).  At points where a call synchronises anyway, verify it;
@@ -960,6 +969,58 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
         return r;
     };
 
+    // Concurrent particular sweeps (small grids): the sub-intervals of this rank's block are
+    // independent leapfrog problems from zero (the parfor of PAPER:358-361).  When one sweep
+    // cannot fill the GPU they run concurrently on side streams, each into its own buffer, and
+    // the Horner chain on `stream` consumes them in order as they complete.
+    const int nb = first >= 1 ? last - first + 1 : 0;
+    const int nstr = std::min(nb, 8);
+    const bool conc = nb >= 2 && nb <= 64 && concurrent_sweeps(G);
+    std::vector<void *> Pc;
+    if (conc) {
+        while ((int)G.conc.size() < nb + nstr) {
+            void *q = nullptr;
+            if ((rc = dev_alloc(&q, sbytes))) return rc;
+            if ((rc = dev_memset_async(q, 0, sbytes, nullptr)) || (rc = dev_sync(nullptr))) return rc;
+            G.conc.push_back(q);
+            G.device_bytes += sbytes;
+        }
+        while ((int)G.streams.size() < nstr) {
+            void *q = nullptr;
+            if ((rc = dev_stream_create(&q))) return rc;
+            G.streams.push_back(q);
+        }
+        while ((int)G.events.size() < nb + 1) {
+            void *q = nullptr;
+            if ((rc = dev_event_create(&q))) return rc;
+            G.events.push_back(q);
+        }
+        Pc.assign(G.conc.begin(), G.conc.begin() + nb);
+        std::vector<void *> scratch(G.conc.begin() + nb, G.conc.begin() + nb + nstr);
+        for (int q = 0; q < nstr; ++q)   // side streams start after the work already on `stream`
+            if ((rc = dev_stream_after(G.streams[q], stream, G.events[nb]))) return rc;
+        for (int q = 0; q < nb; ++q) {
+            const int i = first + q, sq = q % nstr;
+            KernelArgs kq = ka;
+            kq.stream = G.streams[sq];
+            kq.static_sched = true;                        // concurrent launches: no shared counter
+            if ((rc = dev_memset_async(Pc[q], 0, sbytes, kq.stream))) return rc;
+            void *bufs[2] = {Pc[q], scratch[sq]};
+            const size_t qoff = (size_t)B[i - 1] * nsrc * G.esize();
+            if ((rc = k_leapfrog(kq, bufs, B[i] - B[i - 1], (const SrcDev *)G.d_src, nsrc,
+                                 (const char *)G.d_q + qoff))) return rc;
+            if (bufs[0] != Pc[q]) std::swap(Pc[q], scratch[sq]);   // result buffer <-> scratch
+            if ((rc = k_check_finite_async(kq, Pc[q], dflag + i))) return rc;
+            if (cudaEventRecord((cudaEvent_t)G.events[q], (cudaStream_t)kq.stream) != cudaSuccess)
+                return check_cuda("event record");
+            S.leapfrog_steps += B[i] - B[i - 1];
+            S.curl_applications += 2 * (B[i] - B[i - 1]);
+        }
+        // keep the buffer roles for the next call (results may now live in former scratch)
+        for (int q = 0; q < nb; ++q) G.conc[q] = Pc[q];
+        for (int q = 0; q < nstr; ++q) G.conc[nb + q] = scratch[q];
+    }
+
     if (first >= 1) {
         if (first == 1 && has_u0) {
             if ((rc = pack_any(ka, G, e0, h0, W, &host_io))) return rc;
@@ -969,16 +1030,22 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
         for (int i = first; i <= last; ++i) {
             const int64_t M = B[i] - B[i - 1];
             int id = ev.open(0);
-            if ((rc = dev_memset_async(P, 0, sbytes, stream))) return rc;
-            void *bufs[2] = {P, X[0]};
-            const size_t qoff = (size_t)B[i - 1] * nsrc * G.esize();
-            const int id5 = ev.open(5);
-            if ((rc = k_leapfrog(ka, bufs, M, (const SrcDev *)G.d_src, nsrc, (const char *)G.d_q + qoff))) return rc;
-            ev.close(id5);
-            if (bufs[0] != P) std::swap(P, X[0]);
-            S.leapfrog_steps += M;
-            S.curl_applications += 2 * M;
-            if ((rc = k_check_finite_async(ka, P, dflag + i))) return rc;
+            if (conc) {
+                if (cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)G.events[i - first], 0) != cudaSuccess)
+                    return check_cuda("stream wait");
+                P = Pc[i - first];
+            } else {
+                if ((rc = dev_memset_async(P, 0, sbytes, stream))) return rc;
+                void *bufs[2] = {P, X[0]};
+                const size_t qoff = (size_t)B[i - 1] * nsrc * G.esize();
+                const int id5 = ev.open(5);
+                if ((rc = k_leapfrog(ka, bufs, M, (const SrcDev *)G.d_src, nsrc, (const char *)G.d_q + qoff))) return rc;
+                ev.close(id5);
+                if (bufs[0] != P) std::swap(P, X[0]);
+                S.leapfrog_steps += M;
+                S.curl_applications += 2 * M;
+                if ((rc = k_check_finite_async(ka, P, dflag + i))) return rc;
+            }
             ev.close(id);
             id = ev.open(1);
             if (W_valid && (rc = propagate(i))) return rc;

@@ -2072,7 +2072,8 @@ static int leapfrog_fused_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps,
             if (!trm.probe) trm.np = 0;
         }
         kern<<<grid, G::NTHR, Cfg::lf_smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf,
-                                                 (T *)(even ? bufs[1] : bufs[0]), launch_sched(g, sch, grid), sl,
+                                                 (T *)(even ? bufs[1] : bufs[0]),
+                                                 ka.static_sched ? sch : launch_sched(g, sch, grid), sl,
                                                  nsrc ? (const T *)q_dev + m * nsrc : nullptr, trm);
         ++*ka.launches;
     }
@@ -2120,7 +2121,7 @@ static int leapfrog_r_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int
             if (!trm.probe) trm.np = 0;
         }
         kern<<<grid, G::NTHR, smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf, (T *)(even ? bufs[1] : bufs[0]),
-                                          launch_sched(g, sch, grid),
+                                          ka.static_sched ? sch : launch_sched(g, sch, grid),
                                           sl, nsrc ? (const T *)q_dev + m * nsrc : nullptr, trm);
         ++*ka.launches;
     }
@@ -2168,7 +2169,7 @@ static int leapfrog_v_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int
             if (!trm.probe) trm.np = 0;
         }
         kern<<<grid, G::NTHR, smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf, (float *)(even ? bufs[1] : bufs[0]),
-                                          launch_sched(g, sch, grid), sl,
+                                          ka.static_sched ? sch : launch_sched(g, sch, grid), sl,
                                           nsrc ? (const float *)q_dev + m * nsrc : nullptr, trm);
         ++*ka.launches;
     }

@@ -230,6 +230,12 @@ void grid_free_device(Grid &G) {
     dev_free(G.d_q);
     dev_free(G.d_et);
     G.d_et = nullptr;
+    for (void *q : G.conc) dev_free(q);
+    G.conc.clear();
+    for (void *q : G.streams) dev_stream_destroy(q);
+    G.streams.clear();
+    for (void *q : G.events) dev_event_destroy(q);
+    G.events.clear();
     dev_free(G.d_sched);
     G.d_sched = nullptr;
     G.sched_base = 0;

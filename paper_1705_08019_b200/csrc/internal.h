@@ -62,6 +62,9 @@ struct Grid {
     void *d_canon[2] = {nullptr, nullptr};   // canonical-layout staging of host-pointer fields
     std::vector<void *> kry;    // Krylov basis vectors (f3), allocated on first use
     void *d_et = nullptr;       // early-termination norms / flags (f2)
+    std::vector<void *> conc;   // state buffers of concurrently swept sub-intervals
+    std::vector<void *> streams; // their cudaStream_t / cudaEvent_t handles (created on demand)
+    std::vector<void *> events;
     void *d_sched = nullptr;    // monotone unit counter of the fused kernels' dynamic schedule
     unsigned long long sched_base = 0;   // host shadow: value of *d_sched before the next launch
     int64_t d_q_cap = 0;
@@ -107,6 +110,11 @@ int dev_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream);
 int dev_memcpy_d2d_async(void *dst, const void *src, size_t bytes, void *stream);
 int dev_set_device(int device);
 int dev_sync(void *stream);
+int dev_stream_create(void **s);
+void dev_stream_destroy(void *s);
+int dev_event_create(void **e);
+void dev_event_destroy(void *e);
+int dev_stream_after(void *waiter, void *from, void *ev);
 int check_cuda(const char *what);
 
 // early termination of the Newton sum (f2; reading 18): per op the kernels accumulate the
@@ -126,6 +134,7 @@ struct KernelArgs {
     void *stream;
     int64_t *launches;
     const EtDev *et = nullptr;   // per-call early-termination buffers (op/apps set per launch)
+    bool static_sched = false;   // launches that run concurrently with others: no shared counter
 };
 
 // per-step trace outputs of a leapfrog sequence (f1): device pointers at the row of the

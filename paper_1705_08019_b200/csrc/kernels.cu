@@ -66,6 +66,30 @@ int dev_set_device(int device) {
     if (cudaSetDevice(device) != cudaSuccess) return check_cuda("cudaSetDevice");
     return PARAEXP_OK;
 }
+int dev_stream_create(void **s) {
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return check_cuda("stream create");
+    *s = (void *)st;
+    return PARAEXP_OK;
+}
+void dev_stream_destroy(void *s) {
+    if (s) cudaStreamDestroy((cudaStream_t)s);
+}
+int dev_event_create(void **e) {
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return check_cuda("event create");
+    *e = (void *)ev;
+    return PARAEXP_OK;
+}
+void dev_event_destroy(void *e) {
+    if (e) cudaEventDestroy((cudaEvent_t)e);
+}
+// `waiter` waits for the work enqueued on `from` so far (event `ev` is recorded on `from`)
+int dev_stream_after(void *waiter, void *from, void *ev) {
+    if (cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)from) != cudaSuccess) return check_cuda("event record");
+    if (cudaStreamWaitEvent((cudaStream_t)waiter, (cudaEvent_t)ev, 0) != cudaSuccess) return check_cuda("stream wait");
+    return PARAEXP_OK;
+}
 int dev_sync(void *stream) {
     if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return check_cuda("sync");
     return PARAEXP_OK;
