@@ -280,6 +280,9 @@ bool fused_supported(const Grid &g);
 
 int k_leapfrog(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev *src_dev,
                int nsrc, const void *q_dev, const TraceDev *tr) {
+    const bool tracing = tr && (tr->energy || (tr->probe && tr->np > 0));
+    if (ka.g->kernels == PARAEXP_KERNELS_FUSED && !tracing && nsrc <= 16 && small_supported(*ka.g))
+        return k_leapfrog_small(ka, bufs[0], nsteps, nsrc, q_dev);
     if (ka.g->kernels == PARAEXP_KERNELS_FUSED && fused_supported(*ka.g))
         return k_leapfrog_fused(ka, bufs, nsteps, src_dev, nsrc, q_dev, tr);
     return k_leapfrog_unfused(ka, bufs[0], nsteps, src_dev, nsrc, q_dev, tr);
@@ -467,6 +470,18 @@ static int run_plan(const KernelArgs &ka, const Plan &plan, void *bufs[4], parae
         return PARAEXP_OK;
     }
     const int id = ev && plan.s > 0 ? ev->open(6) : -1;
+    if (!plan.early_term && plan.s > 0 && ka.g->kernels == PARAEXP_KERNELS_FUSED && small_supported(*ka.g) &&
+        plan.ops.size() <= 80) {
+        // small grid: every substep of the propagator in one single-CTA launch (small.cu)
+        int rc = k_poly_small(ka, plan, bufs[0]);
+        if (rc) return rc;
+        if (id >= 0) ev->close(id);
+        if (st) {
+            st->a_applications += (int64_t)plan.s * plan.m;
+            st->substeps += plan.s;
+        }
+        return PARAEXP_OK;
+    }
     if (plan.early_term && plan.s > 0) {
         // f2: per substep the op norms and the done flag are reset; the kernels count the
         // A-applications they actually perform (reading 18)

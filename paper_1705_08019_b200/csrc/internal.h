@@ -167,6 +167,10 @@ int k_half_start(const KernelArgs &ka, void *state);
 // return bufs[0] names the result and bufs[1..3] the free buffers.
 int k_poly_substep(const KernelArgs &ka, const Plan &plan, void *bufs[4]);
 int k_poly_substep_unfused(const KernelArgs &ka, const Plan &plan, void *bufs[4]);
+// small grids (small.cu): one CTA, state in shared memory, whole sequences per launch
+bool small_supported(const Grid &g);
+int k_leapfrog_small(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc, const void *q_dev);
+int k_poly_small(const KernelArgs &ka, const Plan &plan, void *state);
 // x <- x + alpha y (state-sized), or over components [c0, c1)
 int k_axpy(const KernelArgs &ka, void *x, const void *y, double alpha);
 int k_axpy_comps(const KernelArgs &ka, void *x, const void *y, double alpha, int c0, int c1);
