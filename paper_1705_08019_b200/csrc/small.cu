@@ -25,7 +25,11 @@ static constexpr int64_t small_max_cells() {
 }
 
 bool small_supported(const Grid &g) {
-    if (getenv("PARAEXP_NO_SMALL")) return false;
+    static const bool off = [] {
+        const char *e = getenv("PARAEXP_NO_SMALL");
+        return e && atoi(e) != 0;
+    }();
+    if (off) return false;
     const int64_t cells = (int64_t)g.nx * g.ny * g.nz;
     return g.dtype == PARAEXP_F64 ? cells <= small_max_cells<double>() : cells <= small_max_cells<float>();
 }
