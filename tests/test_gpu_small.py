@@ -62,7 +62,7 @@ def run_case(mode, n, dtype, expect_small):
     assert_parity((ge, gh), ref, dtype, f"{mode} {n} {dtype} leapfrog")
     assert (st["kernel_launches"] < 10) == expect_small, st
     rho = og.rho_cfl
-    for m, s in ((150, 1), (41, 2), (1, 3)):
+    for m, s in ((150, 1), (40, 2), (1, 3)):
         plan = fit.make_plan("leja", m, s, 20 * og.dt, rho)
         r2 = fit.expmv(og, plan, e, h, dtype=dtype)
         ge, gh, st = lib_expmv(lg, 20 * og.dt, e, h, m=m, s=s, rho=rho)
