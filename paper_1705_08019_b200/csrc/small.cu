@@ -6,8 +6,9 @@
 // CTA keeps the state in shared memory and runs a whole leapfrog sequence (rows a2/a3) or a whole
 // polynomial propagator p(X)^s (row a6) in a single launch, with __syncthreads between the curl
 // half-sweeps.  Arithmetic, operation order and liveness are those of the unfused kernels in
-// kernels.cu (the same curl helpers on a compact view of the layout), so results match them and
-// the oracle at the north_star tolerances.  Independent problems (ParaExp's sub-interval sweeps)
+// kernels.cu (the curl helpers' operand order, on a compact copy of the layout), so results match
+// them and the oracle at the north_star tolerances.  Per-cell indices, liveness and neighbour flags
+// are computed once per launch, so the time loops do no index arithmetic.  Independent problems (ParaExp's sub-interval sweeps)
 // run as independent single-CTA launches on separate streams, i.e. concurrently on separate SMs.
 #include <cuda_runtime.h>
 
@@ -39,69 +40,150 @@ struct SmallSrc {
     int c[16], i[16], j[16], k[16];
 };
 
-// compact (shared-memory) view of the stored box: px = nx, plane = nx*ny, cs = cells
+constexpr int kQChunk = 256;   // leapfrog steps of source values staged in shared memory at a time
+
+// Per owned cell, computed once per launch: the compact index x, the padded (global) index g
+// (per-edge / per-face coefficient arrays) and a flag word -- bits 0-5: the -1/+1 neighbours
+// exist (i>0, j>0, k>0, i+1<nx, j+1<ny, k+1<nz), bits 6-8: e_c live, bits 9-11: h_c live,
+// bits 12-31: k (z-table coefficients).  The time loops then do no index arithmetic.
+struct SmallCell {
+    int x, g;
+    unsigned f;
+};
+
 template <typename T>
-__device__ __forceinline__ Dev<T> compact(const Dev<T> &D) {
-    Dev<T> C = D;
-    C.px = D.nx;
-    C.plane = (int64_t)D.nx * D.ny;
-    C.cs = C.plane * D.nz;
-    return C;
+__device__ __forceinline__ SmallCell small_cell(const Dev<T> &D, int x) {
+    SmallCell c;
+    c.x = x;
+    const int i = x % D.nx, j = (x / D.nx) % D.ny, k = x / (D.nx * D.ny);
+    c.g = (int)D.idx(i, j, k);
+    c.f = (unsigned)(i > 0) | ((unsigned)(j > 0) << 1) | ((unsigned)(k > 0) << 2) |
+          ((unsigned)(i + 1 < D.nx) << 3) | ((unsigned)(j + 1 < D.ny) << 4) | ((unsigned)(k + 1 < D.nz) << 5);
+    for (int q = 0; q < 3; ++q) {
+        c.f |= (unsigned)D.e_live(q, i, j, k) << (6 + q);
+        c.f |= (unsigned)D.h_live(q, i, j, k) << (9 + q);
+    }
+    c.f |= (unsigned)k << 12;
+    return c;
 }
 
-// ---------------------------------------------------------------------------------------
-// leapfrog: nsteps steps on the state (device layout) in place
-// ---------------------------------------------------------------------------------------
-template <typename T, int EM, bool HA>
-__global__ void __launch_bounds__(kSmallThreads, 1) leapfrog_small_kernel(Dev<T> D, Coef<T, EM, HA> cf,
-                                                                          T *__restrict__ st, int64_t nsteps,
-                                                                          SmallSrc src, const T *__restrict__ q) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *S = reinterpret_cast<T *>(smem_raw);
-    const Dev<T> C = compact(D);
-    const int cells = (int)C.cs;
+// (C e) and (C^T h) at a cell of the compact layout (px = nx, plane = nx*ny) from its flag word;
+// the same operands and operation order as curl_at / curlT_at (kernels_common.cuh).
+template <typename T>
+__device__ __forceinline__ void curl_f(const T *ex, const T *ey, const T *ez, int x, unsigned f, int px,
+                                       int plane, T &c0, T &c1, T &c2) {
+    const T ex0 = ex[x], ey0 = ey[x], ez0 = ez[x];
+    const T ez_jp = (f & 16u) ? ez[x + px] : T(0);
+    const T ex_jp = (f & 16u) ? ex[x + px] : T(0);
+    const T ey_kp = (f & 32u) ? ey[x + plane] : T(0);
+    const T ex_kp = (f & 32u) ? ex[x + plane] : T(0);
+    const T ez_ip = (f & 8u) ? ez[x + 1] : T(0);
+    const T ey_ip = (f & 8u) ? ey[x + 1] : T(0);
+    c0 = ((ey0 + ez_jp) - ey_kp) - ez0;
+    c1 = ((ez0 + ex_kp) - ez_ip) - ex0;
+    c2 = ((ex0 + ey_ip) - ex_jp) - ey0;
+}
+
+template <typename T>
+__device__ __forceinline__ void curlT_f(const T *hx, const T *hy, const T *hz, int x, unsigned f, int px,
+                                        int plane, T &c0, T &c1, T &c2) {
+    const T hx0 = hx[x], hy0 = hy[x], hz0 = hz[x];
+    const T hz_jm = (f & 2u) ? hz[x - px] : T(0);
+    const T hx_jm = (f & 2u) ? hx[x - px] : T(0);
+    const T hy_km = (f & 4u) ? hy[x - plane] : T(0);
+    const T hx_km = (f & 4u) ? hx[x - plane] : T(0);
+    const T hz_im = (f & 1u) ? hz[x - 1] : T(0);
+    const T hy_im = (f & 1u) ? hy[x - 1] : T(0);
+    c0 = ((hz0 - hz_jm) - hy0) + hy_km;
+    c1 = ((hx0 - hx_km) - hz0) + hz_im;
+    c2 = ((hy0 - hy_im) - hx0) + hx_jm;
+}
+
+template <typename T>
+__device__ __forceinline__ void load_state(const Dev<T> &D, const T *st, T *S, int cells) {
     for (int c = 0; c < 6; ++c)
         for (int x = threadIdx.x; x < cells; x += blockDim.x) {
             const int i = x % D.nx, j = (x / D.nx) % D.ny, k = x / (D.nx * D.ny);
             S[c * cells + x] = st[c * D.cs + D.idx(i, j, k)];
         }
-    __syncthreads();
-    T *ex = S, *ey = S + cells, *ez = S + 2 * cells, *hx = S + 3 * cells, *hy = S + 4 * cells, *hz = S + 5 * cells;
-    for (int64_t m = 0; m < nsteps; ++m) {
-        // e <- e + bE .* (C^T h)
-        for (int x = threadIdx.x; x < cells; x += blockDim.x) {
-            const int i = x % D.nx, j = (x / D.nx) % D.ny, k = x / (D.nx * D.ny);
-            const int64_t g = D.idx(i, j, k);
-            T c0, c1, c2;
-            curlT_at(C, hx, hy, hz, i, j, k, (int64_t)x, c0, c1, c2);
-            if (D.e_live(0, i, j, k)) ex[x] = ex[x] + cf.bE(0, k, g) * c0;
-            if (D.e_live(1, i, j, k)) ey[x] = ey[x] + cf.bE(1, k, g) * c1;
-            if (D.e_live(2, i, j, k)) ez[x] = ez[x] + cf.bE(2, k, g) * c2;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0)       // e_s <- e_s - q[m][s], sequentially in s
-            for (int r = 0; r < src.n; ++r) {
-                const int x = src.i[r] + D.nx * (src.j[r] + D.ny * src.k[r]);
-                S[src.c[r] * cells + x] = S[src.c[r] * cells + x] - q[m * src.n + r];
-            }
-        __syncthreads();
-        // h <- h - bH .* (C e)
-        for (int x = threadIdx.x; x < cells; x += blockDim.x) {
-            const int i = x % D.nx, j = (x / D.nx) % D.ny, k = x / (D.nx * D.ny);
-            const int64_t g = D.idx(i, j, k);
-            T c0, c1, c2;
-            curl_at(C, ex, ey, ez, i, j, k, (int64_t)x, c0, c1, c2);
-            if (D.h_live(0, i, j, k)) hx[x] = hx[x] - (T(1) * cf.bH(0, g)) * c0;
-            if (D.h_live(1, i, j, k)) hy[x] = hy[x] - (T(1) * cf.bH(1, g)) * c1;
-            if (D.h_live(2, i, j, k)) hz[x] = hz[x] - (T(1) * cf.bH(2, g)) * c2;
-        }
-        __syncthreads();
-    }
+}
+
+template <typename T>
+__device__ __forceinline__ void store_state(const Dev<T> &D, T *st, const T *S, int cells) {
     for (int c = 0; c < 6; ++c)
         for (int x = threadIdx.x; x < cells; x += blockDim.x) {
             const int i = x % D.nx, j = (x / D.nx) % D.ny, k = x / (D.nx * D.ny);
             st[c * D.cs + D.idx(i, j, k)] = S[c * cells + x];
         }
+}
+
+// ---------------------------------------------------------------------------------------
+// leapfrog: nsteps steps on the state (device layout) in place.  Thread t owns cells
+// t, t + 1024, ... (R of them).  The source values of kQChunk steps are staged in shared memory;
+// the owner of a source's cell subtracts it right after its own e-update (e_s <- e_s - q[m][s],
+// in s order for sources on the same edge), so a step takes two barriers.
+// ---------------------------------------------------------------------------------------
+template <typename T, int EM, bool HA, int R>
+__global__ void __launch_bounds__(kSmallThreads, 1) leapfrog_small_kernel(Dev<T> D, Coef<T, EM, HA> cf,
+                                                                          T *__restrict__ st, int64_t nsteps,
+                                                                          SmallSrc src, const T *__restrict__ q) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *S = reinterpret_cast<T *>(smem_raw);
+    const int cells = D.nx * D.ny * D.nz, px = D.nx, plane = D.nx * D.ny;
+    T *Q = S + 6 * cells;
+    load_state(D, st, S, cells);
+    SmallCell cl[R];
+    unsigned smask[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int x = threadIdx.x + r * kSmallThreads;
+        cl[r] = small_cell(D, x < cells ? x : 0);
+        cl[r].x = x;
+        smask[r] = 0;
+        for (int s = 0; s < src.n; ++s)
+            if (src.i[s] + D.nx * (src.j[s] + D.ny * src.k[s]) == x) smask[r] |= 1u << s;
+    }
+    T *ex = S, *ey = S + cells, *ez = S + 2 * cells, *hx = S + 3 * cells, *hy = S + 4 * cells, *hz = S + 5 * cells;
+    for (int64_t m = 0; m < nsteps; ++m) {
+        const int mq = (int)(m % kQChunk);
+        if (src.n > 0 && mq == 0) {
+            const int64_t n = min((int64_t)kQChunk, nsteps - m) * src.n;
+            for (int t = threadIdx.x; t < n; t += blockDim.x) Q[t] = q[m * src.n + t];
+        }
+        __syncthreads();                    // h (and Q) complete
+        // e <- e + bE .* (C^T h); then the owned sources
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int x = cl[r].x;
+            if (x >= cells) continue;
+            const unsigned f = cl[r].f;
+            const int k = (int)(f >> 12);
+            T c0, c1, c2;
+            curlT_f(hx, hy, hz, x, f, px, plane, c0, c1, c2);
+            if (f & 64u) ex[x] = ex[x] + cf.bE(0, k, cl[r].g) * c0;
+            if (f & 128u) ey[x] = ey[x] + cf.bE(1, k, cl[r].g) * c1;
+            if (f & 256u) ez[x] = ez[x] + cf.bE(2, k, cl[r].g) * c2;
+            for (unsigned sm = smask[r]; sm; sm &= sm - 1) {
+                const int s = __ffs(sm) - 1;
+                S[src.c[s] * cells + x] = S[src.c[s] * cells + x] - Q[mq * src.n + s];
+            }
+        }
+        __syncthreads();
+        // h <- h - bH .* (C e)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int x = cl[r].x;
+            if (x >= cells) continue;
+            const unsigned f = cl[r].f;
+            T c0, c1, c2;
+            curl_f(ex, ey, ez, x, f, px, plane, c0, c1, c2);
+            if (f & 512u) hx[x] = hx[x] - (T(1) * cf.bH(0, cl[r].g)) * c0;
+            if (f & 1024u) hy[x] = hy[x] - (T(1) * cf.bH(1, cl[r].g)) * c1;
+            if (f & 2048u) hz[x] = hz[x] - (T(1) * cf.bH(2, cl[r].g)) * c2;
+        }
+    }
+    __syncthreads();
+    store_state(D, st, S, cells);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -113,6 +195,22 @@ struct SmallOps {
     double a[kSmallMaxOps], b[kSmallMaxOps], e2[kSmallMaxOps], c[kSmallMaxOps];
 };
 
+// out = X in at an owned cell (e rows: bE C^T h, h rows: -bH C e; dead DOFs 0)
+template <typename T, int EM, bool HA>
+__device__ __forceinline__ void small_applyX(const Coef<T, EM, HA> &cf, const T *in, int cells, const SmallCell &c,
+                                             int px, int plane, T o[6]) {
+    const int x = c.x, k = (int)(c.f >> 12);
+    T a0, a1, a2, b0, b1, b2;
+    curlT_f(in + 3 * cells, in + 4 * cells, in + 5 * cells, x, c.f, px, plane, a0, a1, a2);
+    curl_f(in, in + cells, in + 2 * cells, x, c.f, px, plane, b0, b1, b2);
+    o[0] = (c.f & 64u) ? cf.bE(0, k, c.g) * a0 : T(0);
+    o[1] = (c.f & 128u) ? cf.bE(1, k, c.g) * a1 : T(0);
+    o[2] = (c.f & 256u) ? cf.bE(2, k, c.g) * a2 : T(0);
+    o[3] = (c.f & 512u) ? -(cf.bH(0, c.g) * b0) : T(0);
+    o[4] = (c.f & 1024u) ? -(cf.bH(1, c.g) * b1) : T(0);
+    o[5] = (c.f & 2048u) ? -(cf.bH(2, c.g) * b2) : T(0);
+}
+
 // y (the Newton sum) stays in registers: thread t owns cells t, t + 1024, ... (R of them)
 template <typename T, int EM, bool HA, int R>
 __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, Coef<T, EM, HA> cf,
@@ -120,28 +218,17 @@ __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, 
                                                                       const __grid_constant__ SmallOps ops) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *W = reinterpret_cast<T *>(smem_raw);
-    const Dev<T> C = compact(D);
-    const int cells = (int)C.cs;
+    const int cells = D.nx * D.ny * D.nz, px = D.nx, plane = D.nx * D.ny;
     T *U = W + 6 * cells;
-    for (int c = 0; c < 6; ++c)
-        for (int x = threadIdx.x; x < cells; x += blockDim.x) {
-            const int i = x % D.nx, j = (x / D.nx) % D.ny, k = x / (D.nx * D.ny);
-            W[c * cells + x] = st[c * D.cs + D.idx(i, j, k)];
-        }
+    load_state(D, st, W, cells);
+    SmallCell cl[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int x = threadIdx.x + r * kSmallThreads;
+        cl[r] = small_cell(D, x < cells ? x : 0);
+        cl[r].x = x;
+    }
     __syncthreads();
-    auto applyX = [&](const T *in, T *out, int x) {       // out(x) = X in at cell x
-        const int i = x % D.nx, j = (x / D.nx) % D.ny, k = x / (D.nx * D.ny);
-        const int64_t g = D.idx(i, j, k);
-        T a0, a1, a2, b0, b1, b2;
-        curlT_at(C, in + 3 * cells, in + 4 * cells, in + 5 * cells, i, j, k, (int64_t)x, a0, a1, a2);
-        curl_at(C, in, in + cells, in + 2 * cells, i, j, k, (int64_t)x, b0, b1, b2);
-        out[x] = D.e_live(0, i, j, k) ? cf.bE(0, k, g) * a0 : T(0);
-        out[cells + x] = D.e_live(1, i, j, k) ? cf.bE(1, k, g) * a1 : T(0);
-        out[2 * cells + x] = D.e_live(2, i, j, k) ? cf.bE(2, k, g) * a2 : T(0);
-        out[3 * cells + x] = D.h_live(0, i, j, k) ? -(cf.bH(0, g) * b0) : T(0);
-        out[4 * cells + x] = D.h_live(1, i, j, k) ? -(cf.bH(1, g) * b1) : T(0);
-        out[5 * cells + x] = D.h_live(2, i, j, k) ? -(cf.bH(2, g) * b2) : T(0);
-    };
     T y[R][6];
     for (int q = 0; q < s; ++q) {
 #pragma unroll
@@ -149,33 +236,28 @@ __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, 
 #pragma unroll
             for (int c = 0; c < 6; ++c) y[r][c] = T(0);
         for (int o = 0; o < ops.n; ++o) {
-            const T a = (T)ops.a[o], b = (T)ops.b[o], e2 = (T)ops.e2[o], cl = (T)ops.c[o];
+            const T a = (T)ops.a[o], b = (T)ops.b[o], e2 = (T)ops.e2[o], cc = (T)ops.c[o];
             const int kind = ops.kind[o];
-            for (int x = threadIdx.x; x < cells; x += blockDim.x) applyX(W, U, x);   // U = X W
+#pragma unroll
+            for (int r = 0; r < R; ++r) {                 // U = X W
+                if (cl[r].x >= cells) continue;
+                T u[6];
+                small_applyX(cf, W, cells, cl[r], px, plane, u);
+#pragma unroll
+                for (int c = 0; c < 6; ++c) U[c * cells + cl[r].x] = u[c];
+            }
             __syncthreads();
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const int x = threadIdx.x + r * kSmallThreads;
+                const int x = cl[r].x;
                 if (x >= cells) continue;
                 T xu[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
-                if (kind != 1) {                          // X U at the own cell (U neighbours)
-                    const int i = x % D.nx, j = (x / D.nx) % D.ny, k = x / (D.nx * D.ny);
-                    const int64_t g = D.idx(i, j, k);
-                    T a0, a1, a2, b0, b1, b2;
-                    curlT_at(C, U + 3 * cells, U + 4 * cells, U + 5 * cells, i, j, k, (int64_t)x, a0, a1, a2);
-                    curl_at(C, U, U + cells, U + 2 * cells, i, j, k, (int64_t)x, b0, b1, b2);
-                    xu[0] = D.e_live(0, i, j, k) ? cf.bE(0, k, g) * a0 : T(0);
-                    xu[1] = D.e_live(1, i, j, k) ? cf.bE(1, k, g) * a1 : T(0);
-                    xu[2] = D.e_live(2, i, j, k) ? cf.bE(2, k, g) * a2 : T(0);
-                    xu[3] = D.h_live(0, i, j, k) ? -(cf.bH(0, g) * b0) : T(0);
-                    xu[4] = D.h_live(1, i, j, k) ? -(cf.bH(1, g) * b1) : T(0);
-                    xu[5] = D.h_live(2, i, j, k) ? -(cf.bH(2, g) * b2) : T(0);
-                }
+                if (kind != 1) small_applyX(cf, U, cells, cl[r], px, plane, xu);   // X U (U neighbours)
 #pragma unroll
                 for (int c = 0; c < 6; ++c) {
                     const T wv = W[c * cells + x], uv = U[c * cells + x];
                     T yn = (y[r][c] + a * wv) + b * uv;
-                    if (kind == 2) yn = yn + cl * (xu[c] + e2 * wv);
+                    if (kind == 2) yn = yn + cc * (xu[c] + e2 * wv);
                     y[r][c] = yn;
                     if (kind == 0) W[c * cells + x] = xu[c] + e2 * wv;   // own cell only: safe in place
                 }
@@ -185,18 +267,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, 
         // b <- y (the next substep's start vector)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int x = threadIdx.x + r * kSmallThreads;
+            const int x = cl[r].x;
             if (x >= cells) continue;
 #pragma unroll
             for (int c = 0; c < 6; ++c) W[c * cells + x] = y[r][c];
         }
         __syncthreads();
     }
-    for (int c = 0; c < 6; ++c)
-        for (int x = threadIdx.x; x < cells; x += blockDim.x) {
-            const int i = x % D.nx, j = (x / D.nx) % D.ny, k = x / (D.nx * D.ny);
-            st[c * D.cs + D.idx(i, j, k)] = W[c * cells + x];
-        }
+    store_state(D, st, W, cells);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -218,8 +296,9 @@ int k_leapfrog_small(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
-        const size_t smem = (size_t)6 * g.nx * g.ny * g.nz * sizeof(T);
-        auto kern = leapfrog_small_kernel<T, EM, HA>;
+        constexpr int R = (int)(small_max_cells<T>() / kSmallThreads);
+        const size_t smem = ((size_t)6 * g.nx * g.ny * g.nz + (size_t)kQChunk * nsrc) * sizeof(T);
+        auto kern = leapfrog_small_kernel<T, EM, HA, R>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<1, kSmallThreads, smem, (cudaStream_t)ka.stream>>>(make_dev<T>(g), make_coef<T, EM, HA>(g, 1.0),
                                                                    (T *)state, nsteps, sl, (const T *)q_dev);
