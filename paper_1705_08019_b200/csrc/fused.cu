@@ -68,6 +68,39 @@ __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+
+// Programmatic dependent launch (PDL): the fused kernels are launched with programmatic stream
+// serialisation, so a kernel's launch and CTA setup overlap the tail of the previous one; every
+// fused kernel first waits for its predecessor grid to complete (griddepcontrol.wait, which also
+// makes that grid's memory visible) before touching global memory, so semantics are unchanged.
+__device__ __forceinline__ void pdl_sync() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+static bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("PARAEXP_PDL");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ---------------------------------------------------------------------------------------
 // geometry
 // ---------------------------------------------------------------------------------------
@@ -199,6 +232,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ out,
     Sched sch, SrcList src, const T *__restrict__ q, const __grid_constant__ TraceDev tr) {
+    pdl_sync();
     using G = Geo<T, BX, BY>;
     using SL = StageL<T, EM, HA, G>;
     constexpr int NR = ONEBAR ? 3 : 2;
@@ -384,6 +418,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ out,
     Sched sch, SrcList src, const T *__restrict__ q, const __grid_constant__ TraceDev tr) {
+    pdl_sync();
     using G = Geo<T, BX, BY>;
     using SL = StageL<T, EM, HA, G>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -581,6 +616,7 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<float> D, Coef<float, EM, HA> cf, float *__restrict__ out,
     Sched sch, SrcList src, const float *__restrict__ q, const __grid_constant__ TraceDev tr) {
+    pdl_sync();
     using G = GeoV<BY>;
     using SL = StageL<float, EM, HA, G>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -819,6 +855,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
     T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
+    pdl_sync();
     using G = Geo<T, BX, BY>;
     if (et.norms && et_skip(et)) {                        // early termination (f2)
         // a skipped launch still advances the dynamic-schedule counter by units + gridDim,
@@ -1098,6 +1135,7 @@ template <typename T, int EM, int BX, int BY, int S>
 __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 2) horner_fused_kernel(
     const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_b, Dev<T> D,
     Coef<T, EM, false> cf, T *__restrict__ rout, Sched sch, T a, T beta, T e2, T sc, int mode) {
+    pdl_sync();
     using G = Geo<T, BX, BY>;
     using SH = StageH<T, BX, BY>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1307,6 +1345,7 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
     T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
+    pdl_sync();
     using G = GeoW<T, BY>;
     using V2 = typename Vec2<T>::type;
     using SL = StageL<T, EM, HA, G>;
@@ -1650,6 +1689,7 @@ __global__ void __launch_bounds__(GeoU<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3)
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
     const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
     T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode) {
+    pdl_sync();
     using G = Geo<T, BX, BY>;
     using U = GeoU<T, BX, BY>;
     using SL = StageL<T, EM, HA, G>;
@@ -2071,7 +2111,7 @@ static int leapfrog_fused_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps,
             trm.probe = tr->probe ? tr->probe + m * tr->np : nullptr;
             if (!trm.probe) trm.np = 0;
         }
-        kern<<<grid, G::NTHR, Cfg::lf_smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf,
+        launch_k(kern, grid, G::NTHR, Cfg::lf_smem, s, even ? tmA : tmB, tmE, tmH, D, cf,
                                                  (T *)(even ? bufs[1] : bufs[0]),
                                                  ka.static_sched ? sch : launch_sched(g, sch, grid), sl,
                                                  nsrc ? (const T *)q_dev + m * nsrc : nullptr, trm);
@@ -2120,7 +2160,7 @@ static int leapfrog_r_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int
             trm.probe = tr->probe ? tr->probe + m * tr->np : nullptr;
             if (!trm.probe) trm.np = 0;
         }
-        kern<<<grid, G::NTHR, smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf, (T *)(even ? bufs[1] : bufs[0]),
+        launch_k(kern, grid, G::NTHR, smem, s, even ? tmA : tmB, tmE, tmH, D, cf, (T *)(even ? bufs[1] : bufs[0]),
                                           ka.static_sched ? sch : launch_sched(g, sch, grid),
                                           sl, nsrc ? (const T *)q_dev + m * nsrc : nullptr, trm);
         ++*ka.launches;
@@ -2168,7 +2208,7 @@ static int leapfrog_v_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int
             trm.probe = tr->probe ? tr->probe + m * tr->np : nullptr;
             if (!trm.probe) trm.np = 0;
         }
-        kern<<<grid, G::NTHR, smem, s>>>(even ? tmA : tmB, tmE, tmH, D, cf, (float *)(even ? bufs[1] : bufs[0]),
+        launch_k(kern, grid, G::NTHR, smem, s, even ? tmA : tmB, tmE, tmH, D, cf, (float *)(even ? bufs[1] : bufs[0]),
                                           ka.static_sched ? sch : launch_sched(g, sch, grid), sl,
                                           nsrc ? (const float *)q_dev + m * nsrc : nullptr, trm);
         ++*ka.launches;
@@ -2252,7 +2292,7 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     for (const Op &op : plan.ops) {
         et.op = opi++;
         et.apps = op.kind == 1 ? 1 : 2;
-        kern<<<grid, G::NTHR, Cfg::pair_smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a), T(op.b),
+        launch_k(kern, grid, G::NTHR, Cfg::pair_smem, s, tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a), T(op.b),
                                                    T(op.e2), T(op.c), init, op.kind, et);
         ++*ka.launches;
         if (op.kind == 0) {
@@ -2303,7 +2343,7 @@ static int poly_r_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
     int init = 1;
     for (const Op &op : plan.ops) {
-        kern<<<grid, U::NTHR, smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a), T(op.b), T(op.e2), T(op.c),
+        launch_k(kern, grid, U::NTHR, smem, s, tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a), T(op.b), T(op.e2), T(op.c),
                                           init, op.kind);
         ++*ka.launches;
         if (op.kind == 0) {
@@ -2349,7 +2389,7 @@ static int poly_horner_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
         const Op &op = plan.ops[q];
         const T sc = (T)(q == K - 1 ? op.c : 1.0);
         const int mode = op.kind == 1 ? 1 : 0;
-        kern<<<grid, G::NTHR, smem, s>>>(*in, tmB, D, cf, (T *)out, launch_sched(g, sch, grid), T(op.a), T(op.b),
+        launch_k(kern, grid, G::NTHR, smem, s, *in, tmB, D, cf, (T *)out, launch_sched(g, sch, grid), T(op.a), T(op.b),
                                           T(op.e2), sc, mode);
         ++*ka.launches;
         in = out == r1 ? &tm1 : &tm2;
@@ -2407,7 +2447,7 @@ static int poly_v_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     for (const Op &op : plan.ops) {
         et.op = opi++;
         et.apps = op.kind == 1 ? 1 : 2;
-        kern<<<grid, G::NTHR, smem, s>>>(tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), (T)op.a,
+        launch_k(kern, grid, G::NTHR, smem, s, tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), (T)op.a,
                                           (T)op.b, (T)op.e2, (T)op.c, init, op.kind, et);
         ++*ka.launches;
         if (op.kind == 0) {
