@@ -1990,9 +1990,12 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
     const int cap = std::max(8, (int)(4.0 * resident / std::max(1, s.tiles_x)));
     for (int ch = 1; ch <= g.nz; ++ch) {
         const int nch = (g.nz + ch - 1) / ch;
-        if (ch < std::min(g.nz, 8) && nch > 1) continue;
-        if (ch > cap && ch > 8) continue;
         const double units = (double)s.ntiles * nch;
+        // chunks below 8 planes only while every unit still gets its own CTA (mid-size,
+        // L2-resident grids, where a unit's time is latency: measured at 64^3 fp64 chunk 4
+        // 10.3 us vs chunk 8 12.3 us per leapfrog step, 32^3 chunk 1 6.2 vs 12.3 us)
+        if (ch < std::min(g.nz, 8) && nch > 1 && units > resident) continue;
+        if (ch > cap && ch > 8) continue;
         const double waves = units / resident;
         const double eff_waves = std::ceil(waves);
         // cost ~ rounds * (chunk + 2 halo planes)
