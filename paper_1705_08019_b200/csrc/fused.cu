@@ -2027,6 +2027,7 @@ static bool dynamic_sched() {
 static Sched launch_sched(const Grid &g, Sched sch, int grid) {
     Grid &G = const_cast<Grid &>(g);
     if (!dynamic_sched() || !G.d_sched) return sch;
+    if (grid >= sch.units) return sch;   // one wave: unit = blockIdx.x, no counter round trips
     sch.ctr = (unsigned long long *)G.d_sched;
     sch.base = G.sched_base;
     G.sched_base += (unsigned long long)sch.units + (unsigned long long)grid;
