@@ -86,6 +86,25 @@ static bool pdl_enabled() {
     return on;
 }
 
+// Grid-wide barrier of a cooperative launch (all CTAs co-resident): the w' stores of every CTA
+// (generic proxy) are made visible to the TMA loads (async proxy) of the next op.
+__device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned target) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        unsigned v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v >= target) break;
+            __nanosleep(32);
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
+}
+
 template <typename... KArgs, typename... Args>
 static void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args &&...args) {
     cudaLaunchConfig_t cfg = {};
@@ -98,6 +117,22 @@ static void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, c
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// cooperative launch (co-residency of the whole grid guaranteed; used with grid_barrier)
+template <typename... KArgs, typename... Args>
+static void launch_coop(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -850,11 +885,13 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
 // tile's w'(k) and y(k).  Ring depth 2 (two barriers per plane) or 3 (ONEBAR).
 // min 2 CTAs/SM: the measured K2 rate depends on two resident CTAs per SM (a register
 // growth to > 102 per thread halves the occupancy: 376 vs 288 us per A-application)
-template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
+template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR, bool MULTI = false>
 __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) pair_fused_kernel(
-    const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
-    const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
-    T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
+    const __grid_constant__ CUtensorMap tm_state_p, const __grid_constant__ CUtensorMap tm_cE,
+    const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout_p,
+    T *__restrict__ y, Sched sch, T a_p, T b_p, T e2_p, T cl_p, int init_p, int mode_p, EtDev et,
+    const __grid_constant__ CUtensorMap tm_state2, T *__restrict__ wout2, const Op *__restrict__ ops, int nops,
+    unsigned *gbar) {
     pdl_sync();
     using G = Geo<T, BX, BY>;
     if (et.norms && et_skip(et)) {                        // early termination (f2)
@@ -893,6 +930,15 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
     }
     __syncthreads();
     uint32_t lcount = 0;
+    // MULTI: every op of the substep in one (cooperative, one-wave) launch, a grid barrier
+    // between ops; w ping-pongs between the two buffers/maps after each kind-0 op
+    bool flip = false;
+    for (int o = 0; o < (MULTI ? nops : 1); ++o) {
+    const T a = MULTI ? T(ops[o].a) : a_p, b = MULTI ? T(ops[o].b) : b_p;
+    const T e2 = MULTI ? T(ops[o].e2) : e2_p, cl = MULTI ? T(ops[o].c) : cl_p;
+    const int mode = MULTI ? ops[o].kind : mode_p, init = MULTI ? (o == 0 ? init_p : 0) : init_p;
+    const CUtensorMap *tm_state = (MULTI && flip) ? &tm_state2 : &tm_state_p;
+    T *__restrict__ wout = (MULTI && flip) ? wout2 : wout_p;
     for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
         const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
@@ -914,7 +960,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
         if (tid == 0)
             for (int p = 0; p < min(S, nplanes); ++p) {
                 const uint32_t L = lcount + p;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], tm_state, &tm_cE,
                                           &tm_cH, x0, y0, kb - 1 + p);
             }
         for (int p = 0; p + 1 < nplanes; ++p) {
@@ -995,7 +1041,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
             __syncthreads();
             if (ONEBAR && tid == 0 && p >= 1 && p - 1 + S < nplanes) {
                 const uint32_t L = lcount + p - 1 + S;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], tm_state, &tm_cE,
                                           &tm_cH, x0, y0, kb - 1 + p - 1 + S);
             }
             if (doB) {
@@ -1096,13 +1142,18 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
                 __syncthreads();
                 if (tid == 0 && p + S < nplanes) {
                     const uint32_t L = lcount + p + S;
-                    issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                    issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], tm_state, &tm_cE,
                                               &tm_cH, x0, y0, kb - 1 + p + S);
                 }
             }
         }
         if (ONEBAR) __syncthreads();
         lcount += nplanes;
+    }
+    if (MULTI) {
+        if (mode == 0) flip = !flip;
+        if (o + 1 < nops) grid_barrier(gbar, (unsigned)(o + 1) * gridDim.x);
+    }
     }
     if (et.norms) {
         const double ds = block_sum(dacc);
@@ -2267,6 +2318,15 @@ int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const 
     });
 }
 
+constexpr int kMaxMultiOps = 256;
+static bool multi_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("PARAEXP_MULTI");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 template <typename T, int EM, bool HA, int S, bool ONEBAR>
 static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     constexpr int BX = 32, BY = 8;
@@ -2292,12 +2352,36 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     int init = 1;
     EtDev et;
     if (ka.et) et = *ka.et;
+    const int nops = (int)plan.ops.size();
+    if (multi_enabled() && !ka.et && nops >= 2 && nops <= kMaxMultiOps && grid >= sch.units) {
+        // one wave: the whole substep in ONE cooperative launch (grid barrier between ops)
+        auto kernM = pair_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR, true>;
+        static const int per_smM = resident_per_sm(kernM, G::NTHR, Cfg::pair_smem);
+        if (per_smM >= per_sm) {
+            Grid &GG = const_cast<Grid &>(g);
+            if (!GG.d_ops && (rc = dev_alloc(&GG.d_ops, kMaxMultiOps * sizeof(Op)))) return rc;
+            cudaMemcpyAsync(GG.d_ops, plan.ops.data(), nops * sizeof(Op), cudaMemcpyHostToDevice, s);
+            unsigned *gbar = (unsigned *)((char *)GG.d_sched + 64);
+            cudaMemsetAsync(gbar, 0, sizeof(unsigned), s);
+            launch_coop(kernM, grid, G::NTHR, Cfg::pair_smem, s, tmW, tmE, tmH, D, cf, sp, yy, sch, T(0), T(0),
+                        T(0), T(0), 1, 0, et, tmS, w, (const Op *)GG.d_ops, nops, gbar);
+            ++*ka.launches;
+            for (const Op &op : plan.ops)
+                if (op.kind == 0) std::swap(w, sp);
+            bufs[0] = yy;
+            bufs[1] = w;
+            bufs[2] = sp;
+            bufs[3] = sp2;
+            return check_cuda("poly fused multi");
+        }
+    }
     int opi = 0;
     for (const Op &op : plan.ops) {
         et.op = opi++;
         et.apps = op.kind == 1 ? 1 : 2;
         launch_k(kern, grid, G::NTHR, Cfg::pair_smem, s, tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a), T(op.b),
-                                                   T(op.e2), T(op.c), init, op.kind, et);
+                                                   T(op.e2), T(op.c), init, op.kind, et, tmW, sp, (const Op *)nullptr, 0,
+                                                   (unsigned *)nullptr);
         ++*ka.launches;
         if (op.kind == 0) {
             std::swap(w, sp);

@@ -238,6 +238,8 @@ void grid_free_device(Grid &G) {
     G.events.clear();
     dev_free(G.d_sched);
     G.d_sched = nullptr;
+    dev_free(G.d_ops);
+    G.d_ops = nullptr;
     G.sched_base = 0;
     for (void *q : G.kry) dev_free(q);
     G.kry.clear();
