@@ -2319,10 +2319,12 @@ int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const 
 }
 
 constexpr int kMaxMultiOps = 256;
+// opt-in (PARAEXP_MULTI=1): measured no faster than PDL-overlapped single-op launches at 64^3
+// (6.7 vs 6.4 us per A-application) -- a unit's z-march latency, not the launch, bounds there
 static bool multi_enabled() {
     static const bool on = [] {
         const char *e = getenv("PARAEXP_MULTI");
-        return !(e && atoi(e) == 0);
+        return e && atoi(e) != 0;
     }();
     return on;
 }
