@@ -18,7 +18,8 @@
 namespace pe {
 
 constexpr int kSmallThreads = 1024;
-constexpr int kSmallMaxOps = 80;   // pair ops per substep (m <= 150 -> 75)
+constexpr int kSmallMaxOps = 80;
+constexpr size_t kSmallSmemMax = 232448;   // 227 KB opt-in shared memory per CTA   // pair ops per substep (m <= 150 -> 75)
 
 template <typename T>
 static constexpr int64_t small_max_cells() {
@@ -130,7 +131,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) leapfrog_small_kernel(Dev<T>
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *S = reinterpret_cast<T *>(smem_raw);
     const int cells = D.nx * D.ny * D.nz, px = D.nx, plane = D.nx * D.ny;
-    T *Q = S + 6 * cells;
+    // per-edge / per-face coefficients (EM 2, HA) are staged once as beta values in shared
+    // memory [bE0 bE1 bE2 bH0 bH1 bH2][cells]: read from global every step they miss L1
+    constexpr bool CS = (EM == 2 || HA);
+    T *CF = S + 6 * cells;
+    T *Q = S + (CS ? 12 : 6) * cells;
     load_state(D, st, S, cells);
     SmallCell cl[R];
     unsigned smask[R];
@@ -142,7 +147,18 @@ __global__ void __launch_bounds__(kSmallThreads, 1) leapfrog_small_kernel(Dev<T>
         smask[r] = 0;
         for (int s = 0; s < src.n; ++s)
             if (src.i[s] + D.nx * (src.j[s] + D.ny * src.k[s]) == x) smask[r] |= 1u << s;
+        if (CS && x < cells) {
+            const int k = (int)(cl[r].f >> 12);
+            for (int c = 0; c < 3; ++c) {
+                CF[c * cells + x] = cf.bE(c, k, cl[r].g);
+                CF[(3 + c) * cells + x] = T(1) * cf.bH(c, cl[r].g);
+            }
+        }
     }
+    auto bEx = [&](int c, int k, const SmallCell &q) -> T { return CS ? CF[c * cells + q.x] : cf.bE(c, k, q.g); };
+    auto bHx = [&](int c, const SmallCell &q) -> T {
+        return CS ? CF[(3 + c) * cells + q.x] : T(1) * cf.bH(c, q.g);
+    };
     T *ex = S, *ey = S + cells, *ez = S + 2 * cells, *hx = S + 3 * cells, *hy = S + 4 * cells, *hz = S + 5 * cells;
     for (int64_t m = 0; m < nsteps; ++m) {
         const int mq = (int)(m % kQChunk);
@@ -160,9 +176,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) leapfrog_small_kernel(Dev<T>
             const int k = (int)(f >> 12);
             T c0, c1, c2;
             curlT_f(hx, hy, hz, x, f, px, plane, c0, c1, c2);
-            if (f & 64u) ex[x] = ex[x] + cf.bE(0, k, cl[r].g) * c0;
-            if (f & 128u) ey[x] = ey[x] + cf.bE(1, k, cl[r].g) * c1;
-            if (f & 256u) ez[x] = ez[x] + cf.bE(2, k, cl[r].g) * c2;
+            if (f & 64u) ex[x] = ex[x] + bEx(0, k, cl[r]) * c0;
+            if (f & 128u) ey[x] = ey[x] + bEx(1, k, cl[r]) * c1;
+            if (f & 256u) ez[x] = ez[x] + bEx(2, k, cl[r]) * c2;
             for (unsigned sm = smask[r]; sm; sm &= sm - 1) {
                 const int s = __ffs(sm) - 1;
                 S[src.c[s] * cells + x] = S[src.c[s] * cells + x] - Q[mq * src.n + s];
@@ -177,9 +193,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) leapfrog_small_kernel(Dev<T>
             const unsigned f = cl[r].f;
             T c0, c1, c2;
             curl_f(ex, ey, ez, x, f, px, plane, c0, c1, c2);
-            if (f & 512u) hx[x] = hx[x] - (T(1) * cf.bH(0, cl[r].g)) * c0;
-            if (f & 1024u) hy[x] = hy[x] - (T(1) * cf.bH(1, cl[r].g)) * c1;
-            if (f & 2048u) hz[x] = hz[x] - (T(1) * cf.bH(2, cl[r].g)) * c2;
+            if (f & 512u) hx[x] = hx[x] - bHx(0, cl[r]) * c0;
+            if (f & 1024u) hy[x] = hy[x] - bHx(1, cl[r]) * c1;
+            if (f & 2048u) hz[x] = hz[x] - bHx(2, cl[r]) * c2;
         }
     }
     __syncthreads();
@@ -196,30 +212,35 @@ struct SmallOps {
 };
 
 // out = X in at an owned cell (e rows: bE C^T h, h rows: -bH C e; dead DOFs 0)
+// CF (optional): the beta values staged in shared memory [bE0 bE1 bE2 bH0 bH1 bH2][cells]
 template <typename T, int EM, bool HA>
-__device__ __forceinline__ void small_applyX(const Coef<T, EM, HA> &cf, const T *in, int cells, const SmallCell &c,
-                                             int px, int plane, T o[6]) {
+__device__ __forceinline__ void small_applyX(const Coef<T, EM, HA> &cf, const T *CF, const T *in, int cells,
+                                             const SmallCell &c, int px, int plane, T o[6]) {
     const int x = c.x, k = (int)(c.f >> 12);
     T a0, a1, a2, b0, b1, b2;
     curlT_f(in + 3 * cells, in + 4 * cells, in + 5 * cells, x, c.f, px, plane, a0, a1, a2);
     curl_f(in, in + cells, in + 2 * cells, x, c.f, px, plane, b0, b1, b2);
-    o[0] = (c.f & 64u) ? cf.bE(0, k, c.g) * a0 : T(0);
-    o[1] = (c.f & 128u) ? cf.bE(1, k, c.g) * a1 : T(0);
-    o[2] = (c.f & 256u) ? cf.bE(2, k, c.g) * a2 : T(0);
-    o[3] = (c.f & 512u) ? -(cf.bH(0, c.g) * b0) : T(0);
-    o[4] = (c.f & 1024u) ? -(cf.bH(1, c.g) * b1) : T(0);
-    o[5] = (c.f & 2048u) ? -(cf.bH(2, c.g) * b2) : T(0);
+    auto be = [&](int q) -> T { return CF ? CF[q * cells + x] : cf.bE(q, k, c.g); };
+    auto bh = [&](int q) -> T { return CF ? CF[(3 + q) * cells + x] : cf.bH(q, c.g); };
+    o[0] = (c.f & 64u) ? be(0) * a0 : T(0);
+    o[1] = (c.f & 128u) ? be(1) * a1 : T(0);
+    o[2] = (c.f & 256u) ? be(2) * a2 : T(0);
+    o[3] = (c.f & 512u) ? -(bh(0) * b0) : T(0);
+    o[4] = (c.f & 1024u) ? -(bh(1) * b1) : T(0);
+    o[5] = (c.f & 2048u) ? -(bh(2) * b2) : T(0);
 }
 
 // y (the Newton sum) stays in registers: thread t owns cells t, t + 1024, ... (R of them)
 template <typename T, int EM, bool HA, int R>
 __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, Coef<T, EM, HA> cf,
                                                                       T *__restrict__ st, int s,
-                                                                      const __grid_constant__ SmallOps ops) {
+                                                                      const __grid_constant__ SmallOps ops,
+                                                                      int stage_cf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *W = reinterpret_cast<T *>(smem_raw);
     const int cells = D.nx * D.ny * D.nz, px = D.nx, plane = D.nx * D.ny;
     T *U = W + 6 * cells;
+    T *CF = stage_cf ? U + 6 * cells : nullptr;   // staged betas (EM 2 / HA, when they fit)
     load_state(D, st, W, cells);
     SmallCell cl[R];
 #pragma unroll
@@ -227,6 +248,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, 
         const int x = threadIdx.x + r * kSmallThreads;
         cl[r] = small_cell(D, x < cells ? x : 0);
         cl[r].x = x;
+        if (CF && x < cells) {
+            const int k = (int)(cl[r].f >> 12);
+            for (int c = 0; c < 3; ++c) {
+                CF[c * cells + x] = cf.bE(c, k, cl[r].g);
+                CF[(3 + c) * cells + x] = cf.bH(c, cl[r].g);
+            }
+        }
     }
     __syncthreads();
     T y[R][6];
@@ -242,7 +270,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, 
             for (int r = 0; r < R; ++r) {                 // U = X W
                 if (cl[r].x >= cells) continue;
                 T u[6];
-                small_applyX(cf, W, cells, cl[r], px, plane, u);
+                small_applyX(cf, CF, W, cells, cl[r], px, plane, u);
 #pragma unroll
                 for (int c = 0; c < 6; ++c) U[c * cells + cl[r].x] = u[c];
             }
@@ -252,7 +280,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, 
                 const int x = cl[r].x;
                 if (x >= cells) continue;
                 T xu[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
-                if (kind != 1) small_applyX(cf, U, cells, cl[r], px, plane, xu);   // X U (U neighbours)
+                if (kind != 1) small_applyX(cf, CF, U, cells, cl[r], px, plane, xu);   // X U (U neighbours)
 #pragma unroll
                 for (int c = 0; c < 6; ++c) {
                     const T wv = W[c * cells + x], uv = U[c * cells + x];
@@ -297,7 +325,8 @@ int k_leapfrog_small(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
         constexpr int R = (int)(small_max_cells<T>() / kSmallThreads);
-        const size_t smem = ((size_t)6 * g.nx * g.ny * g.nz + (size_t)kQChunk * nsrc) * sizeof(T);
+        constexpr size_t nv = (EM == 2 || HA) ? 12 : 6;   // state (+ staged coefficients)
+        const size_t smem = (nv * g.nx * g.ny * g.nz + (size_t)kQChunk * nsrc) * sizeof(T);
         auto kern = leapfrog_small_kernel<T, EM, HA, R>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<1, kSmallThreads, smem, (cudaStream_t)ka.stream>>>(make_dev<T>(g), make_coef<T, EM, HA>(g, 1.0),
@@ -325,11 +354,13 @@ int k_poly_small(const KernelArgs &ka, const Plan &plan, void *state) {
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
         constexpr int R = (int)(small_max_cells<T>() / kSmallThreads);
-        const size_t smem = (size_t)12 * g.nx * g.ny * g.nz * sizeof(T);
+        const size_t cells = (size_t)g.nx * g.ny * g.nz;
+        const int stage = ((EM == 2 || HA) && 18 * cells * sizeof(T) <= kSmallSmemMax) ? 1 : 0;
+        const size_t smem = (stage ? 18 : 12) * cells * sizeof(T);
         auto kern = poly_small_kernel<T, EM, HA, R>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmemMax);
         kern<<<1, kSmallThreads, smem, (cudaStream_t)ka.stream>>>(make_dev<T>(g), make_coef<T, EM, HA>(g, plan.sigma),
-                                                                   (T *)state, plan.s, ops);
+                                                                   (T *)state, plan.s, ops, stage);
         ++*ka.launches;
         return check_cuda("poly small");
     });
