@@ -213,15 +213,15 @@ struct SmallOps {
 
 // out = X in at an owned cell (e rows: bE C^T h, h rows: -bH C e; dead DOFs 0)
 // CF (optional): the beta values staged in shared memory [bE0 bE1 bE2 bH0 bH1 bH2][cells]
-template <typename T, int EM, bool HA>
+template <typename T, int EM, bool HA, bool STG>
 __device__ __forceinline__ void small_applyX(const Coef<T, EM, HA> &cf, const T *CF, const T *in, int cells,
                                              const SmallCell &c, int px, int plane, T o[6]) {
     const int x = c.x, k = (int)(c.f >> 12);
     T a0, a1, a2, b0, b1, b2;
     curlT_f(in + 3 * cells, in + 4 * cells, in + 5 * cells, x, c.f, px, plane, a0, a1, a2);
     curl_f(in, in + cells, in + 2 * cells, x, c.f, px, plane, b0, b1, b2);
-    auto be = [&](int q) -> T { return CF ? CF[q * cells + x] : cf.bE(q, k, c.g); };
-    auto bh = [&](int q) -> T { return CF ? CF[(3 + q) * cells + x] : cf.bH(q, c.g); };
+    auto be = [&](int q) -> T { return STG ? CF[q * cells + x] : cf.bE(q, k, c.g); };
+    auto bh = [&](int q) -> T { return STG ? CF[(3 + q) * cells + x] : cf.bH(q, c.g); };
     o[0] = (c.f & 64u) ? be(0) * a0 : T(0);
     o[1] = (c.f & 128u) ? be(1) * a1 : T(0);
     o[2] = (c.f & 256u) ? be(2) * a2 : T(0);
@@ -231,16 +231,15 @@ __device__ __forceinline__ void small_applyX(const Coef<T, EM, HA> &cf, const T 
 }
 
 // y (the Newton sum) stays in registers: thread t owns cells t, t + 1024, ... (R of them)
-template <typename T, int EM, bool HA, int R>
+template <typename T, int EM, bool HA, int R, bool STG>
 __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, Coef<T, EM, HA> cf,
                                                                       T *__restrict__ st, int s,
-                                                                      const __grid_constant__ SmallOps ops,
-                                                                      int stage_cf) {
+                                                                      const __grid_constant__ SmallOps ops) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *W = reinterpret_cast<T *>(smem_raw);
     const int cells = D.nx * D.ny * D.nz, px = D.nx, plane = D.nx * D.ny;
     T *U = W + 6 * cells;
-    T *CF = stage_cf ? U + 6 * cells : nullptr;   // staged betas (EM 2 / HA, when they fit)
+    T *CF = U + 6 * cells;                         // staged betas (STG: EM 2 / HA, when they fit)
     load_state(D, st, W, cells);
     SmallCell cl[R];
 #pragma unroll
@@ -248,7 +247,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, 
         const int x = threadIdx.x + r * kSmallThreads;
         cl[r] = small_cell(D, x < cells ? x : 0);
         cl[r].x = x;
-        if (CF && x < cells) {
+        if (STG && x < cells) {
             const int k = (int)(cl[r].f >> 12);
             for (int c = 0; c < 3; ++c) {
                 CF[c * cells + x] = cf.bE(c, k, cl[r].g);
@@ -270,7 +269,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, 
             for (int r = 0; r < R; ++r) {                 // U = X W
                 if (cl[r].x >= cells) continue;
                 T u[6];
-                small_applyX(cf, CF, W, cells, cl[r], px, plane, u);
+                small_applyX<T, EM, HA, STG>(cf, CF, W, cells, cl[r], px, plane, u);
 #pragma unroll
                 for (int c = 0; c < 6; ++c) U[c * cells + cl[r].x] = u[c];
             }
@@ -280,7 +279,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) poly_small_kernel(Dev<T> D, 
                 const int x = cl[r].x;
                 if (x >= cells) continue;
                 T xu[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
-                if (kind != 1) small_applyX(cf, CF, U, cells, cl[r], px, plane, xu);   // X U (U neighbours)
+                if (kind != 1) small_applyX<T, EM, HA, STG>(cf, CF, U, cells, cl[r], px, plane, xu);   // X U (U neighbours)
 #pragma unroll
                 for (int c = 0; c < 6; ++c) {
                     const T wv = W[c * cells + x], uv = U[c * cells + x];
@@ -355,12 +354,12 @@ int k_poly_small(const KernelArgs &ka, const Plan &plan, void *state) {
         constexpr bool HA = decltype(tHA)::value;
         constexpr int R = (int)(small_max_cells<T>() / kSmallThreads);
         const size_t cells = (size_t)g.nx * g.ny * g.nz;
-        const int stage = ((EM == 2 || HA) && 18 * cells * sizeof(T) <= kSmallSmemMax) ? 1 : 0;
+        const bool stage = (EM == 2 || HA) && 18 * cells * sizeof(T) <= kSmallSmemMax;
         const size_t smem = (stage ? 18 : 12) * cells * sizeof(T);
-        auto kern = poly_small_kernel<T, EM, HA, R>;
+        auto kern = stage ? poly_small_kernel<T, EM, HA, R, (EM == 2 || HA)> : poly_small_kernel<T, EM, HA, R, false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmemMax);
         kern<<<1, kSmallThreads, smem, (cudaStream_t)ka.stream>>>(make_dev<T>(g), make_coef<T, EM, HA>(g, plan.sigma),
-                                                                   (T *)state, plan.s, ops, stage);
+                                                                   (T *)state, plan.s, ops);
         ++*ka.launches;
         return check_cuda("poly small");
     });
