@@ -10,7 +10,8 @@ region starts; the working set (815 MB per state vector) exceeds the 126 MB L2, 
 flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W]
-                  [--workload c3|c3-f32|c3-p64|c2|c1|c4|c5-<n>[-f64]|wave2d[-k]]
+                  [--workload c3|c3-f32|c3-p64|c2|c1|c4|c5-<n>[-f64]|c5s-<n>[-f64]|wave2d[-k]]
+                  [--p P]
                   [--impl ours|reference] [--no-cpu-baseline]
 
 Under torchrun (N > 1) every rank runs one process per GPU; sub-intervals are sharded in
@@ -38,7 +39,7 @@ FALLBACK_HBM_GBS = 6650.0
 
 
 def workload(name):
-    from synth import config_c1, config_c2, config_c3, config_c4, config_c5, config_wave2d
+    from synth import config_c1, config_c2, config_c3, config_c4, config_c5, config_c5s, config_wave2d
     if name == "c3":
         return config_c3("f64", p=8, nsteps=4096)
     if name == "c3-f32":
@@ -54,6 +55,9 @@ def workload(name):
     if name.startswith("wave2d"):          # wave2d[-k]: the paper's 2-D wave, n_t from T = 2e-7 s
         k = float(name.split("-")[1]) if "-" in name else 1.0
         return config_wave2d(41, k)
+    if name.startswith("c5s-"):           # c5s-<n>[-f64]: C5 + a centred source, ParaExp (addition)
+        n = int(name.split("-")[1])
+        return config_c5s(n=n, dtype="f64" if name.endswith("f64") else "f32")
     if name.startswith("c5-"):
         n = int(name.split("-")[1])
         return config_c5(n=n, dtype="f64" if name.endswith("f64") else "f32")
@@ -140,26 +144,52 @@ def committed_traffic(kernel, w):
     return sum(vals) / len(vals), path
 
 
-def cpu_baseline(w, budget_steps=None):
-    """The oracle as it stands, on the host cores, on a bounded sample of the workload:
-    leapfrog steps + one degree-8 Leja substep on the full grid (cell-updates/s)."""
-    from oracle import fit
-    g = fit.Grid.from_workload(w)
+def _oracle_sample(fit, g, w, nlf):
+    """nlf leapfrog steps + one degree-8 Leja substep of the oracle on the full grid; returns
+    (leapfrog seconds, expmv seconds)."""
     e, h = g.zeros()
-    nlf = budget_steps or (20 if w.cells <= 20_000_000 else 4)
     t0 = time.perf_counter()
     e, h = fit.leapfrog(g, e, h, nlf, w.sources, t0=0.0)
     t1 = time.perf_counter()
     plan = fit.make_plan("leja", 8, 1, 3 * g.dt, g.rho_cfl)
     fit.expmv(g, plan, e + 1.0 * g.live_e, h, mode="pairs")
     t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+def cpu_baseline(w, solve_stats=None, single_thread=True):
+    """The oracle as it stands, on the host cores, on a bounded sample of the workload:
+    20 leapfrog steps (4 above 20 M cells) + one degree-8 Leja substep (8 A-applications) on
+    the full grid, cell-updates/s.  Also: the same rate on ONE thread (2 steps + the substep),
+    and the oracle's ParaExp wall time for the whole solve extrapolated from the two measured
+    rates and the solve's leapfrog steps / A-applications (an extrapolation, not a run)."""
+    from oracle import fit
+    g = fit.Grid.from_workload(w)
+    nlf = 20 if w.cells <= 20_000_000 else 4
+    cores = fit.num_threads()
+    tl, te = _oracle_sample(fit, g, w, nlf)
     cu = (nlf + 8) * w.cells
-    return {"value": cu / (t2 - t0), "unit": "cell-updates/s", "cores": fit.num_threads(),
-            "kind": "oracle",
-            "sample": f"{w.name} grid {w.nx}x{w.ny}x{w.nz} {w.dtype}: {nlf} leapfrog steps + one "
-                      f"degree-8 Leja substep (8 A-applications), plain C/OpenMP + numpy oracle",
-            "leapfrog_rate": nlf * w.cells / (t1 - t0), "expmv_rate": 8 * w.cells / (t2 - t1),
-            "seconds": t2 - t0}
+    out = {"value": cu / (tl + te), "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
+           "sample": f"{w.name} grid {w.nx}x{w.ny}x{w.nz} {w.dtype}: {nlf} leapfrog steps + one "
+                     f"degree-8 Leja substep (8 A-applications), plain C/OpenMP oracle",
+           "leapfrog_rate": nlf * w.cells / tl, "expmv_rate": 8 * w.cells / te, "seconds": tl + te}
+    if single_thread:
+        fit.set_threads(1)
+        try:
+            tl1, te1 = _oracle_sample(fit, g, w, 2)
+        finally:
+            fit.set_threads(cores)
+        out["one_thread"] = {"value": 10 * w.cells / (tl1 + te1), "cores": 1,
+                             "sample": "2 leapfrog steps + one degree-8 Leja substep",
+                             "leapfrog_rate": 2 * w.cells / tl1, "expmv_rate": 8 * w.cells / te1}
+    if solve_stats:
+        lf, aa = solve_stats["leapfrog_steps"], solve_stats["a_applications"]
+        sec = lf * w.cells / out["leapfrog_rate"] + aa * w.cells / out["expmv_rate"]
+        out["paraexp_wall_s_extrapolated"] = sec
+        out["paraexp_extrapolation"] = (f"{lf} leapfrog steps / leapfrog_rate + {aa} A-applications / "
+                                        f"expmv_rate on {cores} cores (the oracle's own Horner sum does "
+                                        f"the same work as one GPU)")
+    return out
 
 
 def run_reference(args, rank, world):
@@ -169,8 +199,10 @@ def run_reference(args, rank, world):
     w = workload(args.workload)
     steps = []
     cb = None
+    if args.p:
+        w.p = args.p
     for it in range(args.warmup + args.steps):
-        r = cpu_baseline(w, budget_steps=2)
+        r = cpu_baseline(w, single_thread=False)
         if it >= args.warmup:
             steps.append(r)
         cb = r
@@ -199,6 +231,7 @@ def main():
     ap.add_argument("--kernels", default="auto", choices=["auto", "unfused", "fused"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-serial", action="store_true")
+    ap.add_argument("--p", type=int, default=0, help="override the workload's sub-interval count")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -217,6 +250,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = workload(args.workload)
+    if args.p:
+        w.p = args.p
     grid = pe.Grid.from_workload(w, device=local, kernels=args.kernels)
     stream = torch.cuda.current_stream(local)
     info = grid.info(compute_rho_pow=True, stream=stream.cuda_stream)
@@ -395,10 +430,8 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
     }
-    if not args.no_cpu_baseline and world == 1:
-        out["cpu_baseline"] = cpu_baseline(w)
-    elif not args.no_cpu_baseline and rank == 0:
-        out["cpu_baseline"] = cpu_baseline(w)
+    if not args.no_cpu_baseline and world == 1:      # rank 0 at N = 1 only
+        out["cpu_baseline"] = cpu_baseline(w, solve_stats=stats[-1])
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -32,7 +32,10 @@
  *             paraexp_last_error() returns a thread-local message for the last failure.
  *             On error the output buffers are unspecified.
  *  Threads    A grid owns a device workspace: calls on one grid must not run
- *             concurrently from several host threads.
+ *             concurrently from several host threads.  Calls on one grid from one
+ *             thread may use different streams: each call records an event at its end
+ *             and the next call's stream waits for it before touching the grid's
+ *             workspaces, so the device work of consecutive calls never overlaps.
  */
 #ifndef PARAEXP_H
 #define PARAEXP_H
@@ -122,7 +125,7 @@ typedef struct {
 int paraexp_grid_create(const paraexp_grid_desc *desc, paraexp_grid **out);
 void paraexp_grid_destroy(paraexp_grid *grid);
 /* Fill *out.  If compute_rho_pow != 0 and the grid is on a device, runs the Lanczos
- * norm estimate K5 (40 steps, stream-synchronous on `stream`) and caches it. */
+ * norm estimate K5 (60 steps, stream-synchronous on `stream`) and caches it. */
 int paraexp_grid_info(paraexp_grid *grid, int32_t compute_rho_pow, void *stream,
                       paraexp_grid_info_t *out);
 /* Export the fp64 coefficients the library assembled, canonical layout, host pointers of
@@ -162,7 +165,10 @@ typedef struct {
     int32_t fail_interval;     /* solve: sub-interval index of a divergence, else 0       */
     double ms_particular, ms_tails, ms_reduce, ms_finish, ms_total; /* device-event times */
     double ms_leapfrog_kernels;  /* device time of the leapfrog kernel sequences (a2/a3)      */
-    double ms_poly_kernels;      /* device time of the polynomial substep kernels (a6)         */
+    double ms_poly_kernels;      /* device time of the polynomial substep kernels (a6, incl.
+                                    solve's dt/2 reconstruction propagator)                   */
+    int32_t rho_fallback;        /* 1 if the rho safety net re-ran with rho = rho_cfl        */
+    double norm_deviation;       /* max | ||E_i b||_M / ||b||_M - 1 | seen by the safety net  */
 } paraexp_stats;
 
 /* ---- leapfrog (a2, a3) ----------------------------------------------------------- */
@@ -228,7 +234,15 @@ int paraexp_leapfrog_trace(paraexp_grid *grid, const paraexp_source *src, int32_
  *            termination", reading 18); the skipped ops launch and return at once;
  *            stats.a_applications reports the A-applications actually performed
  *   beta     with eps_A == 0 and beta > 0: eps_A = eps_A* = beta dt^2 / rho
- *            (eq:tolerance_leja_2; see paraexp_optimal_tolerance)          */
+ *            (eq:tolerance_leja_2; see paraexp_optimal_tolerance)
+ *   rho_check  rho safety net (SURVEY finding 8): exp(tau A) preserves the energy norm
+ *            (A skew in <.,.>_M), so every propagator's energy norm is
+ *            compared before and after (one fused dot each); a deviation above
+ *            max(1e-9 (f64) / 1e-3 (f32), 10 eps_A rho tau) (fixed (m, s): 1e-3) means rho
+ *            missed the spectrum, and the propagator (expmv) / the rank's block (solve) is
+ *            recomputed with rho = rho_cfl (stats.rho_fallback = 1).
+ *            0 = on when rho is the K5 estimate (opts rho == 0), off for an explicit rho;
+ *            > 0 = on; < 0 = off.  Never for Krylov (norm-preserving by construction).      */
 typedef struct {
     int32_t method;
     int32_t m, s;
@@ -236,6 +250,7 @@ typedef struct {
     double rho;
     int32_t early_term;
     double beta;
+    int32_t rho_check;
 } paraexp_expmv_opts;
 
 /* Plan export (reading 25: parity is defined at a fixed plan). */
@@ -272,27 +287,60 @@ void paraexp_comm_destroy(paraexp_comm *comm);
 /* COLLECTIVE over `comm` (NULL => single GPU, world 1): every rank calls with identical
  * arguments.  Time interval (t0, t0 + nsteps dt] is split into p sub-intervals of
  * nsteps/p steps, residual steps to the last.  Sub-intervals are assigned
- * to ranks in contiguous blocks (rank r gets an equal share, earlier ranks get the
- * remainder); a rank computes, for each owned j, the particular solution v_j by
- * leapfrog from zero with global source times, the seed s_j = (e_j, h_j + cH/2 C e_j)
- * (reading 9) and accumulates its tails to T_p by Horner over the per-sub-interval
- * propagators E_i (SURVEY finding 9):  W <- E_i W + s_i.  The rank owning sub-interval
- * 1 also carries u0 (reading 12).  W is summed with ncclReduce onto the root = owner of
- * sub-interval p, which reconstructs (eq:averaging1/2, reading 10):
+ * to ranks in contiguous blocks, cost-balanced (paraexp_schedule with tail_ratio = the
+ * A-applications of one propagator over the steps of one sub-interval); a rank computes,
+ * for each owned j, the particular solution v_j by leapfrog from zero with global source
+ * times, the seed s_j = (e_j, h_j + cH/2 C e_j) (reading 9) and accumulates its tails to
+ * T_p by Horner over the per-sub-interval propagators E_i (SURVEY finding 9):
+ * W <- E_i W + s_i.  The rank owning sub-interval 1 also carries u0 (reading 12).  W is
+ * summed with ncclReduce onto the root = owner of sub-interval p, which reconstructs
+ * (eq:averaging1/2, reading 10):
  *      e_out = e_p + W_e,   h_out = h_p + [exp(dt/2 A) W]_h.
- * tail_mode PARAEXP_TAIL_LEAPFROG propagates the staggered seeds with leapfrog instead
- * (debug identity: equals serial leapfrog).
+ * = paraexp_solve_block on every rank, a sum of the blocks' W, paraexp_solve_finish on the
+ * root.  tail_mode PARAEXP_TAIL_LEAPFROG propagates the staggered seeds with leapfrog
+ * instead (debug identity: equals serial leapfrog).
  *   e0, h0   same-time initial value u0 at t0 (device, canonical) or NULL => 0
  *   e_out, h_out  device, canonical; written on the root, or on every rank when
  *            broadcast_out != 0 (one ncclBroadcast).  Output convention equals
  *            paraexp_leapfrog from (e0, h0 - cH/2 C e0): (e^(n), h^(n+1/2)).
- * Errors: EINVAL (p < 1, nsteps < p), ENOTSUP, EDIVERGED / EOVERFLOW (stats.fail_interval),
- *         ENCCL, ECUDA.  Synchronises `stream` before returning. */
+ * With a communicator the call waits for its stream while polling ncclCommGetAsyncError
+ * (a failed peer => the communicator is aborted, ENCCL).
+ * Errors: EINVAL (p < 1, nsteps < p), ENOTSUP, EDIVERGED (particular sweep of
+ *         stats.fail_interval non-finite) / EOVERFLOW (propagator E_{fail_interval}
+ *         produced a non-finite field), ENCCL, ECUDA.  Synchronises `stream` before
+ *         returning. */
 int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
                   int32_t nsrc, double t0, int64_t nsteps, int32_t p,
                   const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
                   const void *e0, const void *h0, void *e_out, void *h_out, void *stream,
                   paraexp_stats *stats);
+
+/* One rank's share of paraexp_solve without any communication (the parfor body of
+ * PAPER:358-365 for the block paraexp_schedule gives `rank` of `world`), for callers that
+ * sum the blocks themselves (MPI, gloo, or several virtual ranks on one GPU).
+ *   w_e, w_h  out (device or host, canonical): this rank's tails carried to T_p,
+ *            W_rank = sum_{owned j < p} E_p..E_{j+1} s_j (+ E_p..E_1 u0 if it owns j = 1);
+ *            zero if the rank owns no sub-interval.  The sum of W_rank over ranks is the
+ *            W that paraexp_solve reduces.
+ *   v_e, v_h  out on the root only (stats.root == rank; may be NULL elsewhere): the
+ *            particular state (e_p^(M), h_p^(M+1/2)) of sub-interval p.
+ * All ranks must use the same rho: pass opts->rho > 0 (e.g. rank 0's stats.rho) unless
+ * the grids are identical (the K5 estimate is then cached per grid).  The rho safety net
+ * acts per rank.  Synchronises `stream`.  Errors as paraexp_solve (no ENCCL). */
+int paraexp_solve_block(paraexp_grid *grid, int32_t rank, int32_t world,
+                        const paraexp_source *src, int32_t nsrc, double t0, int64_t nsteps,
+                        int32_t p, const paraexp_expmv_opts *opts, int32_t tail_mode,
+                        const void *e0, const void *h0, void *w_e, void *w_h, void *v_e,
+                        void *v_h, void *stream, paraexp_stats *stats);
+
+/* Reconstruction on the root (a9, eq:averaging1/2, reading 10) from the summed W = (w_e,
+ * w_h) and the root's particular state (v_e, v_h):  e_out = v_e + w_e,
+ * h_out = v_h + [exp(dt/2 A) W]_h (tail_mode EXP; a degree-24 Taylor propagator with
+ * rho from opts as in paraexp_expmv), or (e_out, h_out) = v + W (tail_mode LEAPFROG).
+ * All pointers canonical, device or host; the outputs may alias v.  Synchronises. */
+int paraexp_solve_finish(paraexp_grid *grid, const paraexp_expmv_opts *opts, int32_t tail_mode,
+                         const void *w_e, const void *w_h, const void *v_e, const void *v_h,
+                         void *e_out, void *h_out, void *stream, paraexp_stats *stats);
 
 /* paraexp_solve (tail_mode EXP) with a trace of the reconstructed solution at the
  * sub-interval boundaries T_1 .. T_p (see paraexp_trace above; f1).  Collective. */
@@ -307,9 +355,15 @@ int paraexp_solve_trace(paraexp_grid *grid, paraexp_comm *comm, const paraexp_so
  * (SPEC:345-353).  EINVAL if p < 1 or nsteps < p. */
 int paraexp_partition(int64_t nsteps, int32_t p, int64_t *bounds);
 /* Contiguous block [first, last] (1-based sub-interval indices) owned by `rank` of `world`
- * for p sub-intervals; first = last + 1 = 0 if the rank owns none.  root = owner of p. */
-int paraexp_schedule(int32_t p, int32_t world, int32_t rank, int32_t *first, int32_t *last,
-                     int32_t *root);
+ * for p sub-intervals; first = 0, last = -1 if the rank owns none; root = owner of p.
+ * Cost-balanced: with a block [f, l] costing (l - f + 1) sweeps plus
+ * (p - f) propagators (one more if f = 1 and has_u0), a propagator costing tail_ratio
+ * sweeps, the blocks minimise the largest rank cost (bisection on the makespan, then each
+ * rank in order takes as many sub-intervals as fit -- the fewest ranks, hence the least
+ * Horner work, at that makespan).  tail_ratio <= 0: equal shares, the remainder to the
+ * later ranks.  Host-only. */
+int paraexp_schedule(int32_t p, int32_t world, int32_t rank, double tail_ratio, int32_t has_u0,
+                     int32_t *first, int32_t *last, int32_t *root);
 /* Symmetrised Leja sequence xi'_0..xi'_{count-1} on [-1,1] (reading 14). */
 int paraexp_leja_points(int32_t count, double *xi);
 /* Plan without a grid: tau and rho given, dt used only for sigma (may be 1). */

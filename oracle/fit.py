@@ -53,7 +53,11 @@ def lib():
         _lib.or_curlT.argtypes = [i, i, i, dp, dp]
         _lib.or_leapfrog.argtypes = [i, i, i, dp, dp, ctypes.c_long, i, lp, dp, dp, dp]
         _lib.or_apply_A.argtypes = [i, i, i, dp, dp, dp, dp, dp, dp]
+        ip = ctypes.POINTER(ctypes.c_int)
+        _lib.or_expmv_pairs.argtypes = [i, i, i, dp, dp, i, ip, dp, dp, dp, dp, i, dp, dp]
+        _lib.or_expmv_pairs.restype = ctypes.c_int
         _lib.or_num_threads.restype = ctypes.c_int
+        _lib.or_set_threads.argtypes = [i]
     return _lib
 
 
@@ -67,6 +71,11 @@ def _up(a):
 
 def num_threads() -> int:
     return lib().or_num_threads()
+
+
+def set_threads(n: int) -> None:
+    """OpenMP thread count of the C loops (timing only; results do not depend on it)."""
+    lib().or_set_threads(int(n))
 
 
 def _round(x, dtype):
@@ -503,7 +512,7 @@ def expmv_pairs_et(g: Grid, plan: Plan, e, h, eps: float, dtype: str = "f64"):
     return be, bh, apps
 
 
-def expmv_pairs(g: Grid, plan: Plan, e, h, dtype: str = "f64"):
+def expmv_pairs_numpy(g: Grid, plan: Plan, e, h, dtype: str = "f64"):
     """The same polynomial in real arithmetic, conjugate pairs folded (readings 28-29):
         pair: u = X w; y += a w + b u; w = X u + e2 w
         last: u = X w; y += a w + b u + c (X u + e2 w)      half (m = 1): u = X w; y += a w + b u
@@ -532,6 +541,24 @@ def expmv_pairs(g: Grid, plan: Plan, e, h, dtype: str = "f64"):
                 else:
                     we, wh = we2, wh2
         be, bh = ye, yh
+    return be, bh
+
+
+def expmv_pairs(g: Grid, plan: Plan, e, h, dtype: str = "f64"):
+    """expmv_pairs_numpy's recurrence, the same steps in the same order, run by the plain C
+    loops of fit_oracle.c (or_expmv_pairs) -- fast enough for the full-horizon parity runs.
+    Pinned to expmv_pairs_numpy (tests/test_oracle_expmv.py)."""
+    X = ScaledOp(g, (plan.tau / plan.s) / (plan.gamma * g.dt), dtype)
+    consts = pair_constants(plan, dtype)
+    kinds = np.array([{"pair": 0, "half": 1, "last": 2}[k] for k, *_ in consts], dtype=np.intc)
+    a, b, e2, c = (np.array([x[q] for x in consts], dtype=np.float64) for q in (1, 2, 3, 4))
+    be = np.array(e, dtype=np.float64, copy=True)
+    bh = np.array(h, dtype=np.float64, copy=True)
+    rc = lib().or_expmv_pairs(g.nx, g.ny, g.nz, _dp(X.sE), _dp(X.sH), len(consts),
+                              kinds.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _dp(a), _dp(b),
+                              _dp(e2), _dp(c), int(plan.s), _dp(be), _dp(bh))
+    if rc != 0:
+        raise MemoryError("or_expmv_pairs: workspace allocation failed")
     return be, bh
 
 

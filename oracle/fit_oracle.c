@@ -20,6 +20,7 @@
  * (no blocking, no fusion, no reordering of the per-entry arithmetic).
  */
 #include <math.h>
+#include <stdlib.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -250,5 +251,83 @@ int or_num_threads(void) {
     return omp_get_max_threads();
 #else
     return 1;
+#endif
+}
+
+/* ------------------------------------------------------------------------ */
+/* The real conjugate-pair Newton recurrence (DESIGN readings 28-29),
+ * s substeps of the same op list, step by step exactly as fit.expmv_pairs states it:
+ *   substep: w = b; y = 0; for each op:
+ *     u = X w;  y = (y + a w) + b u;
+ *     pair: w = X u + e2 w        last: y = y + c (X u + e2 w)        half: (nothing)
+ *   b = y
+ * X is or_apply_A with the caller's scaled coefficients sE, sH.  kind: 0 pair, 1 half,
+ * 2 last.  Elementwise updates are plain loops (OpenMP splits the index range only); the
+ * association of each update is the one written above.                                  */
+static void axpy2(long n, double *y, double a, const double *w, double b, const double *u) {
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < n; ++i) y[i] = (y[i] + a * w[i]) + b * u[i];
+}
+static void xpay(long n, double *out, const double *x, double e2, const double *w) {
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < n; ++i) out[i] = x[i] + e2 * w[i];
+}
+static void axpy1(long n, double *y, double c, const double *x) {
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < n; ++i) y[i] = y[i] + c * x[i];
+}
+
+int or_expmv_pairs(int nx, int ny, int nz, const double *sE, const double *sH, int nops,
+                   const int *kind, const double *a, const double *b, const double *e2,
+                   const double *c, int s, double *e, double *h) {
+    long Np = (long)(nx + 1) * (ny + 1) * (nz + 1);
+    long n = 3 * Np;
+    /* workspace of 10 vectors, kept between calls (the Python side calls one at a time) */
+    static double *buf = NULL;
+    static long buf_n = 0;
+    if (n > buf_n) {
+        free(buf);
+        buf = (double *)malloc(sizeof(double) * 10 * n);
+        buf_n = buf ? n : 0;
+    }
+    if (!buf) return -1;
+    /* vectors are (e, h) pairs of n doubles each */
+    double *we = buf, *wh = buf + n, *ue = buf + 2 * n, *uh = buf + 3 * n;
+    double *xe = buf + 4 * n, *xh = buf + 5 * n, *ye = buf + 6 * n, *yh = buf + 7 * n;
+    double *te = buf + 8 * n, *th = buf + 9 * n;
+    for (int q = 0; q < s; ++q) {
+        memcpy(we, e, sizeof(double) * n);
+        memcpy(wh, h, sizeof(double) * n);
+        memset(ye, 0, sizeof(double) * n);
+        memset(yh, 0, sizeof(double) * n);
+        for (int o = 0; o < nops; ++o) {
+            or_apply_A(nx, ny, nz, sE, sH, we, wh, ue, uh);          /* u = X w */
+            axpy2(n, ye, a[o], we, b[o], ue);                          /* y = (y + a w) + b u */
+            axpy2(n, yh, a[o], wh, b[o], uh);
+            if (kind[o] == 1) continue;                                /* half */
+            or_apply_A(nx, ny, nz, sE, sH, ue, uh, xe, xh);          /* X u */
+            xpay(n, te, xe, e2[o], we);                                /* X u + e2 w */
+            xpay(n, th, xh, e2[o], wh);
+            if (kind[o] == 2) {                                        /* last */
+                axpy1(n, ye, c[o], te);
+                axpy1(n, yh, c[o], th);
+            } else {                                                   /* pair: w = X u + e2 w */
+                double *t = we; we = te; te = t;
+                t = wh; wh = th; th = t;
+            }
+        }
+        memcpy(e, ye, sizeof(double) * n);
+        memcpy(h, yh, sizeof(double) * n);
+    }
+    return 0;
+}
+
+/* thread count of the OpenMP loops (1 = the single-thread oracle rate of bench.py) */
+void or_set_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    omp_set_num_threads(n);
+#else
+    (void)n;
 #endif
 }

@@ -17,6 +17,7 @@ from .abi import (EDIVERGED, EINVAL, ENOTSUP, EOVERFLOW, F32, F64, KERNELS_AUTO,
                   KERNELS_UNFUSED, KRYLOV, LEJA, TAIL_EXP, TAIL_LEAPFROG, TAYLOR, ParaexpError, check)
 
 __all__ = ["Grid", "Comm", "leapfrog", "leapfrog_trace", "expmv", "expmv_plan", "solve", "solve_trace",
+           "solve_block", "solve_finish",
            "optimal_tolerance",
            "partition", "schedule",
            "leja_points", "plan_host", "theta", "version", "make_sources", "ParaexpError"]
@@ -152,11 +153,12 @@ def make_sources(sources: Optional[Iterable]) -> tuple:
     return arr, len(srcs)
 
 
-def _opts(method="leja", m=0, s=0, eps_A=1e-12, rho=0.0, early_term=False, beta=0.0):
+def _opts(method="leja", m=0, s=0, eps_A=1e-12, rho=0.0, early_term=False, beta=0.0, rho_check=0):
     o = abi.paraexp_expmv_opts()
     o.method = _METHOD[method] if isinstance(method, str) else int(method)
     o.m, o.s, o.eps_A, o.rho = int(m), int(s), float(eps_A), float(rho or 0.0)
     o.early_term, o.beta = int(bool(early_term)), float(beta or 0.0)
+    o.rho_check = int(rho_check)
     return o
 
 
@@ -175,7 +177,7 @@ def leapfrog(grid: Grid, e, h, nsteps: int, sources=None, t0: float = 0.0,
     st = abi.paraexp_stats()
     check(abi.lib.paraexp_leapfrog(grid.handle, arr, n, float(t0), int(nsteps), _field(e, grid, "e"),
                                    _field(h, grid, "h"), int(bool(check_finite)),
-                                   _stream(stream, grid), C.byref(st)), "paraexp_leapfrog")
+                                   _stream(stream, grid), C.byref(st)), "paraexp_leapfrog", st)
     return st.as_dict()
 
 
@@ -207,7 +209,7 @@ def leapfrog_trace(grid: Grid, e, h, nsteps: int, sources=None, t0: float = 0.0,
     st = abi.paraexp_stats()
     check(abi.lib.paraexp_leapfrog_trace(grid.handle, arr, n, float(t0), int(nsteps), _field(e, grid, "e"),
                                          _field(h, grid, "h"), C.byref(t), _stream(stream, grid),
-                                         C.byref(st)), "paraexp_leapfrog_trace")
+                                         C.byref(st)), "paraexp_leapfrog_trace", st)
     if pr is not None:
         pr = pr[:nsteps * len(probes)].view(nsteps, len(probes))
     if en is not None:
@@ -216,13 +218,13 @@ def leapfrog_trace(grid: Grid, e, h, nsteps: int, sources=None, t0: float = 0.0,
 
 
 def expmv(grid: Grid, tau: float, e, h, method="leja", m=0, s=0, eps_A=1e-12, rho=0.0,
-          stream=None, early_term=False, beta=0.0) -> dict:
+          stream=None, early_term=False, beta=0.0, rho_check=0) -> dict:
     """paraexp_expmv: (h, e) <- exp(tau A_orig)(h, e) in place."""
-    o = _opts(method, m, s, eps_A, rho, early_term, beta)
+    o = _opts(method, m, s, eps_A, rho, early_term, beta, rho_check)
     st = abi.paraexp_stats()
     check(abi.lib.paraexp_expmv(grid.handle, float(tau), C.byref(o), _field(e, grid, "e"),
                                 _field(h, grid, "h"), _stream(stream, grid), C.byref(st)),
-          "paraexp_expmv")
+          "paraexp_expmv", st)
     return st.as_dict()
 
 
@@ -265,10 +267,11 @@ def partition(nsteps: int, p: int) -> list:
     return list(out)
 
 
-def schedule(p: int, world: int, rank: int) -> tuple:
+def schedule(p: int, world: int, rank: int, tail_ratio: float = 0.0, has_u0: bool = False) -> tuple:
+    """paraexp_schedule: (first, last, root); tail_ratio <= 0 gives equal shares."""
     f, l, r = C.c_int32(), C.c_int32(), C.c_int32()
-    check(abi.lib.paraexp_schedule(int(p), int(world), int(rank), C.byref(f), C.byref(l),
-                                   C.byref(r)), "paraexp_schedule")
+    check(abi.lib.paraexp_schedule(int(p), int(world), int(rank), float(tail_ratio), int(bool(has_u0)),
+                                   C.byref(f), C.byref(l), C.byref(r)), "paraexp_schedule")
     return f.value, l.value, r.value
 
 
@@ -314,13 +317,17 @@ class Comm:
             self._h = None
 
 
+def _tail_mode(tail_mode):
+    return tail_mode if isinstance(tail_mode, int) else {"exp": TAIL_EXP, "leapfrog": TAIL_LEAPFROG}[tail_mode]
+
+
 def solve(grid: Grid, nsteps: int, p: int, sources=None, t0: float = 0.0, method="leja", m=0,
           s=0, eps_A=1e-12, rho=0.0, tail_mode=TAIL_EXP, u0=None, e_out=None, h_out=None,
           comm: Optional[Comm] = None, broadcast_out=False, stream=None, early_term=False,
-          beta=0.0) -> dict:
+          beta=0.0, rho_check=0) -> dict:
     """paraexp_solve (Algorithm 1): returns the stats dict; output in e_out/h_out."""
     arr, n = make_sources(sources)
-    o = _opts(method, m, s, eps_A, rho, early_term, beta)
+    o = _opts(method, m, s, eps_A, rho, early_term, beta, rho_check)
     st = abi.paraexp_stats()
     e0 = h0 = C.c_void_p(0)
     if u0 is not None:
@@ -328,11 +335,11 @@ def solve(grid: Grid, nsteps: int, p: int, sources=None, t0: float = 0.0, method
         h0 = _field(u0[1], grid, "h0")
     eo = _field(e_out, grid, "e_out") if e_out is not None else C.c_void_p(0)
     ho = _field(h_out, grid, "h_out") if h_out is not None else C.c_void_p(0)
-    tm = tail_mode if isinstance(tail_mode, int) else {"exp": TAIL_EXP, "leapfrog": TAIL_LEAPFROG}[tail_mode]
+    tm = _tail_mode(tail_mode)
     check(abi.lib.paraexp_solve(grid.handle, comm.handle if comm else C.c_void_p(0), arr, n,
                                 float(t0), int(nsteps), int(p), C.byref(o), tm,
                                 int(bool(broadcast_out)), e0, h0, eo, ho, _stream(stream, grid),
-                                C.byref(st)), "paraexp_solve")
+                                C.byref(st)), "paraexp_solve", st)
     return st.as_dict()
 
 
@@ -355,9 +362,43 @@ def solve_trace(grid: Grid, nsteps: int, p: int, sources=None, t0: float = 0.0, 
     check(abi.lib.paraexp_solve_trace(grid.handle, comm.handle if comm else C.c_void_p(0), arr, n,
                                       float(t0), int(nsteps), int(p), C.byref(o),
                                       int(bool(broadcast_out)), e0, h0, eo, ho, C.byref(t),
-                                      _stream(stream, grid), C.byref(st)), "paraexp_solve_trace")
+                                      _stream(stream, grid), C.byref(st)), "paraexp_solve_trace", st)
     if pr is not None:
         pr = pr[:p * len(probes)].view(p, len(probes))
     if en is not None:
         en = en[:p]
     return st.as_dict(), en, pr
+
+
+def solve_block(grid: Grid, rank: int, world: int, nsteps: int, p: int, w, sources=None,
+                t0: float = 0.0, method="leja", m=0, s=0, eps_A=1e-12, rho=0.0, tail_mode=TAIL_EXP,
+                u0=None, v=None, stream=None, early_term=False, beta=0.0, rho_check=0) -> dict:
+    """paraexp_solve_block: this rank's tails W (written into the tensor pair w = (w_e, w_h))
+    and, on the root (stats['root'] == rank), its particular state into v = (v_e, v_h)."""
+    arr, n = make_sources(sources)
+    o = _opts(method, m, s, eps_A, rho, early_term, beta, rho_check)
+    st = abi.paraexp_stats()
+    e0 = h0 = C.c_void_p(0)
+    if u0 is not None:
+        e0, h0 = _field(u0[0], grid, "e0"), _field(u0[1], grid, "h0")
+    ve = vh = C.c_void_p(0)
+    if v is not None:
+        ve, vh = _field(v[0], grid, "v_e"), _field(v[1], grid, "v_h")
+    check(abi.lib.paraexp_solve_block(grid.handle, int(rank), int(world), arr, n, float(t0), int(nsteps),
+                                      int(p), C.byref(o), _tail_mode(tail_mode), e0, h0,
+                                      _field(w[0], grid, "w_e"), _field(w[1], grid, "w_h"), ve, vh,
+                                      _stream(stream, grid), C.byref(st)), "paraexp_solve_block", st)
+    return st.as_dict()
+
+
+def solve_finish(grid: Grid, w, v, e_out, h_out, method="leja", eps_A=1e-12, rho=0.0,
+                 tail_mode=TAIL_EXP, stream=None) -> dict:
+    """paraexp_solve_finish: reconstruction on the root from the summed W and its v."""
+    o = _opts(method, 0, 0, eps_A, rho)
+    st = abi.paraexp_stats()
+    check(abi.lib.paraexp_solve_finish(grid.handle, C.byref(o), _tail_mode(tail_mode),
+                                       _field(w[0], grid, "w_e"), _field(w[1], grid, "w_h"),
+                                       _field(v[0], grid, "v_e"), _field(v[1], grid, "v_h"),
+                                       _field(e_out, grid, "e_out"), _field(h_out, grid, "h_out"),
+                                       _stream(stream, grid), C.byref(st)), "paraexp_solve_finish", st)
+    return st.as_dict()

@@ -65,7 +65,8 @@ class paraexp_stats(C.Structure):
                 ("fail_interval", C.c_int32), ("ms_particular", C.c_double),
                 ("ms_tails", C.c_double), ("ms_reduce", C.c_double), ("ms_finish", C.c_double),
                 ("ms_total", C.c_double), ("ms_leapfrog_kernels", C.c_double),
-                ("ms_poly_kernels", C.c_double)]
+                ("ms_poly_kernels", C.c_double), ("rho_fallback", C.c_int32),
+                ("norm_deviation", C.c_double)]
 
     def as_dict(self):
         return {f[0]: getattr(self, f[0]) for f in self._fields_}
@@ -73,7 +74,8 @@ class paraexp_stats(C.Structure):
 
 class paraexp_expmv_opts(C.Structure):
     _fields_ = [("method", C.c_int32), ("m", C.c_int32), ("s", C.c_int32), ("eps_A", C.c_double),
-                ("rho", C.c_double), ("early_term", C.c_int32), ("beta", C.c_double)]
+                ("rho", C.c_double), ("early_term", C.c_int32), ("beta", C.c_double),
+                ("rho_check", C.c_int32)]
 
 
 class paraexp_plan_info(C.Structure):
@@ -116,8 +118,14 @@ _sigs = {
                                       _vp, _vp, _vp, _vp, C.POINTER(paraexp_trace), _vp,
                                       C.POINTER(paraexp_stats)]),
     "paraexp_partition": (C.c_int, [C.c_int64, C.c_int32, C.POINTER(C.c_int64)]),
-    "paraexp_schedule": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
-                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "paraexp_schedule": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32,
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "paraexp_solve_block": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(paraexp_source), C.c_int32,
+                                      C.c_double, C.c_int64, C.c_int32, C.POINTER(paraexp_expmv_opts),
+                                      C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                      C.POINTER(paraexp_stats)]),
+    "paraexp_solve_finish": (C.c_int, [_vp, C.POINTER(paraexp_expmv_opts), C.c_int32, _vp, _vp, _vp, _vp,
+                                       _vp, _vp, _vp, C.POINTER(paraexp_stats)]),
     "paraexp_leja_points": (C.c_int, [C.c_int32, _dp]),
     "paraexp_plan_host": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                     C.c_double, C.c_double, C.POINTER(paraexp_plan_info)]),
@@ -142,7 +150,11 @@ class ParaexpError(RuntimeError):
         super().__init__(f"{where}: {lib.paraexp_strerror(code).decode()} ({code}): {msg}")
 
 
-def check(code, where):
+def check(code, where, stats=None):
+    """Raise ParaexpError for a negative status; the call's stats (e.g. fail_interval) ride
+    along as ``err.stats``."""
     if code < 0:
-        raise ParaexpError(code, where)
+        err = ParaexpError(code, where)
+        err.stats = stats.as_dict() if stats is not None else None
+        raise err
     return code

@@ -3,12 +3,15 @@
 // See include/paraexp.h for the contract of every function.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -38,6 +41,31 @@ static int ensure_ws(Grid &G, int n) {
     }
     return PARAEXP_OK;
 }
+
+// ---- stream order across calls -----------------------------------------------------------
+// Calls on one grid share its workspaces (ws, the source table, the schedule counter), so a
+// call enqueued on another stream than the previous call first waits for the previous call's
+// work (an event recorded at the end of every call).
+struct CallScope {
+    Grid &G;
+    void *stream;
+    CallScope(Grid &g, void *s) : G(g), stream(s) {
+        if (G.call_event && G.call_stream != stream)
+            cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)G.call_event, 0);
+    }
+    ~CallScope() {
+        if (!G.call_event) dev_event_create(&G.call_event);
+        if (G.call_event) cudaEventRecord((cudaEvent_t)G.call_event, (cudaStream_t)stream);
+        G.call_stream = stream;
+    }
+};
+
+// the driver's view of a communicator (rho broadcast); empty for one rank / no comm
+struct CommView {
+    void *ctx = nullptr;
+    int (*bcast_rho)(void *ctx, double *rho, void *stream) = nullptr;
+};
+typedef CommView paraexp_comm_view;
 
 // ---- concurrent particular sweeps ------------------------------------------------------------
 // On by default for grids of at most 2^19 cells (64^3: one fused sweep covers ~128 (tile, chunk)
@@ -527,7 +555,7 @@ static int run_plan(const KernelArgs &ka, const Plan &plan, void *bufs[4], parae
 }
 
 static int opts_plan(Grid &G, double tau, const paraexp_expmv_opts *o, double rho, Plan &plan) {
-    paraexp_expmv_opts def{PARAEXP_LEJA, 0, 0, 1e-12, 0.0, 0, 0.0};
+    paraexp_expmv_opts def{PARAEXP_LEJA, 0, 0, 1e-12, 0.0, 0, 0.0, 0};
     if (!o) o = &def;
     double eps = o->eps_A;
     if (eps == 0.0 && o->beta > 0) {   // eq:tolerance_leja_2 (f2, reading 30)
@@ -541,6 +569,27 @@ static int opts_plan(Grid &G, double tau, const paraexp_expmv_opts *o, double rh
     plan.early_term = o->early_term != 0;
     plan.eps_A = eps;
     return PARAEXP_OK;
+}
+
+// rho safety net (SURVEY finding 8): on when rho came from the K5 estimate (or opts->rho_check
+// > 0), never for Krylov (norm-preserving by construction) or when rho is already rho_cfl.
+static void schedule_blocks(int p, int world, double ratio, bool u0, std::vector<int> &F,
+                            std::vector<int> &L, int &root);
+static int ensure_norms(Grid &G);
+
+static bool rho_check_on(const Grid &G, const paraexp_expmv_opts *o, double rho) {
+    const int mode = o ? o->rho_check : 0;
+    const bool explicit_rho = o && o->rho > 0;
+    if (o && o->method == PARAEXP_KRYLOV) return false;
+    return (mode > 0 || (mode == 0 && !explicit_rho)) && rho < G.rho_cfl;
+}
+// tolerance on | ||p(X)^s b||_M / ||b||_M - 1 |: the planner bounds the forward error per
+// substep by eps_A theta (reading 16), i.e. eps_A rho tau over the propagator; fixed plans
+// and fp32 rounding get a floor.  A rho that misses the spectrum makes the polynomial grow
+// exponentially outside the Leja interval, far beyond either bound.
+static double norm_tol(const Grid &G, const Plan &P, bool auto_plan) {
+    const double floor_tol = G.dtype == PARAEXP_F64 ? 1e-9 : 1e-3;
+    return auto_plan ? std::max(floor_tol, 10.0 * P.eps_A * P.rho * P.tau) : std::max(floor_tol, 1e-3);
 }
 
 }  // namespace pe
@@ -563,6 +612,13 @@ struct NcclApi {
     ncclResult_t (*Broadcast)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    // optional (checked at use): async error polling, abort, symmetric windows (NCCL >= 2.27)
+    ncclResult_t (*GetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+    ncclResult_t (*MemAlloc)(void **, size_t) = nullptr;
+    ncclResult_t (*MemFree)(void *) = nullptr;
+    ncclResult_t (*WindowRegister)(ncclComm_t, void *, size_t, void **, int) = nullptr;
+    ncclResult_t (*WindowDeregister)(ncclComm_t, void *) = nullptr;
 };
 NcclApi g_nccl;
 const int kNcclSum = 0, kNcclF32 = 7, kNcclF64 = 8;
@@ -582,6 +638,12 @@ int load_nccl() {
     g_nccl.Broadcast = (decltype(g_nccl.Broadcast))dlsym(h, "ncclBroadcast");
     g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
     g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+    g_nccl.GetAsyncError = (decltype(g_nccl.GetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+    g_nccl.CommAbort = (decltype(g_nccl.CommAbort))dlsym(h, "ncclCommAbort");
+    g_nccl.MemAlloc = (decltype(g_nccl.MemAlloc))dlsym(h, "ncclMemAlloc");
+    g_nccl.MemFree = (decltype(g_nccl.MemFree))dlsym(h, "ncclMemFree");
+    g_nccl.WindowRegister = (decltype(g_nccl.WindowRegister))dlsym(h, "ncclCommWindowRegister");
+    g_nccl.WindowDeregister = (decltype(g_nccl.WindowDeregister))dlsym(h, "ncclCommWindowDeregister");
     if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.CommDestroy || !g_nccl.Reduce ||
         !g_nccl.Broadcast || !g_nccl.AllReduce || !g_nccl.GetErrorString)
         return pe::fail(PARAEXP_ENCCL, "libnccl.so.2 lacks required symbols");
@@ -597,7 +659,102 @@ int nccl_check(ncclResult_t r, const char *what) {
 struct paraexp_comm {
     ncclComm_t comm;
     int rank, world, device;
+    bool aborted = false;
+    void *win_buf = nullptr;    // ncclMemAlloc'd reduce buffer registered as a symmetric window
+    size_t win_bytes = 0;
+    void *win = nullptr;
 };
+
+namespace {
+// Wait for `stream` while polling NCCL's asynchronous error state: a failed peer would
+// otherwise leave cudaStreamSynchronize blocked forever.  On an error the communicator is
+// aborted (it must then only be destroyed) and ENCCL returned.
+int comm_wait(paraexp_comm *comm, void *stream) {
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery((cudaStream_t)stream);
+        if (q == cudaSuccess) return PARAEXP_OK;
+        if (q != cudaErrorNotReady) return pe::check_cuda("stream query");
+        if (g_nccl.GetAsyncError && !comm->aborted) {
+            ncclResult_t ae = 0;
+            g_nccl.GetAsyncError(comm->comm, &ae);
+            if (ae != 0 && ae != 7 /* ncclInProgress */) {
+                if (g_nccl.CommAbort) g_nccl.CommAbort(comm->comm);
+                comm->aborted = true;
+                return pe::fail(PARAEXP_ENCCL, std::string("NCCL asynchronous error: ") + g_nccl.GetErrorString(ae));
+            }
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+}
+
+struct CommCtx {
+    paraexp_comm *comm;
+    pe::Grid *G;
+};
+
+// every rank takes rank 0's rho (the K5 estimate uses atomics and can differ in the last bits)
+int bcast_rho_nccl(void *ctx, double *rho, void *stream) {
+    CommCtx *c = (CommCtx *)ctx;
+    double *d = (double *)c->G->d_red;
+    int rc = pe::dev_memcpy_h2d_async(d, rho, sizeof(double), stream);
+    if (rc) return rc;
+    if ((rc = nccl_check(g_nccl.Broadcast(d, d, 1, kNcclF64, 0, c->comm->comm, (cudaStream_t)stream),
+                         "ncclBroadcast(rho)"))) return rc;
+    if ((rc = comm_wait(c->comm, stream))) return rc;
+    return pe::dev_memcpy_d2h(rho, d, sizeof(double), stream);
+}
+
+// a8: W summed onto the root.  With PARAEXP_NCCL_WINDOW=1 the reduction runs on an
+// ncclMemAlloc'd buffer registered as a symmetric window (NCCL_WIN_COLL_SYMMETRIC: lets NCCL
+// use NVLS / symmetric kernels); W is staged through it with two device copies.
+int comm_reduce_W(paraexp_comm *comm, const pe::Grid &G, void *W, size_t bytes, int root, void *stream) {
+    const int dt = G.dtype == PARAEXP_F64 ? kNcclF64 : kNcclF32;
+    const size_t n = bytes / G.esize();
+    const char *w = getenv("PARAEXP_NCCL_WINDOW");
+    if (w && atoi(w) != 0) {
+        if (!g_nccl.MemAlloc || !g_nccl.WindowRegister)
+            return pe::fail(PARAEXP_ENCCL, "PARAEXP_NCCL_WINDOW: NCCL lacks ncclMemAlloc / ncclCommWindowRegister");
+        if (comm->win_bytes < bytes) {
+            if (comm->win && g_nccl.WindowDeregister) g_nccl.WindowDeregister(comm->comm, comm->win);
+            if (comm->win_buf && g_nccl.MemFree) g_nccl.MemFree(comm->win_buf);
+            comm->win = comm->win_buf = nullptr;
+            comm->win_bytes = 0;
+            int rc = nccl_check(g_nccl.MemAlloc(&comm->win_buf, bytes), "ncclMemAlloc");
+            if (rc) return rc;
+            if ((rc = nccl_check(g_nccl.WindowRegister(comm->comm, comm->win_buf, bytes, &comm->win, 1),
+                                 "ncclCommWindowRegister"))) return rc;
+            comm->win_bytes = bytes;
+        }
+        if (cudaMemcpyAsync(comm->win_buf, W, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) != cudaSuccess)
+            return pe::check_cuda("window stage");
+        int rc = nccl_check(g_nccl.Reduce(comm->win_buf, comm->win_buf, n, dt, kNcclSum, root, comm->comm,
+                                          (cudaStream_t)stream), "ncclReduce");
+        if (rc) return rc;
+        if (comm->rank == root &&
+            cudaMemcpyAsync(W, comm->win_buf, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) != cudaSuccess)
+            return pe::check_cuda("window unstage");
+        return PARAEXP_OK;
+    }
+    return nccl_check(g_nccl.Reduce(W, W, n, dt, kNcclSum, root, comm->comm, (cudaStream_t)stream), "ncclReduce");
+}
+
+int comm_allreduce_trace(paraexp_comm *comm, const pe::TraceDev &tr, int p, void *stream) {
+    int rc = PARAEXP_OK;
+    if (tr.np > 0)
+        rc = nccl_check(g_nccl.AllReduce(tr.probe, tr.probe, (size_t)p * tr.np, kNcclF64, kNcclSum, comm->comm,
+                                         (cudaStream_t)stream), "ncclAllReduce");
+    if (!rc && tr.energy)
+        rc = nccl_check(g_nccl.AllReduce(tr.energy, tr.energy, (size_t)p, kNcclF64, kNcclSum, comm->comm,
+                                         (cudaStream_t)stream), "ncclAllReduce");
+    return rc;
+}
+
+int comm_bcast_state(paraexp_comm *comm, const pe::Grid &G, void *P, int root, void *stream) {
+    const int dt = G.dtype == PARAEXP_F64 ? kNcclF64 : kNcclF32;
+    return nccl_check(g_nccl.Broadcast(P, P, (size_t)G.L.state_elems(), dt, root, comm->comm,
+                                       (cudaStream_t)stream), "ncclBroadcast");
+}
+}  // namespace
 
 extern "C" {
 
@@ -628,23 +785,15 @@ int paraexp_partition(int64_t nsteps, int32_t p, int64_t *bounds) {
     return PARAEXP_OK;
 }
 
-int paraexp_schedule(int32_t p, int32_t world, int32_t rank, int32_t *first, int32_t *last,
-                     int32_t *root) {
+int paraexp_schedule(int32_t p, int32_t world, int32_t rank, double tail_ratio, int32_t has_u0,
+                     int32_t *first, int32_t *last, int32_t *root) {
     if (p < 1 || world < 1 || rank < 0 || rank >= world) return pe::fail(PARAEXP_EINVAL, "bad schedule arguments");
-    // contiguous blocks; ranks with longer tails (earlier blocks) get the smaller share
-    const int active = std::min(p, world);
-    const int base = p / active, rem = p % active;
-    int f = 0, l = -1;
-    if (rank < active) {
-        // ranks active-rem .. active-1 get base+1
-        int start = 1;
-        for (int r = 0; r < rank; ++r) start += base + (r >= active - rem ? 1 : 0);
-        f = start;
-        l = start + base + (rank >= active - rem ? 1 : 0) - 1;
-    }
-    if (first) *first = f;
-    if (last) *last = l;
-    if (root) *root = active - 1;
+    std::vector<int> F, L;
+    int r = 0;
+    pe::schedule_blocks(p, world, tail_ratio, has_u0 != 0, F, L, r);
+    if (first) *first = F[rank];
+    if (last) *last = L[rank];
+    if (root) *root = r;
     return PARAEXP_OK;
 }
 
@@ -655,6 +804,7 @@ int paraexp_grid_info(paraexp_grid *grid, int32_t compute_rho_pow, void *stream,
     if (compute_rho_pow && G.device >= 0 && G.rho_pow == 0) {
         int64_t launches = 0;
         pe::dev_set_device(G.device);
+        pe::CallScope scope(G, stream);
         int rc = pe::compute_rho_pow(G, stream, &launches);
         if (rc) return rc;
     }
@@ -709,6 +859,11 @@ static int leapfrog_impl(paraexp_grid *grid, const paraexp_source *src, int32_t 
     S = paraexp_stats();
     int rc = dev_set_device(G.device);
     if (rc) return rc;
+    CallScope scope(G, stream);
+    nvtxRangePushA("paraexp_leapfrog");
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop;
     std::vector<SrcDev> sd;
     if ((rc = prepare_sources(G, src, nsrc, t0, 0, nsteps, stream, sd))) return rc;
     TraceDev tr;
@@ -776,18 +931,47 @@ int paraexp_expmv(paraexp_grid *grid, double tau, const paraexp_expmv_opts *opts
     S = paraexp_stats();
     int rc = dev_set_device(G.device);
     if (rc) return rc;
-    const double rho = default_rho(G, opts, stream, &S.kernel_launches, &rc);
+    CallScope scope(G, stream);
+    nvtxRangePushA("paraexp_expmv");
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop;
+    double rho = default_rho(G, opts, stream, &S.kernel_launches, &rc);
     if (rc) return rc;
     Plan plan;
     if ((rc = opts_plan(G, tau, opts, rho, plan))) return rc;
-    if ((rc = ensure_ws(G, 4))) return rc;
+    const bool chk = tau > 0 && rho_check_on(G, opts, rho);
+    if ((rc = ensure_ws(G, chk ? 5 : 4)) || (rc = ensure_norms(G))) return rc;
     KernelArgs ka{&G, stream, &S.kernel_launches};
     Events ev(stream);
     const int id = ev.open(4);
     void *bufs[4] = {G.ws[0], G.ws[1], G.ws[2], G.ws[3]};
     bool host_io = false;
     if ((rc = pack_any(ka, G, e, h, bufs[0], &host_io))) return rc;
+    double *nrm = (double *)G.d_norms;
+    const size_t sbytes = (size_t)G.L.state_elems() * G.esize();
+    if (chk) {   // rho safety net: keep the input, compare energy norms before / after
+        if ((rc = dev_memset_async(nrm, 0, 2 * sizeof(double), stream)) ||
+            (rc = k_dot_M_async(ka, bufs[0], bufs[0], nrm, G.dt)) ||
+            (rc = dev_memcpy_d2d_async(G.ws[4], bufs[0], sbytes, stream))) return rc;
+    }
     if ((rc = run_plan(ka, plan, bufs, &S, &ev))) return rc;
+    if (chk) {
+        double n2[2];
+        if ((rc = k_dot_M_async(ka, bufs[0], bufs[0], nrm + 1, G.dt)) ||
+            (rc = dev_memcpy_d2h(n2, nrm, 2 * sizeof(double), stream))) return rc;
+        const double dev = n2[0] > 0 ? std::fabs(std::sqrt(n2[1] / n2[0]) - 1.0) : 0.0;
+        S.norm_deviation = dev;
+        if (!(dev <= norm_tol(G, plan, !(opts && opts->m > 0)))) {
+            S.rho_fallback = 1;
+            rho = G.rho_cfl;
+            if ((rc = opts_plan(G, tau, opts, rho, plan))) return rc;
+            if ((rc = dev_memcpy_d2d_async(bufs[0], G.ws[4], sbytes, stream))) return rc;
+            S.a_applications = 0;
+            S.substeps = 0;
+            if ((rc = run_plan(ka, plan, bufs, &S, &ev))) return rc;
+        }
+    }
     if ((rc = unpack_any(ka, G, bufs[0], e, h, &host_io))) return rc;
     ev.close(id);
     S.rho = rho;
@@ -832,146 +1016,253 @@ int paraexp_comm_create(const uint8_t id[128], int32_t rank, int32_t world, int3
 
 void paraexp_comm_destroy(paraexp_comm *comm) {
     if (!comm) return;
-    if (g_nccl.ok) g_nccl.CommDestroy(comm->comm);
+    if (g_nccl.ok && !comm->aborted) {
+        if (comm->win && g_nccl.WindowDeregister) g_nccl.WindowDeregister(comm->comm, comm->win);
+        g_nccl.CommDestroy(comm->comm);
+    }
+    if (comm->win_buf && g_nccl.MemFree) g_nccl.MemFree(comm->win_buf);
     delete comm;
 }
 
-static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
-                      int32_t nsrc, double t0, int64_t nsteps, int32_t p,
-                      const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
-                      const void *e0, const void *h0, void *e_out, void *h_out,
-                      const paraexp_trace *trace, void *stream, paraexp_stats *st);
+}  // extern "C"
 
-int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
-                  int32_t nsrc, double t0, int64_t nsteps, int32_t p,
-                  const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
-                  const void *e0, const void *h0, void *e_out, void *h_out, void *stream,
-                  paraexp_stats *st) {
-    return solve_impl(grid, comm, src, nsrc, t0, nsteps, p, opts, tail_mode, broadcast_out, e0, h0, e_out,
-                      h_out, nullptr, stream, st);
+// =====================================================================================
+// ParaExp driver (Algorithm 1): block (a4, a7) -> reduce (a8) -> finish (a9)
+// =====================================================================================
+namespace pe {
+
+struct SolveCtx {
+    int64_t nsteps = 0;
+    int p = 0, rank = 0, world = 1, first = 0, last = -1, root = 0;
+    int tail_mode = PARAEXP_TAIL_EXP;
+    bool has_u0 = false;
+    bool rho_check = false;     // norm-preservation check of every propagator (SURVEY finding 8)
+    bool auto_plan = true;      // (m, s) chosen by the planner (eps_A meaningful for the check)
+    double rho = 0, ratio = 0;
+    std::vector<int64_t> B;
+    std::map<int64_t, Plan> plans;
+    Plan half;
+    const paraexp_expmv_opts *opts = nullptr;
+};
+
+struct SolveBufs {
+    void *P = nullptr;          // particular state of the current / last sub-interval
+    void *W = nullptr;          // Horner accumulator of the tails
+    void *X[3] = {nullptr, nullptr, nullptr};
+};
+
+// one plan per distinct sub-interval length plus the dt/2 shift plan (reading 10)
+static int build_plans(Grid &G, SolveCtx &c) {
+    c.plans.clear();
+    for (int i = 1; i <= c.p; ++i) {
+        const int64_t M = c.B[i] - c.B[i - 1];
+        if (!c.plans.count(M)) {
+            Plan pl;
+            int rc = opts_plan(G, M * G.dt, c.opts, c.rho, pl);
+            if (rc) return rc;
+            c.plans[M] = pl;
+        }
+    }
+    const double theta = c.rho * G.dt * 0.5;
+    const int sh = std::max(1, (int)std::ceil(theta));
+    return make_plan(PARAEXP_TAYLOR, 24, sh, 0.0, 0.5 * G.dt, c.rho, G.dt, c.half);
 }
 
-int paraexp_solve_trace(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
-                        int32_t nsrc, double t0, int64_t nsteps, int32_t p,
-                        const paraexp_expmv_opts *opts, int32_t broadcast_out, const void *e0,
-                        const void *h0, void *e_out, void *h_out, const paraexp_trace *trace,
-                        void *stream, paraexp_stats *st) {
-    return solve_impl(grid, comm, src, nsrc, t0, nsteps, p, opts, PARAEXP_TAIL_EXP, broadcast_out, e0, h0,
-                      e_out, h_out, trace, stream, st);
+// Cost of one propagator E_i relative to one sub-interval's leapfrog sweep.  The fused pair
+// kernel streams the same bytes per A-application as the leapfrog kernel per step,
+// so the ratio is A-applications of E_i over steps of sub-interval i.
+static double tail_ratio(const SolveCtx &c) {
+    if (c.tail_mode == PARAEXP_TAIL_LEAPFROG) return 1.0;
+    const Plan &P = c.plans.at(c.B[1] - c.B[0]);
+    return (double)P.m * P.s / (double)(c.B[1] - c.B[0]);
 }
 
-static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
-                      int32_t nsrc, double t0, int64_t nsteps, int32_t p,
-                      const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
-                      const void *e0, const void *h0, void *e_out, void *h_out,
-                      const paraexp_trace *trace, void *stream, paraexp_stats *st) {
-    using namespace pe;
-    if (!grid) return fail(PARAEXP_EINVAL, "null grid");
-    Grid &G = grid->g;
-    if (G.device < 0) return fail(PARAEXP_ENOTSUP, "host-only grid");
+// Contiguous blocks of sub-intervals, cost-balanced: rank r owning [f, l] costs
+// (l - f + 1) sweeps + (p - f) propagators (+ one more for the u0 tail if f = 1), in units of a
+// sweep with propagator/sweep = ratio.  The smallest makespan C is found by bisection; the
+// forward greedy at C (each rank takes as many sub-intervals as fit) realises it and uses the
+// fewest ranks -- with Horner tails that is also the least total work.  ratio <= 0: equal
+// shares, the remainder to the later ranks (earlier blocks carry the longer tails).
+static void schedule_blocks(int p, int world, double ratio, bool u0, std::vector<int> &F,
+                            std::vector<int> &L, int &root) {
+    F.assign(world, 0);
+    L.assign(world, -1);
+    const int active = std::min(p, world);
+    if (!(ratio > 0) || active == 1) {
+        const int base = p / active, rem = p % active;
+        int start = 1;
+        for (int r = 0; r < active; ++r) {
+            const int n = base + (r >= active - rem ? 1 : 0);
+            F[r] = start;
+            L[r] = start + n - 1;
+            start += n;
+        }
+        root = active - 1;
+        return;
+    }
+    auto greedy = [&](double C, bool assign) -> bool {
+        int f = 1;
+        for (int r = 0; r < active && f <= p; ++r) {
+            const double tail = (p - f) * ratio + (f == 1 && u0 ? ratio : 0.0);
+            int n = (int)std::floor(C - tail + 1e-9);
+            if (n < 1) return false;
+            n = std::min(n, p - f + 1);
+            if (assign) {
+                F[r] = f;
+                L[r] = f + n - 1;
+            }
+            f += n;
+        }
+        return f > p;
+    };
+    double lo = (p - 1) * ratio + (u0 ? ratio : 0.0), hi = lo + p;   // lo infeasible, hi feasible
+    for (int it = 0; it < 200 && hi - lo > 1e-9 * hi; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (greedy(mid, false)) hi = mid; else lo = mid;
+    }
+    greedy(hi, true);
+    root = 0;
+    for (int r = 0; r < world; ++r)
+        if (L[r] == p) root = r;
+}
+
+// ---- debug fault injection (PARAEXP_DEBUG_NAN=particular:<i> | tail:<i>) --
+// Writes one NaN into a live interior e_x entry after sub-interval i's particular sweep or
+// after propagator E_i, so the tests can check that EDIVERGED / EOVERFLOW name interval i.
+struct NanHook {
+    int particular = 0, tail = 0;
+    NanHook() {
+        const char *e = getenv("PARAEXP_DEBUG_NAN");
+        if (!e) return;
+        if (!strncmp(e, "particular:", 11)) particular = atoi(e + 11);
+        if (!strncmp(e, "tail:", 5)) tail = atoi(e + 5);
+    }
+};
+static int inject_nan(const Grid &G, void *state, void *stream) {
+    static const double nan64 = std::nan("");
+    static const float nan32 = std::nanf("");
+    const int64_t off = G.nx / 2 + G.L.px * (G.ny / 2 + (int64_t)G.ny * (G.nz / 2));
+    char *dst = (char *)state + off * G.esize();
+    const void *src = G.dtype == PARAEXP_F64 ? (const void *)&nan64 : (const void *)&nan32;
+    return dev_memcpy_h2d_async(dst, src, G.esize(), stream) ? PARAEXP_ECUDA : dev_sync(stream);
+}
+
+static int ensure_norms(Grid &G) {
+    if (G.d_norms) return PARAEXP_OK;
+    int rc = dev_alloc(&G.d_norms, sizeof(double) * 2 * 1002);
+    if (!rc) G.device_bytes += sizeof(double) * 2 * 1002;
+    return rc;
+}
+
+// Resolve the plans, rho and this rank's block.  rho: opts->rho, else min(rho_cfl,
+// 1.05 rho_pow) (reading 17), broadcast from rank 0 when a communicator spans several ranks so
+// that every rank builds the same plans.
+static int solve_prepare(Grid &G, paraexp_comm_view comm, int rank, int world,
+                         const paraexp_expmv_opts *opts, int64_t nsteps, int p, int tail_mode,
+                         bool has_u0, void *stream, paraexp_stats &S, SolveCtx &c) {
     if (p < 1 || nsteps < p) return fail(PARAEXP_EINVAL, "need p >= 1 and nsteps >= p");
     if (p > 1000) return fail(PARAEXP_EINVAL, "p > 1000 not supported");
     if (tail_mode != PARAEXP_TAIL_EXP && tail_mode != PARAEXP_TAIL_LEAPFROG) return fail(PARAEXP_EINVAL, "bad tail mode");
-    if ((e0 == nullptr) != (h0 == nullptr)) return fail(PARAEXP_EINVAL, "e0 and h0 must both be given or both NULL");
-    if (trace && tail_mode != PARAEXP_TAIL_EXP) return fail(PARAEXP_EINVAL, "trace needs tail_mode EXP");
-    const int rank = comm ? comm->rank : 0, world = comm ? comm->world : 1;
-    paraexp_stats local{};
-    paraexp_stats &S = st ? *st : local;
-    S = paraexp_stats();
-    int rc = dev_set_device(G.device);
+    if (world < 1 || rank < 0 || rank >= world) return fail(PARAEXP_EINVAL, "bad rank / world");
+    c.nsteps = nsteps;
+    c.p = p;
+    c.rank = rank;
+    c.world = world;
+    c.tail_mode = tail_mode;
+    c.has_u0 = has_u0;
+    c.opts = opts;
+    c.B.assign(p + 1, 0);
+    paraexp_partition(nsteps, p, c.B.data());
+    int rc;
+    c.rho = default_rho(G, opts, stream, &S.kernel_launches, &rc);
     if (rc) return rc;
-    std::vector<int64_t> B(p + 1);
-    paraexp_partition(nsteps, p, B.data());
-    int first, last, root;
-    paraexp_schedule(p, world, rank, &first, &last, &root);
-    S.first_interval = first;
-    S.last_interval = last;
-    S.root = root;
-    const bool has_u0 = e0 != nullptr;
+    if (comm.bcast_rho && (rc = comm.bcast_rho(comm.ctx, &c.rho, stream))) return rc;
+    const int mode = opts ? opts->rho_check : 0;
+    const bool explicit_rho = opts && opts->rho > 0;
+    c.rho_check = tail_mode == PARAEXP_TAIL_EXP && !(opts && opts->method == PARAEXP_KRYLOV) &&
+                  (mode > 0 || (mode == 0 && !explicit_rho)) && c.rho < G.rho_cfl;
+    c.auto_plan = !(opts && opts->m > 0);
+    if ((rc = build_plans(G, c))) return rc;
+    c.ratio = tail_ratio(c);
+    std::vector<int> F, L;
+    schedule_blocks(p, world, c.ratio, has_u0, F, L, c.root);
+    c.first = F[rank];
+    c.last = L[rank];
+    S.first_interval = c.first;
+    S.last_interval = c.last;
+    S.root = c.root;
+    return PARAEXP_OK;
+}
 
-    double rho = default_rho(G, opts, stream, &S.kernel_launches, &rc);
-    if (rc) return rc;
-    if (comm && world > 1 && !(opts && opts->rho > 0)) {
-        // every rank must build the same plans: the K5 estimate (atomics) can differ in the
-        // last bits between ranks, so all ranks take rank 0's value
-        double *d = (double *)G.d_red;
-        if ((rc = dev_memcpy_h2d_async(d, &rho, sizeof(double), stream))) return rc;
-        if ((rc = nccl_check(g_nccl.Broadcast(d, d, 1, kNcclF64, 0, comm->comm, (cudaStream_t)stream),
-                             "ncclBroadcast(rho)"))) return rc;
-        if ((rc = dev_memcpy_d2h(&rho, d, sizeof(double), stream))) return rc;
-    }
-    S.rho = rho;
-    // one plan per distinct sub-interval length, plus the dt/2 shift plan
-    std::map<int64_t, Plan> plans;
-    for (int i = 1; i <= p; ++i) {
-        const int64_t M = B[i] - B[i - 1];
-        if (!plans.count(M)) {
-            Plan pl;
-            if ((rc = opts_plan(G, M * G.dt, opts, rho, pl))) return rc;
-            plans[M] = pl;
-        }
-    }
-    Plan half;
-    {
-        const double theta = rho * G.dt * 0.5;
-        const int sh = std::max(1, (int)std::ceil(theta));
-        if ((rc = make_plan(PARAEXP_TAYLOR, 24, sh, 0.0, 0.5 * G.dt, rho, G.dt, half))) return rc;
-    }
-    const Plan &P1 = plans[B[1] - B[0]];
-    const Plan &Pp = plans[B[p] - B[p - 1]];
+static void plan_stats(const SolveCtx &c, paraexp_stats &S) {
+    const Plan &P1 = c.plans.at(c.B[1] - c.B[0]);
+    const Plan &Pp = c.plans.at(c.B[c.p] - c.B[c.p - 1]);
+    S.rho = c.rho;
     S.method = P1.method;
     S.m = P1.m;
     S.s_first = P1.s;
     S.s_last = Pp.s;
-    S.m_half = half.m;
-    S.s_half = half.s;
+    S.m_half = c.half.m;
+    S.s_half = c.half.s;
+}
 
-    std::vector<SrcDev> sd;
-    if ((rc = prepare_sources(G, src, nsrc, t0, 0, nsteps, stream, sd))) return rc;
-    TraceDev tr;
-    if ((rc = prepare_trace(G, trace, tr))) return rc;
+// This rank's share of the parfor for its block [first, last]: particular
+// sweeps from zero with global source times (a2/a3), seeds (a4) and the Horner accumulation
+// of the tails to T_p (a7, SURVEY finding 9).  Leaves W (zero if the rank owns nothing) and,
+// on the owner of p, its particular state P.  Device flags: dflag[i] non-finite particular i,
+// norms[2i] / norms[2i+1] = energy of W before / after propagator E_i.
+static int solve_block_dev(Grid &G, const SolveCtx &c, int nsrc, const void *e0, const void *h0,
+                           const TraceDev &tr, const KernelArgs &ka, Events &ev, paraexp_stats &S,
+                           SolveBufs &b, bool &host_io) {
+    const NanHook hook;
+    const int p = c.p, first = c.first, last = c.last;
+    void *stream = ka.stream;
+    const size_t sbytes = (size_t)G.L.state_elems() * G.esize();
+    int rc;
+    b.P = G.ws[0];
+    b.W = G.ws[1];
+    b.X[0] = G.ws[2];
+    b.X[1] = G.ws[3];
+    b.X[2] = G.ws[4];
+    bool W_valid = false;
+    int *dflag = (int *)G.d_flag;
+    double *norms = (double *)G.d_norms;
+    if ((rc = dev_memset_async(dflag, 0, sizeof(int) * (p + 2), stream))) return rc;
+    if ((rc = dev_memset_async(norms, 0, sizeof(double) * 2 * (p + 1), stream))) return rc;
     const bool tracing = tr.energy || tr.np > 0;
     if (tracing) {
         // rows i < p of the energy need the summed field: NaN with several ranks (paraexp.h)
-        std::vector<double> init(p, world > 1 ? std::nan("") : 0.0);
+        std::vector<double> init(p, c.world > 1 ? std::nan("") : 0.0);
         init[p - 1] = 0.0;
         if (tr.energy && (rc = dev_memcpy_h2d_async(tr.energy, init.data(), sizeof(double) * p, stream))) return rc;
         if (tr.np > 0 && (rc = dev_memset_async(tr.probe, 0, sizeof(double) * p * tr.np, stream))) return rc;
         if ((rc = dev_sync(stream))) return rc;
     }
-    if ((rc = ensure_ws(G, 5))) return rc;
-    KernelArgs ka{&G, stream, &S.kernel_launches};
-    const size_t sbytes = (size_t)G.L.state_elems() * G.esize();
-    const int64_t cells = (int64_t)G.nx * G.ny * G.nz;
-    Events ev(stream);
-    const int idt = ev.open(4);
-
-    bool host_io = false;       // host-pointer fields (staged copies; the call syncs anyway)
-    void *P = G.ws[0];          // particular state of the current sub-interval
-    void *W = G.ws[1];          // Horner accumulator of the tails
-    void *X[3] = {G.ws[2], G.ws[3], G.ws[4]};
-    bool W_valid = false;
-    int *dflag = (int *)G.d_flag;
-    if ((rc = dev_memset_async(dflag, 0, sizeof(int) * (p + 2), stream))) return rc;
 
     auto propagate = [&](int i) -> int {   // W <- E_i W
-        const int64_t M = B[i] - B[i - 1];
-        if (tail_mode == PARAEXP_TAIL_EXP) {
-            void *bufs[4] = {W, X[0], X[1], X[2]};
-            int r = run_plan(ka, plans[M], bufs, &S, &ev);
-            W = bufs[0];
-            X[0] = bufs[1];
-            X[1] = bufs[2];
-            X[2] = bufs[3];
-            return r;
+        const int64_t M = c.B[i] - c.B[i - 1];
+        nvtxRangePushA("propagate");
+        int r = PARAEXP_OK;
+        if (c.rho_check) r = k_dot_M_async(ka, b.W, b.W, norms + 2 * i, G.dt);
+        if (!r && c.tail_mode == PARAEXP_TAIL_EXP) {
+            void *bufs[4] = {b.W, b.X[0], b.X[1], b.X[2]};
+            r = run_plan(ka, c.plans.at(M), bufs, &S, &ev);
+            b.W = bufs[0];
+            b.X[0] = bufs[1];
+            b.X[1] = bufs[2];
+            b.X[2] = bufs[3];
+        } else if (!r) {
+            void *bufs[2] = {b.W, b.X[0]};
+            const int id5 = ev.open(5);
+            r = k_leapfrog(ka, bufs, M, nullptr, 0, nullptr);
+            ev.close(id5);
+            if (bufs[0] != b.W) std::swap(b.W, b.X[0]);
+            S.leapfrog_steps += M;
+            S.curl_applications += 2 * M;
         }
-        void *bufs[2] = {W, X[0]};
-        const int id5 = ev.open(5);
-        int r = k_leapfrog(ka, bufs, M, nullptr, 0, nullptr);
-        ev.close(id5);
-        if (bufs[0] != W) std::swap(W, X[0]);
-        S.leapfrog_steps += M;
-        S.curl_applications += 2 * M;
+        if (!r && hook.tail == i) r = inject_nan(G, b.W, stream);
+        if (!r) r = k_dot_M_async(ka, b.W, b.W, norms + 2 * i + 1, G.dt);   // energy after E_i
+        nvtxRangePop();
         return r;
     };
 
@@ -979,8 +1270,8 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
     // same-time solution u(T_i) = v_i(T_i) + sum_{j<i} w_j(T_i)
     auto trace_row = [&](int i) -> int {
         int r = PARAEXP_OK;
-        if (tr.np > 0) r = k_gather(ka, W, tr, tr.probe + (int64_t)(i - 1) * tr.np, 0);
-        if (!r && tr.energy && world == 1) r = k_dot_M_async(ka, W, W, tr.energy + (i - 1), G.dt);
+        if (tr.np > 0) r = k_gather(ka, b.W, tr, tr.probe + (int64_t)(i - 1) * tr.np, 0);
+        if (!r && tr.energy && c.world == 1) r = k_dot_M_async(ka, b.W, b.W, tr.energy + (i - 1), G.dt);
         return r;
     };
 
@@ -1021,15 +1312,16 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
             kq.static_sched = true;                        // concurrent launches: no shared counter
             if ((rc = dev_memset_async(Pc[q], 0, sbytes, kq.stream))) return rc;
             void *bufs[2] = {Pc[q], scratch[sq]};
-            const size_t qoff = (size_t)B[i - 1] * nsrc * G.esize();
-            if ((rc = k_leapfrog(kq, bufs, B[i] - B[i - 1], (const SrcDev *)G.d_src, nsrc,
+            const size_t qoff = (size_t)c.B[i - 1] * nsrc * G.esize();
+            if ((rc = k_leapfrog(kq, bufs, c.B[i] - c.B[i - 1], (const SrcDev *)G.d_src, nsrc,
                                  (const char *)G.d_q + qoff))) return rc;
             if (bufs[0] != Pc[q]) std::swap(Pc[q], scratch[sq]);   // result buffer <-> scratch
+            if (hook.particular == i && (rc = inject_nan(G, Pc[q], kq.stream))) return rc;
             if ((rc = k_check_finite_async(kq, Pc[q], dflag + i))) return rc;
             if (cudaEventRecord((cudaEvent_t)G.events[q], (cudaStream_t)kq.stream) != cudaSuccess)
                 return check_cuda("event record");
-            S.leapfrog_steps += B[i] - B[i - 1];
-            S.curl_applications += 2 * (B[i] - B[i - 1]);
+            S.leapfrog_steps += c.B[i] - c.B[i - 1];
+            S.curl_applications += 2 * (c.B[i] - c.B[i - 1]);
         }
         // keep the buffer roles for the next call (results may now live in former scratch)
         for (int q = 0; q < nb; ++q) G.conc[q] = Pc[q];
@@ -1037,39 +1329,42 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
     }
 
     if (first >= 1) {
-        if (first == 1 && has_u0) {
-            if ((rc = pack_any(ka, G, e0, h0, W, &host_io))) return rc;
-            if (tail_mode == PARAEXP_TAIL_LEAPFROG && (rc = k_half_start(ka, W))) return rc;
+        if (first == 1 && c.has_u0) {
+            if ((rc = pack_any(ka, G, e0, h0, b.W, &host_io))) return rc;
+            if (c.tail_mode == PARAEXP_TAIL_LEAPFROG && (rc = k_half_start(ka, b.W))) return rc;
             W_valid = true;
         }
         for (int i = first; i <= last; ++i) {
-            const int64_t M = B[i] - B[i - 1];
+            const int64_t M = c.B[i] - c.B[i - 1];
             int id = ev.open(0);
+            nvtxRangePushA("particular");
             if (conc) {
                 if (cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)G.events[i - first], 0) != cudaSuccess)
                     return check_cuda("stream wait");
-                P = Pc[i - first];
+                b.P = Pc[i - first];
             } else {
-                if ((rc = dev_memset_async(P, 0, sbytes, stream))) return rc;
-                void *bufs[2] = {P, X[0]};
-                const size_t qoff = (size_t)B[i - 1] * nsrc * G.esize();
+                if ((rc = dev_memset_async(b.P, 0, sbytes, stream))) return rc;
+                void *bufs[2] = {b.P, b.X[0]};
+                const size_t qoff = (size_t)c.B[i - 1] * nsrc * G.esize();
                 const int id5 = ev.open(5);
                 if ((rc = k_leapfrog(ka, bufs, M, (const SrcDev *)G.d_src, nsrc, (const char *)G.d_q + qoff))) return rc;
                 ev.close(id5);
-                if (bufs[0] != P) std::swap(P, X[0]);
+                if (bufs[0] != b.P) std::swap(b.P, b.X[0]);
                 S.leapfrog_steps += M;
                 S.curl_applications += 2 * M;
-                if ((rc = k_check_finite_async(ka, P, dflag + i))) return rc;
+                if (hook.particular == i && (rc = inject_nan(G, b.P, stream))) return rc;
+                if ((rc = k_check_finite_async(ka, b.P, dflag + i))) return rc;
             }
+            nvtxRangePop();
             ev.close(id);
             id = ev.open(1);
             if (W_valid && (rc = propagate(i))) return rc;
             if (i < p) {
-                if (tail_mode == PARAEXP_TAIL_EXP && (rc = k_sync(ka, P))) return rc;
+                if (c.tail_mode == PARAEXP_TAIL_EXP && (rc = k_sync(ka, b.P))) return rc;
                 if (W_valid) {
-                    if ((rc = k_axpy(ka, W, P, 1.0))) return rc;
+                    if ((rc = k_axpy(ka, b.W, b.P, 1.0))) return rc;
                 } else {
-                    if ((rc = dev_memcpy_d2d_async(W, P, sbytes, stream))) return rc;
+                    if ((rc = dev_memcpy_d2d_async(b.W, b.P, sbytes, stream))) return rc;
                     W_valid = true;
                 }
                 if (tracing && (rc = trace_row(i))) return rc;
@@ -1083,62 +1378,109 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
         }
         ev.close(id);
     }
-    if (!W_valid && (rc = dev_memset_async(W, 0, sbytes, stream))) return rc;
-    if ((rc = k_check_finite_async(ka, W, dflag + p + 1))) return rc;
+    if (!W_valid && (rc = dev_memset_async(b.W, 0, sbytes, stream))) return rc;
+    return k_check_finite_async(ka, b.W, dflag + p + 1);
+}
 
-    // a8: sum the tails onto the root
-    // the collectives also run for a one-rank communicator when PARAEXP_FORCE_COLLECTIVES is
-    // set, so the NCCL code path can be exercised on a single GPU (tests)
-    const bool coll = comm && (world > 1 || getenv("PARAEXP_FORCE_COLLECTIVES"));
-    if (coll) {
-        const int id = ev.open(2);
-        const int dt = G.dtype == PARAEXP_F64 ? kNcclF64 : kNcclF32;
-        if ((rc = nccl_check(g_nccl.Reduce(W, W, (size_t)G.L.state_elems(), dt, kNcclSum, root,
-                                          comm->comm, (cudaStream_t)stream), "ncclReduce"))) return rc;
-        ev.close(id);
-    }
-    // a9: reconstruction on the root (eq:averaging1/2, reading 10)
-    const int idf = ev.open(3);
-    if (rank == root && tracing) {
-        // row p: u(T_p) = sync(v_p) + W, same-time (reading 9)
-        if ((rc = dev_memcpy_d2d_async(X[0], P, sbytes, stream))) return rc;
-        if ((rc = k_sync(ka, X[0]))) return rc;
-        if ((rc = k_axpy(ka, X[0], W, 1.0))) return rc;
-        if (tr.np > 0 && (rc = k_gather(ka, X[0], tr, tr.probe + (int64_t)(p - 1) * tr.np, 0))) return rc;
-        if (tr.energy && (rc = k_dot_M_async(ka, X[0], X[0], tr.energy + (p - 1), G.dt))) return rc;
-    }
-    if (tracing && coll) {
-        if (tr.np > 0 && (rc = nccl_check(g_nccl.AllReduce(tr.probe, tr.probe, (size_t)p * tr.np, kNcclF64, kNcclSum,
-                                                          comm->comm, (cudaStream_t)stream), "ncclAllReduce"))) return rc;
-        if (tr.energy && (rc = nccl_check(g_nccl.AllReduce(tr.energy, tr.energy, (size_t)p, kNcclF64, kNcclSum,
-                                                           comm->comm, (cudaStream_t)stream), "ncclAllReduce"))) return rc;
-    }
-    if (rank == root) {
-        if (tail_mode == PARAEXP_TAIL_EXP) {
-            if ((rc = k_axpy_comps(ka, P, W, 1.0, 0, 3))) return rc;       // e_out = e_p + W_e
-            void *bufs[4] = {W, X[0], X[1], X[2]};
-            if ((rc = run_plan(ka, half, bufs, nullptr))) return rc;       // exp(dt/2 A) W
-            S.a_applications += (int64_t)half.s * half.m;
-            if ((rc = k_axpy_comps(ka, P, bufs[0], 1.0, 3, 6))) return rc;  // h_out = h_p + [.]_h
-        } else {
-            if ((rc = k_axpy(ka, P, W, 1.0))) return rc;
+// Read back the block's device flags and propagator norms (synchronises `stream`).
+// Returns EDIVERGED / EOVERFLOW naming the first failing sub-interval, or sets *violation when
+// a propagator changed the energy norm by more than its tolerance (rho too small: the
+// spectrum leaves the Leja interval and the polynomial grows there -- SURVEY finding 8).
+static int block_status(const Grid &G, const SolveCtx &c, void *stream, paraexp_stats &S, bool *violation,
+                        double *max_dev) {
+    const int p = c.p;
+    std::vector<int> flags(p + 2, 0);
+    std::vector<double> nrm(2 * (p + 1), 0.0);
+    int rc = dev_memcpy_d2h(flags.data(), G.d_flag, sizeof(int) * (p + 2), stream);
+    if (!rc) rc = dev_memcpy_d2h(nrm.data(), G.d_norms, sizeof(double) * 2 * (p + 1), stream);
+    if (rc) return rc;
+    for (int i = 1; i <= p; ++i)
+        if (flags[i]) {
+            S.fail_interval = i;
+            return fail(PARAEXP_EDIVERGED, "leapfrog diverged in sub-interval " + std::to_string(i));
+        }
+    *violation = false;
+    *max_dev = 0;
+    const int fprop = c.first >= 1 ? (c.first == 1 && c.has_u0 ? 1 : c.first + 1) : p + 1;
+    for (int i = fprop; i <= p; ++i) {
+        const double after = nrm[2 * i + 1];
+        if (!std::isfinite(after)) {
+            S.fail_interval = i;
+            return fail(PARAEXP_EOVERFLOW, "exp(tA)v tail produced non-finite values in propagator " + std::to_string(i));
+        }
+        if (c.rho_check && nrm[2 * i] > 0) {
+            const double dev = std::fabs(std::sqrt(after / nrm[2 * i]) - 1.0);
+            const Plan &P = c.plans.at(c.B[i] - c.B[i - 1]);
+            const double floor_tol = G.dtype == PARAEXP_F64 ? 1e-9 : 1e-3;
+            const double tol = c.auto_plan ? std::max(floor_tol, 10.0 * P.eps_A * P.rho * P.tau)
+                                           : std::max(floor_tol, 1e-3);
+            *max_dev = std::max(*max_dev, dev);
+            if (!(dev <= tol)) *violation = true;
         }
     }
-    if (broadcast_out && coll) {
-        const int dt = G.dtype == PARAEXP_F64 ? kNcclF64 : kNcclF32;
-        if ((rc = nccl_check(g_nccl.Broadcast(P, P, (size_t)G.L.state_elems(), dt, root, comm->comm,
-                                             (cudaStream_t)stream), "ncclBroadcast"))) return rc;
+    if (flags[p + 1]) {
+        S.fail_interval = c.first;
+        return fail(PARAEXP_EOVERFLOW, "exp(tA)v tails produced non-finite values");
     }
-    if ((rank == root || broadcast_out) && e_out && h_out) {
-        if ((rc = unpack_any(ka, G, P, e_out, h_out, &host_io))) return rc;
+    return PARAEXP_OK;
+}
+
+// solve_block_dev + block_status, with the rho safety net: when a propagator violated norm
+// preservation and rho < rho_cfl, the block is recomputed with rho = rho_cfl (an upper bound of
+// ||A||_2, SURVEY finding 7).  The schedule is kept, so the ranks' partial sums still add up.
+static int solve_block_checked(Grid &G, SolveCtx &c, int nsrc, const void *e0, const void *h0,
+                               const TraceDev &tr, const KernelArgs &ka, Events &ev, paraexp_stats &S,
+                               SolveBufs &b, bool &host_io) {
+    int rc;
+    nvtxRangePushA("paraexp_block");
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if ((rc = solve_block_dev(G, c, nsrc, e0, h0, tr, ka, ev, S, b, host_io))) break;
+        bool viol = false;
+        double dev = 0;
+        if ((rc = block_status(G, c, ka.stream, S, &viol, &dev))) break;
+        S.norm_deviation = dev;
+        if (!viol) break;
+        if (attempt == 1 || !(c.rho < G.rho_cfl)) {
+            rc = fail(PARAEXP_EOVERFLOW, "exp(tA)v tails violate norm preservation even with rho_cfl");
+            break;
+        }
+        S.rho_fallback = 1;
+        c.rho = G.rho_cfl;
+        c.rho_check = false;
+        if ((rc = build_plans(G, c))) break;
+        plan_stats(c, S);
     }
-    ev.close(idf);
-    ev.close(idt);
+    nvtxRangePop();
+    return rc;
+}
+
+// a9 on the owner of p: e_out = e_p + W_e, h_out = h_p + [exp(dt/2 A) W]_h (eq:averaging1/2,
+// reading 10), in place in b.P.
+static int solve_finish_dev(Grid &G, const SolveCtx &c, const KernelArgs &ka, Events &ev,
+                            paraexp_stats &S, SolveBufs &b) {
+    int rc;
+    nvtxRangePushA("paraexp_finish");
+    if (c.tail_mode == PARAEXP_TAIL_EXP) {
+        if ((rc = k_axpy_comps(ka, b.P, b.W, 1.0, 0, 3))) return rc;       // e_out = e_p + W_e
+        void *bufs[4] = {b.W, b.X[0], b.X[1], b.X[2]};
+        if ((rc = run_plan(ka, c.half, bufs, nullptr, &ev))) return rc;     // exp(dt/2 A) W
+        S.a_applications += (int64_t)c.half.s * c.half.m;
+        b.W = bufs[0];
+        b.X[0] = bufs[1];
+        b.X[1] = bufs[2];
+        b.X[2] = bufs[3];
+        if ((rc = k_axpy_comps(ka, b.P, b.W, 1.0, 3, 6))) return rc;       // h_out = h_p + [.]_h
+    } else {
+        if ((rc = k_axpy(ka, b.P, b.W, 1.0))) return rc;
+    }
+    nvtxRangePop();
+    return PARAEXP_OK;
+}
+
+static void finish_stats(const Grid &G, Events &ev, paraexp_stats &S) {
+    const int64_t cells = (int64_t)G.nx * G.ny * G.nz;
     S.curl_applications = 2 * (S.leapfrog_steps + S.a_applications);
     S.cell_updates = (S.leapfrog_steps + S.a_applications) * cells;
-    std::vector<int> flags(p + 2, 0);
-    if ((rc = dev_memcpy_d2h(flags.data(), dflag, sizeof(int) * (p + 2), stream))) return rc;
-    if ((rc = sched_check(G, stream))) return rc;
     double ms[7] = {0, 0, 0, 0, 0, 0, 0};
     ev.sum(ms);
     S.ms_particular = ms[0];
@@ -1148,15 +1490,203 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
     S.ms_total = ms[4];
     S.ms_leapfrog_kernels = ms[5];
     S.ms_poly_kernels = ms[6];
-    for (int i = 1; i <= p; ++i)
-        if (flags[i]) {
-            S.fail_interval = i;
-            return fail(PARAEXP_EDIVERGED, "leapfrog diverged in sub-interval " + std::to_string(i));
-        }
-    if (flags[p + 1]) {
-        S.fail_interval = first;
-        return fail(PARAEXP_EOVERFLOW, "exp(tA)v tails produced non-finite values");
+}
+
+}  // namespace pe
+
+extern "C" {
+
+static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
+                      int32_t nsrc, double t0, int64_t nsteps, int32_t p,
+                      const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
+                      const void *e0, const void *h0, void *e_out, void *h_out,
+                      const paraexp_trace *trace, void *stream, paraexp_stats *st);
+
+int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
+                  int32_t nsrc, double t0, int64_t nsteps, int32_t p,
+                  const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
+                  const void *e0, const void *h0, void *e_out, void *h_out, void *stream,
+                  paraexp_stats *st) {
+    return solve_impl(grid, comm, src, nsrc, t0, nsteps, p, opts, tail_mode, broadcast_out, e0, h0, e_out,
+                      h_out, nullptr, stream, st);
+}
+
+int paraexp_solve_trace(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
+                        int32_t nsrc, double t0, int64_t nsteps, int32_t p,
+                        const paraexp_expmv_opts *opts, int32_t broadcast_out, const void *e0,
+                        const void *h0, void *e_out, void *h_out, const paraexp_trace *trace,
+                        void *stream, paraexp_stats *st) {
+    return solve_impl(grid, comm, src, nsrc, t0, nsteps, p, opts, PARAEXP_TAIL_EXP, broadcast_out, e0, h0,
+                      e_out, h_out, trace, stream, st);
+}
+
+static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *src,
+                      int32_t nsrc, double t0, int64_t nsteps, int32_t p,
+                      const paraexp_expmv_opts *opts, int32_t tail_mode, int32_t broadcast_out,
+                      const void *e0, const void *h0, void *e_out, void *h_out,
+                      const paraexp_trace *trace, void *stream, paraexp_stats *st) {
+    using namespace pe;
+    if (!grid) return fail(PARAEXP_EINVAL, "null grid");
+    Grid &G = grid->g;
+    if (G.device < 0) return fail(PARAEXP_ENOTSUP, "host-only grid");
+    if ((e0 == nullptr) != (h0 == nullptr)) return fail(PARAEXP_EINVAL, "e0 and h0 must both be given or both NULL");
+    if (trace && tail_mode != PARAEXP_TAIL_EXP) return fail(PARAEXP_EINVAL, "trace needs tail_mode EXP");
+    const int rank = comm ? comm->rank : 0, world = comm ? comm->world : 1;
+    paraexp_stats local{};
+    paraexp_stats &S = st ? *st : local;
+    S = paraexp_stats();
+    int rc = dev_set_device(G.device);
+    if (rc) return rc;
+    CallScope scope(G, stream);
+    nvtxRangePushA("paraexp_solve");
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop;
+    // the collectives also run for a one-rank communicator when PARAEXP_FORCE_COLLECTIVES is
+    // set, so the NCCL code path can be exercised on a single GPU (tests)
+    const bool coll = comm && (world > 1 || getenv("PARAEXP_FORCE_COLLECTIVES"));
+    CommCtx cctx{comm, &G};
+    paraexp_comm_view view;
+    if (comm && world > 1 && !(opts && opts->rho > 0)) {
+        view.ctx = &cctx;
+        view.bcast_rho = bcast_rho_nccl;
     }
+    SolveCtx c;
+    if ((rc = solve_prepare(G, view, rank, world, opts, nsteps, p, tail_mode, e0 != nullptr, stream, S, c))) return rc;
+    plan_stats(c, S);
+
+    std::vector<SrcDev> sd;
+    if ((rc = prepare_sources(G, src, nsrc, t0, 0, nsteps, stream, sd))) return rc;
+    TraceDev tr;
+    if ((rc = prepare_trace(G, trace, tr))) return rc;
+    const bool tracing = tr.energy || tr.np > 0;
+    if ((rc = ensure_ws(G, 5)) || (rc = ensure_norms(G))) return rc;
+    KernelArgs ka{&G, stream, &S.kernel_launches};
+    const size_t sbytes = (size_t)G.L.state_elems() * G.esize();
+    Events ev(stream);
+    const int idt = ev.open(4);
+    bool host_io = false;       // host-pointer fields (staged copies; the call syncs anyway)
+    SolveBufs b;
+    if ((rc = solve_block_checked(G, c, nsrc, e0, h0, tr, ka, ev, S, b, host_io))) return rc;
+
+    // a8: sum the tails onto the root
+    if (coll) {
+        const int id = ev.open(2);
+        nvtxRangePushA("paraexp_reduce");
+        rc = comm_reduce_W(comm, G, b.W, sbytes, c.root, stream);
+        nvtxRangePop();
+        if (rc) return rc;
+        ev.close(id);
+    }
+    const int idf = ev.open(3);
+    if (rank == c.root && tracing) {
+        // row p: u(T_p) = sync(v_p) + W, same-time (reading 9)
+        if ((rc = dev_memcpy_d2d_async(b.X[0], b.P, sbytes, stream))) return rc;
+        if ((rc = k_sync(ka, b.X[0]))) return rc;
+        if ((rc = k_axpy(ka, b.X[0], b.W, 1.0))) return rc;
+        if (tr.np > 0 && (rc = k_gather(ka, b.X[0], tr, tr.probe + (int64_t)(p - 1) * tr.np, 0))) return rc;
+        if (tr.energy && (rc = k_dot_M_async(ka, b.X[0], b.X[0], tr.energy + (p - 1), G.dt))) return rc;
+    }
+    if (tracing && coll && (rc = comm_allreduce_trace(comm, tr, p, stream))) return rc;
+    // a9: reconstruction on the root (eq:averaging1/2, reading 10)
+    if (rank == c.root && (rc = solve_finish_dev(G, c, ka, ev, S, b))) return rc;
+    if (broadcast_out && coll && (rc = comm_bcast_state(comm, G, b.P, c.root, stream))) return rc;
+    if ((rank == c.root || broadcast_out) && e_out && h_out) {
+        if ((rc = unpack_any(ka, G, b.P, e_out, h_out, &host_io))) return rc;
+    }
+    ev.close(idf);
+    ev.close(idt);
+    if (coll && (rc = comm_wait(comm, stream))) return rc;
+    if ((rc = dev_sync(stream))) return rc;
+    if ((rc = sched_check(G, stream))) return rc;
+    finish_stats(G, ev, S);
+    return PARAEXP_OK;
+}
+
+int paraexp_solve_block(paraexp_grid *grid, int32_t rank, int32_t world, const paraexp_source *src,
+                        int32_t nsrc, double t0, int64_t nsteps, int32_t p,
+                        const paraexp_expmv_opts *opts, int32_t tail_mode, const void *e0,
+                        const void *h0, void *w_e, void *w_h, void *v_e, void *v_h, void *stream,
+                        paraexp_stats *st) {
+    using namespace pe;
+    if (!grid) return fail(PARAEXP_EINVAL, "null grid");
+    Grid &G = grid->g;
+    if (G.device < 0) return fail(PARAEXP_ENOTSUP, "host-only grid");
+    if ((e0 == nullptr) != (h0 == nullptr)) return fail(PARAEXP_EINVAL, "e0 and h0 must both be given or both NULL");
+    if (!w_e || !w_h) return fail(PARAEXP_EINVAL, "null w_e / w_h");
+    paraexp_stats local{};
+    paraexp_stats &S = st ? *st : local;
+    S = paraexp_stats();
+    int rc = dev_set_device(G.device);
+    if (rc) return rc;
+    CallScope scope(G, stream);
+    SolveCtx c;
+    if ((rc = solve_prepare(G, paraexp_comm_view(), rank, world, opts, nsteps, p, tail_mode, e0 != nullptr,
+                            stream, S, c))) return rc;
+    plan_stats(c, S);
+    std::vector<SrcDev> sd;
+    if ((rc = prepare_sources(G, src, nsrc, t0, 0, nsteps, stream, sd))) return rc;
+    if ((rc = ensure_ws(G, 5)) || (rc = ensure_norms(G))) return rc;
+    KernelArgs ka{&G, stream, &S.kernel_launches};
+    Events ev(stream);
+    const int idt = ev.open(4);
+    bool host_io = false;
+    SolveBufs b;
+    if ((rc = solve_block_checked(G, c, nsrc, e0, h0, TraceDev(), ka, ev, S, b, host_io))) return rc;
+    if ((rc = unpack_any(ka, G, b.W, w_e, w_h, &host_io))) return rc;
+    if (rank == c.root && v_e && v_h && (rc = unpack_any(ka, G, b.P, v_e, v_h, &host_io))) return rc;
+    ev.close(idt);
+    if ((rc = dev_sync(stream))) return rc;
+    if ((rc = sched_check(G, stream))) return rc;
+    finish_stats(G, ev, S);
+    return PARAEXP_OK;
+}
+
+int paraexp_solve_finish(paraexp_grid *grid, const paraexp_expmv_opts *opts, int32_t tail_mode,
+                         const void *w_e, const void *w_h, const void *v_e, const void *v_h,
+                         void *e_out, void *h_out, void *stream, paraexp_stats *st) {
+    using namespace pe;
+    if (!grid) return fail(PARAEXP_EINVAL, "null grid");
+    Grid &G = grid->g;
+    if (G.device < 0) return fail(PARAEXP_ENOTSUP, "host-only grid");
+    if (!w_e || !w_h || !v_e || !v_h || !e_out || !h_out) return fail(PARAEXP_EINVAL, "null field pointer");
+    if (tail_mode != PARAEXP_TAIL_EXP && tail_mode != PARAEXP_TAIL_LEAPFROG) return fail(PARAEXP_EINVAL, "bad tail mode");
+    paraexp_stats local{};
+    paraexp_stats &S = st ? *st : local;
+    S = paraexp_stats();
+    int rc = dev_set_device(G.device);
+    if (rc) return rc;
+    CallScope scope(G, stream);
+    SolveCtx c;
+    c.tail_mode = tail_mode;
+    c.rho = default_rho(G, opts, stream, &S.kernel_launches, &rc);
+    if (rc) return rc;
+    {
+        const double theta = c.rho * G.dt * 0.5;
+        if ((rc = make_plan(PARAEXP_TAYLOR, 24, std::max(1, (int)std::ceil(theta)), 0.0, 0.5 * G.dt, c.rho, G.dt,
+                            c.half))) return rc;
+    }
+    S.rho = c.rho;
+    S.m_half = c.half.m;
+    S.s_half = c.half.s;
+    if ((rc = ensure_ws(G, 5))) return rc;
+    KernelArgs ka{&G, stream, &S.kernel_launches};
+    Events ev(stream);
+    const int idt = ev.open(4);
+    bool host_io = false;
+    SolveBufs b;
+    b.P = G.ws[0];
+    b.W = G.ws[1];
+    b.X[0] = G.ws[2];
+    b.X[1] = G.ws[3];
+    b.X[2] = G.ws[4];
+    if ((rc = pack_any(ka, G, w_e, w_h, b.W, &host_io))) return rc;
+    if ((rc = pack_any(ka, G, v_e, v_h, b.P, &host_io))) return rc;
+    if ((rc = solve_finish_dev(G, c, ka, ev, S, b))) return rc;
+    if ((rc = unpack_any(ka, G, b.P, e_out, h_out, &host_io))) return rc;
+    ev.close(idt);
+    if ((rc = dev_sync(stream))) return rc;
+    finish_stats(G, ev, S);
     return PARAEXP_OK;
 }
 

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <type_traits>
+#include <map>
 #include <mutex>
 
 #include "internal.h"
@@ -86,25 +87,6 @@ static bool pdl_enabled() {
     return on;
 }
 
-// Grid-wide barrier of a cooperative launch (all CTAs co-resident): the w' stores of every CTA
-// (generic proxy) are made visible to the TMA loads (async proxy) of the next op.
-__device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned target) {
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(ctr, 1u);
-        unsigned v;
-        while (true) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-            if (v >= target) break;
-            __nanosleep(32);
-        }
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    __syncthreads();
-}
-
 template <typename... KArgs, typename... Args>
 static void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args &&...args) {
     cudaLaunchConfig_t cfg = {};
@@ -117,22 +99,6 @@ static void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, c
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
-
-// cooperative launch (co-residency of the whole grid guaranteed; used with grid_barrier)
-template <typename... KArgs, typename... Args>
-static void launch_coop(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args &&...args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3((unsigned)block);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -249,199 +215,20 @@ __device__ __forceinline__ void curl_stage(const T *E0, const T *E1, int s, T &c
 }
 
 // ---------------------------------------------------------------------------------------
-// K1: fused leapfrog step
+// K1r: fused leapfrog step, row-aligned warps and register-carried own values
 // ---------------------------------------------------------------------------------------
-// Per-CTA pipeline (S stages).  Iteration p works on planes k = kb-1+p and k+1:
-//   phase A: e'(k+1) on the tile + halo  -> ring slot (k+1) % NR (and global for tile points)
+// Per-CTA pipeline (S stages, ring depth 2, two barriers per plane).  Iteration p works on
+// planes k = kb-1+p and k+1:
+//   phase A: e'(k+1) on the tile + halo  -> ring slot (k+1) % 2 (and global for tile points)
 //   barrier
 //   phase B: h'(k) on the tile           -> global
-//   [barrier]  refill
-// ONEBAR = false: two barriers per plane, ring depth 2, the slot of plane k is refilled at the
-//   end of iteration k.
-// ONEBAR = true: one barrier per plane, ring depth 3, the slot of plane k-1 is refilled right
-//   after the barrier of iteration k (every warp has then left phase B of iteration k-1).
+//   barrier, refill the stage of plane k
 // TR: also accumulate the step's energy E_{m+1} = dt [sum e'^2/cE + sum h h'/cH] (eq:energy)
 // and write the probe values e' (f1; paraexp.h trace).
-template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR, bool TR>
-__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR) leapfrog_fused_kernel(
-    const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
-    const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ out,
-    Sched sch, SrcList src, const T *__restrict__ q, const __grid_constant__ TraceDev tr) {
-    pdl_sync();
-    using G = Geo<T, BX, BY>;
-    using SL = StageL<T, EM, HA, G>;
-    constexpr int NR = ONEBAR ? 3 : 2;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    T *stages = reinterpret_cast<T *>(smem_raw);
-    T *ring = stages + S * SL::SZ;                       // [NR][3][EY][EX] e' planes
-    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(ring + NR * 3 * G::RP) + 15) & ~uintptr_t(15));
-    const int tid = threadIdx.x;
-    // phase-A point (tile + halo) and phase-B point (tile) of this thread
-    const bool hasA = tid < G::RP;
-    const int ii = tid % G::EX, jj = tid / G::EX;
-    const int sA = (jj + 1) * G::WX + ii + G::OX;
-    const bool tileA = ii < BX && jj < BY;
-    const bool hasB = tid < G::NT;
-    const int tx = tid % BX, ty = tid / BX;
-    const int rB = ty * G::EX + tx;
-    const int sB = (ty + 1) * G::WX + tx + G::OX;
-    T bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
-    const T bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    uint32_t lcount = 0;   // planes loaded by this CTA so far (ring position)
-    double eacc = 0.0;     // TR: this thread's energy contributions
-    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
-        const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
-        const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
-        const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
-        const int nplanes = ke - kb + 2;                 // planes kb-1 .. ke
-        const int iA = x0 + ii, jA = y0 + jj;
-        const bool inA = hasA && iA < D.nx && jA < D.ny;
-        const bool lxA = inA && jA > 0, lyA = inA && iA > 0, lzA = inA && iA > 0 && jA > 0;
-        const bool wrA = inA && tileA;
-        uint32_t smask = 0, pmask = 0;
-        for (int r = 0; r < src.n; ++r)
-            if (inA && src.i[r] == iA && src.j[r] == jA) smask |= 1u << r;
-        if (TR)
-            for (int r = 0; r < tr.np; ++r)
-                if (wrA && tr.i[r] == iA && tr.j[r] == jA) pmask |= 1u << r;
-        T *oA = out + D.idx(wrA ? iA : 0, wrA ? jA : 0, 0);
-        const int iB = x0 + tx, jB = y0 + ty;
-        const bool inB = hasB && iB < D.nx && jB < D.ny;
-        const bool lxB = iB > 0, lyB = jB > 0;
-        T *oB = out + D.idx(inB ? iB : 0, inB ? jB : 0, 0) + 3 * D.cs;
-        if (tid == 0)
-            for (int p = 0; p < min(S, nplanes); ++p) {
-                const uint32_t L = lcount + p;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                          &tm_cH, x0, y0, kb - 1 + p);
-            }
-        for (int p = 0; p + 1 < nplanes; ++p) {         // iteration on planes k = kb-1+p, k+1
-            const int k = kb - 1 + p, kk = k + 1;
-            const uint32_t L0 = lcount + p, L1 = L0 + 1;
-            if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
-            mbar_wait(&bars[L1 % S], (L1 / S) & 1);
-            const T *P0 = stages + (L0 % S) * SL::SZ;    // plane k
-            const T *P1 = stages + (L1 % S) * SL::SZ;    // plane k+1
-            T *R1 = ring + (kk % NR) * 3 * G::RP;
-            if (EM == 1 && kk < D.nz) {
-                bE0 = __ldg(cf.tab + kk) * cf.sig;
-                bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
-                bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
-            }
-            // ---- phase A: e'(k+1) on the tile and its +1 halo ----
-            if (hasA) {
-                T c0, c1, c2;
-                curlT_stage<T, G>(P1, P0, sA, c0, c1, c2);
-                const bool vk = kk < D.nz, kp = kk > 0;
-                T e0, e1, e2;
-                if (EM == 2) {
-                    e0 = (lxA && vk && kp) ? P1[sA] + (P1[SL::ST + sA] * cf.sig) * c0 : T(0);
-                    e1 = (lyA && vk && kp) ? P1[G::PL + sA] + (P1[SL::ST + G::PL + sA] * cf.sig) * c1 : T(0);
-                    e2 = (lzA && vk) ? P1[2 * G::PL + sA] + (P1[SL::ST + 2 * G::PL + sA] * cf.sig) * c2 : T(0);
-                } else {
-                    e0 = (lxA && vk && kp) ? P1[sA] + bE0 * c0 : T(0);
-                    e1 = (lyA && vk && kp) ? P1[G::PL + sA] + bE1 * c1 : T(0);
-                    e2 = (lzA && vk) ? P1[2 * G::PL + sA] + bE2 * c2 : T(0);
-                }
-                if (smask && vk)
-                    for (int r = 0; r < src.n; ++r)
-                        if (((smask >> r) & 1u) && src.k[r] == kk) {
-                            const int sc = src.c[r];
-                            const T qv = q[r];
-                            if (sc == 0) e0 = e0 - qv;
-                            if (sc == 1) e1 = e1 - qv;
-                            if (sc == 2) e2 = e2 - qv;
-                        }
-                R1[tid] = e0;
-                R1[G::RP + tid] = e1;
-                R1[2 * G::RP + tid] = e2;
-                if (wrA && vk && kk >= kb && kk < ke) {
-                    T *o = oA + (int64_t)kk * D.plane;
-                    o[0] = e0;
-                    o[D.cs] = e1;
-                    o[2 * D.cs] = e2;
-                    if (TR) {
-                        T w0 = bE0, w1 = bE1, w2 = bE2;
-                        if (EM == 2) {
-                            w0 = P1[SL::ST + sA] * cf.sig;
-                            w1 = P1[SL::ST + G::PL + sA] * cf.sig;
-                            w2 = P1[SL::ST + 2 * G::PL + sA] * cf.sig;
-                        }
-                        if (w0 != T(0)) eacc += (double)e0 * (double)e0 / (double)w0;
-                        if (w1 != T(0)) eacc += (double)e1 * (double)e1 / (double)w1;
-                        if (w2 != T(0)) eacc += (double)e2 * (double)e2 / (double)w2;
-                        if (pmask)
-                            for (int r = 0; r < tr.np; ++r)
-                                if (((pmask >> r) & 1u) && tr.k[r] == kk)
-                                    tr.probe[r] = (double)(tr.c[r] == 0 ? e0 : (tr.c[r] == 1 ? e1 : e2));
-                    }
-                }
-            }
-            __syncthreads();
-            if (ONEBAR && tid == 0 && p >= 1 && p - 1 + S < nplanes) {
-                const uint32_t L = lcount + p - 1 + S;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                          &tm_cH, x0, y0, kb - 1 + p - 1 + S);
-            }
-            // ---- phase B: h'(k) on the tile ----
-            if (k >= kb && inB) {
-                const T *R0 = ring + (k % NR) * 3 * G::RP;
-                const T ex0 = R0[rB], ey0 = R0[G::RP + rB], ez0 = R0[2 * G::RP + rB];
-                const T ez_jp = R0[2 * G::RP + rB + G::EX], ex_jp = R0[rB + G::EX];
-                const T ez_ip = R0[2 * G::RP + rB + 1], ey_ip = R0[G::RP + rB + 1];
-                const T ex_kp = R1[rB], ey_kp = R1[G::RP + rB];
-                const T c0 = ((ey0 + ez_jp) - ey_kp) - ez0;
-                const T c1 = ((ez0 + ex_kp) - ez_ip) - ex0;
-                const T c2 = ((ex0 + ey_ip) - ex_jp) - ey0;
-                const T hx = P0[3 * G::PL + sB], hy = P0[4 * G::PL + sB], hz = P0[5 * G::PL + sB];
-                T *o = oB + (int64_t)k * D.plane;
-                T g0 = bH0, g1 = bH1, g2 = bH2;
-                if (HA) {
-                    const int ch = SL::ST + SL::CE;
-                    g0 = P0[ch + sB] * cf.sig;
-                    g1 = P0[ch + G::PL + sB] * cf.sig;
-                    g2 = P0[ch + 2 * G::PL + sB] * cf.sig;
-                }
-                const T n0 = lxB ? hx - g0 * c0 : hx;
-                const T n1 = lyB ? hy - g1 * c1 : hy;
-                const T n2 = k > 0 ? hz - g2 * c2 : hz;
-                o[0] = n0;
-                o[D.cs] = n1;
-                o[2 * D.cs] = n2;
-                if (TR) {
-                    if (lxB && g0 != T(0)) eacc += (double)hx * (double)n0 / (double)g0;
-                    if (lyB && g1 != T(0)) eacc += (double)hy * (double)n1 / (double)g1;
-                    if (k > 0 && g2 != T(0)) eacc += (double)hz * (double)n2 / (double)g2;
-                }
-            }
-            if (!ONEBAR) {
-                __syncthreads();
-                // plane k is consumed: refill its slot with plane k + S
-                if (tid == 0 && p + S < nplanes) {
-                    const uint32_t L = lcount + p + S;
-                    issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                              &tm_cH, x0, y0, kb - 1 + p + S);
-                }
-            }
-        }
-        if (ONEBAR) __syncthreads();
-        lcount += nplanes;
-    }
-    if (TR && tr.energy) {
-        const double sum = block_sum(eacc);
-        if (tid == 0 && sum != 0.0) atomicAdd(tr.energy, sum * tr.dt);
-    }
-}
-
 // ---------------------------------------------------------------------------------------
 // K1r: the leapfrog step with row-aligned warps and register-carried own values
 // ---------------------------------------------------------------------------------------
-// Same staging and phases as K1 (ONEBAR = false).  Differences:
+// Mapping:
 //  * phase-A points are mapped so that warps 0..BY cover whole 32-wide rows (the +1 halo
 //    column x0+BX is handled by the last warp): no warp straddles two rows;
 //  * the thread of tile point (tx, ty) is the phase-A thread of the same point, so phase B
@@ -882,16 +669,14 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
 // K2: fused Newton pair  u = X w ; y <- (init?0:y) + a w + b u ; [w' = X u + e2 w]
 // ---------------------------------------------------------------------------------------
 // Phase A of iteration k: u_e(k+1) on the +1 halo and u_h(k) on the -1 halo; phase B: the
-// tile's w'(k) and y(k).  Ring depth 2 (two barriers per plane) or 3 (ONEBAR).
+// tile's w'(k) and y(k).  Ring depth 2 (two barriers per plane).
 // min 2 CTAs/SM: the measured K2 rate depends on two resident CTAs per SM (a register
 // growth to > 102 per thread halves the occupancy: 376 vs 288 us per A-application)
-template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR, bool MULTI = false>
+template <typename T, int EM, bool HA, int BX, int BY, int S>
 __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) pair_fused_kernel(
-    const __grid_constant__ CUtensorMap tm_state_p, const __grid_constant__ CUtensorMap tm_cE,
-    const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout_p,
-    T *__restrict__ y, Sched sch, T a_p, T b_p, T e2_p, T cl_p, int init_p, int mode_p, EtDev et,
-    const __grid_constant__ CUtensorMap tm_state2, T *__restrict__ wout2, const Op *__restrict__ ops, int nops,
-    unsigned *gbar) {
+    const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
+    const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
+    T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
     pdl_sync();
     using G = Geo<T, BX, BY>;
     if (et.norms && et_skip(et)) {                        // early termination (f2)
@@ -903,7 +688,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
     }
     double dacc = 0.0, yacc = 0.0;                        // ||delta y||^2, ||y||^2 (energy norm)
     using SL = StageL<T, EM, HA, G>;
-    constexpr int NR = ONEBAR ? 3 : 2;
+    constexpr int NR = 2;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *stages = reinterpret_cast<T *>(smem_raw);
     T *UE = stages + S * SL::SZ;                         // [NR][3][EY][EX]: u_e at (ii, jj)
@@ -930,15 +715,6 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
     }
     __syncthreads();
     uint32_t lcount = 0;
-    // MULTI: every op of the substep in one (cooperative, one-wave) launch, a grid barrier
-    // between ops; w ping-pongs between the two buffers/maps after each kind-0 op
-    bool flip = false;
-    for (int o = 0; o < (MULTI ? nops : 1); ++o) {
-    const T a = MULTI ? T(ops[o].a) : a_p, b = MULTI ? T(ops[o].b) : b_p;
-    const T e2 = MULTI ? T(ops[o].e2) : e2_p, cl = MULTI ? T(ops[o].c) : cl_p;
-    const int mode = MULTI ? ops[o].kind : mode_p, init = MULTI ? (o == 0 ? init_p : 0) : init_p;
-    const CUtensorMap *tm_state = (MULTI && flip) ? &tm_state2 : &tm_state_p;
-    T *__restrict__ wout = (MULTI && flip) ? wout2 : wout_p;
     for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
         const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
@@ -960,7 +736,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
         if (tid == 0)
             for (int p = 0; p < min(S, nplanes); ++p) {
                 const uint32_t L = lcount + p;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], tm_state, &tm_cE,
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
                                           &tm_cH, x0, y0, kb - 1 + p);
             }
         for (int p = 0; p + 1 < nplanes; ++p) {
@@ -1039,11 +815,6 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
                 }
             }
             __syncthreads();
-            if (ONEBAR && tid == 0 && p >= 1 && p - 1 + S < nplanes) {
-                const uint32_t L = lcount + p - 1 + S;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], tm_state, &tm_cE,
-                                          &tm_cH, x0, y0, kb - 1 + p - 1 + S);
-            }
             if (doB) {
                 const T *UE0 = UE + (k % NR) * 3 * G::RP;        // u_e(k)
                 const T *UHm = UH + ((k - 1 + NR) % NR) * 3 * G::RP; // u_h(k-1)
@@ -1138,22 +909,14 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
                 yo[4 * D.cs] = y4;
                 yo[5 * D.cs] = y5;
             }
-            if (!ONEBAR) {
-                __syncthreads();
-                if (tid == 0 && p + S < nplanes) {
-                    const uint32_t L = lcount + p + S;
-                    issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], tm_state, &tm_cE,
-                                              &tm_cH, x0, y0, kb - 1 + p + S);
-                }
+            __syncthreads();
+            if (tid == 0 && p + S < nplanes) {
+                const uint32_t L = lcount + p + S;
+                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                          &tm_cH, x0, y0, kb - 1 + p + S);
             }
         }
-        if (ONEBAR) __syncthreads();
         lcount += nplanes;
-    }
-    if (MULTI) {
-        if (mode == 0) flip = !flip;
-        if (o + 1 < nops) grid_barrier(gbar, (unsigned)(o + 1) * gridDim.x);
-    }
     }
     if (et.norms) {
         const double ds = block_sum(dacc);
@@ -1166,202 +929,6 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
     }
 }
 
-// ---------------------------------------------------------------------------------------
-// K2H: one nested (Horner) step of the pair-block polynomial (DESIGN reading 33)
-// ---------------------------------------------------------------------------------------
-//   r' = (a b + beta X b) + s (X (X r) + e2 r)          (s = c for the innermost step, else 1)
-// Inputs b (the substep's start vector) and r (the running nest) are both TMA-staged with the
-// same 1-cell halo box; X r -> X(X r) runs as in K2 (u_e(k+1), u_h(k) rings, then X u on the
-// tile) and X b is evaluated at the own point straight from the b stage.  HBM per step: read
-// b, r, write r' = 18 values per two A-applications (K2: read w, y, write w', y = 24), paid
-// for with one extra stencil evaluation (X b) per step.  Scalar / z-table materials only.
-template <typename T, int BX, int BY>
-struct StageH {
-    static constexpr int A = 128 / (int)sizeof(T);
-    static constexpr int ST = ((6 * Geo<T, BX, BY>::PL + A - 1) / A) * A;   // one 6-component box
-    static constexpr int SZ = 2 * ST;                                        // r box | b box
-};
-
-template <typename T, int EM, int BX, int BY, int S>
-__global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 2) horner_fused_kernel(
-    const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_b, Dev<T> D,
-    Coef<T, EM, false> cf, T *__restrict__ rout, Sched sch, T a, T beta, T e2, T sc, int mode) {
-    pdl_sync();
-    using G = Geo<T, BX, BY>;
-    using SH = StageH<T, BX, BY>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    T *stages = reinterpret_cast<T *>(smem_raw);
-    T *UE = stages + S * SH::SZ;                         // [2][3][RP]
-    T *UH = UE + 2 * 3 * G::RP;                          // [2][3][RP]
-    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(UH + 2 * 3 * G::RP) + 15) & ~uintptr_t(15));
-    const int tid = threadIdx.x;
-    const bool hasA = tid < G::RP;
-    constexpr int MAIN = BX * G::EY;
-    const int ii = tid < MAIN ? tid % BX : BX, jj = tid < MAIN ? tid / BX : tid - MAIN;
-    const int rA = jj * G::EX + ii;
-    const int sE = (jj + 1) * G::WX + ii + G::OX;
-    const int sH = jj * G::WX + ii - 1 + G::OX;
-    const bool hasB = tid < G::NT;
-    const int tx = tid % BX, ty = tid / BX;
-    const int re = ty * G::EX + tx;
-    const int rh = (ty + 1) * G::EX + (tx + 1);
-    const int sB = (ty + 1) * G::WX + tx + G::OX;
-    T bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
-    const T bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
-    constexpr uint32_t BYTES = (uint32_t)(2 * 6 * G::PL * sizeof(T));
-    auto issue = [&](int slot, uint32_t L, int x0, int y0, int kz) {
-        T *dst = stages + slot * SH::SZ;
-        mbar_expect_tx(&bars[slot], BYTES);
-        tma_load_4d(dst, &tm_r, &bars[slot], x0 - G::OX, y0 - 1, kz, 0);
-        tma_load_4d(dst + SH::ST, &tm_b, &bars[slot], x0 - G::OX, y0 - 1, kz, 0);
-        (void)L;
-    };
-    if (tid == 0) {
-        for (int s2 = 0; s2 < S; ++s2) mbar_init(&bars[s2], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    uint32_t lcount = 0;
-    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
-        const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
-        const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
-        const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
-        const int nplanes = ke - kb + 2;
-        const int iE = x0 + ii, jE = y0 + jj;
-        const bool inE = hasA && iE < D.nx && jE < D.ny;
-        const bool lxE = inE && jE > 0, lyE = inE && iE > 0, lzE = inE && iE > 0 && jE > 0;
-        const int iH = iE - 1, jH = jE - 1;
-        const bool inH = hasA && iH >= 0 && jH >= 0 && iH < D.nx && jH < D.ny;
-        const bool lxH = inH && iH > 0, lyH = inH && jH > 0;
-        const int iB = x0 + tx, jB = y0 + ty;
-        const bool inB = hasB && iB < D.nx && jB < D.ny;
-        const bool lxBe = jB > 0, lyBe = iB > 0, lzBe = iB > 0 && jB > 0;
-        const bool lxBh = iB > 0, lyBh = jB > 0;
-        const int64_t gB = D.idx(inB ? iB : 0, inB ? jB : 0, 0);
-        T bhxk = T(0), bhyk = T(0);                       // b_h(k-1) at the own point (carried)
-        if (tid == 0)
-            for (int p = 0; p < min(S, nplanes); ++p) {
-                const uint32_t L = lcount + p;
-                issue((int)(L % S), L, x0, y0, kb - 1 + p);
-            }
-        for (int p = 0; p + 1 < nplanes; ++p) {
-            const int k = kb - 1 + p, kk = k + 1;
-            const uint32_t L0 = lcount + p, L1 = L0 + 1;
-            const bool doB = k >= kb && inB;
-            if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
-            mbar_wait(&bars[L1 % S], (L1 / S) & 1);
-            const T *P0 = stages + (L0 % S) * SH::SZ;    // r plane k
-            const T *P1 = stages + (L1 % S) * SH::SZ;    // r plane k+1
-            const T *B0 = P0 + SH::ST, *B1 = P1 + SH::ST; // b planes k, k+1
-            T *UE1 = UE + (kk & 1) * 3 * G::RP;
-            T *UH0 = UH + (k & 1) * 3 * G::RP;
-            T bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;
-            if (EM == 1) {
-                if (kk < D.nz) {
-                    bE0 = __ldg(cf.tab + kk) * cf.sig;
-                    bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
-                    bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
-                }
-                if (k >= 0) {
-                    bEk0 = __ldg(cf.tab + k) * cf.sig;
-                    bEk1 = __ldg(cf.tab + D.nz + k) * cf.sig;
-                    bEk2 = __ldg(cf.tab + 2 * D.nz + k) * cf.sig;
-                }
-            }
-            if (mode != 1 && hasA) {
-                {   // u_e(k+1) = bE .* C^T r_h
-                    T c0, c1, c2;
-                    curlT_stage<T, G>(P1, P0, sE, c0, c1, c2);
-                    const bool vk = kk < D.nz, kp = kk > 0;
-                    UE1[rA] = (lxE && vk && kp) ? bE0 * c0 : T(0);
-                    UE1[G::RP + rA] = (lyE && vk && kp) ? bE1 * c1 : T(0);
-                    UE1[2 * G::RP + rA] = (lzE && vk) ? bE2 * c2 : T(0);
-                }
-                {   // u_h(k) = -bH .* C r_e
-                    T c0, c1, c2;
-                    curl_stage<T, G>(P0, P1, sH, c0, c1, c2);
-                    const bool vk = k >= 0 && k < D.nz;
-                    UH0[rA] = (lxH && vk) ? -(bH0 * c0) : T(0);
-                    UH0[G::RP + rA] = (lyH && vk) ? -(bH1 * c1) : T(0);
-                    UH0[2 * G::RP + rA] = (inH && vk && k > 0) ? -(bH2 * c2) : T(0);
-                }
-            }
-            __syncthreads();
-            if (p == 0 && inB) {                          // b_h(kb-1) own for the first X b
-                bhxk = B0[3 * G::PL + sB];
-                bhyk = B0[4 * G::PL + sB];
-            }
-            if (doB) {
-                const T *UE0 = UE + (k & 1) * 3 * G::RP;
-                const T *UHm = UH + ((k - 1) & 1) * 3 * G::RP;
-                const bool kp = k > 0;
-                // X b at the own point (plane k)
-                T xb[6];
-                {
-                    const T *bhx = B0 + 3 * G::PL, *bhy = B0 + 4 * G::PL, *bhz = B0 + 5 * G::PL;
-                    const T hx0 = bhx[sB], hy0 = bhy[sB], hz0 = bhz[sB];
-                    const T d0 = ((hz0 - bhz[sB - G::WX]) - hy0) + bhyk;
-                    const T d1 = ((hx0 - bhxk) - hz0) + bhz[sB - 1];
-                    const T d2 = ((hy0 - bhy[sB - 1]) - hx0) + bhx[sB - G::WX];
-                    xb[0] = (lxBe && kp) ? bEk0 * d0 : T(0);
-                    xb[1] = (lyBe && kp) ? bEk1 * d1 : T(0);
-                    xb[2] = lzBe ? bEk2 * d2 : T(0);
-                    bhxk = hx0;
-                    bhyk = hy0;
-                    const T *bex = B0, *bey = B0 + G::PL, *bez = B0 + 2 * G::PL;
-                    const T ex0 = bex[sB], ey0 = bey[sB], ez0 = bez[sB];
-                    const T c0 = ((ey0 + bez[sB + G::WX]) - B1[G::PL + sB]) - ez0;
-                    const T c1 = ((ez0 + B1[sB]) - bez[sB + 1]) - ex0;
-                    const T c2 = ((ex0 + bey[sB + 1]) - bex[sB + G::WX]) - ey0;
-                    xb[3] = lxBh ? -(bH0 * c0) : T(0);
-                    xb[4] = lyBh ? -(bH1 * c1) : T(0);
-                    xb[5] = kp ? -(bH2 * c2) : T(0);
-                }
-                T x2[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
-                if (mode != 1) {                          // X u = X (X r) at the own point
-                    const T ux0 = UE0[re], uy0 = UE0[G::RP + re], uz0 = UE0[2 * G::RP + re];
-                    const T hx0 = UH0[rh], hy0 = UH0[G::RP + rh], hz0 = UH0[2 * G::RP + rh];
-                    const T uz_jp = UE0[2 * G::RP + re + G::EX], ux_jp = UE0[re + G::EX];
-                    const T uz_ip = UE0[2 * G::RP + re + 1], uy_ip = UE0[G::RP + re + 1];
-                    const T ux_kp = UE1[re], uy_kp = UE1[G::RP + re];
-                    const T c0 = ((uy0 + uz_jp) - uy_kp) - uz0;
-                    const T c1 = ((uz0 + ux_kp) - uz_ip) - ux0;
-                    const T c2 = ((ux0 + uy_ip) - ux_jp) - uy0;
-                    const T hz_jm = UH0[2 * G::RP + rh - G::EX], hx_jm = UH0[rh - G::EX];
-                    const T hz_im = UH0[2 * G::RP + rh - 1], hy_im = UH0[G::RP + rh - 1];
-                    const T hy_km = UHm[G::RP + rh], hx_km = UHm[rh];
-                    const T d0 = ((hz0 - hz_jm) - hy0) + hy_km;
-                    const T d1 = ((hx0 - hx_km) - hz0) + hz_im;
-                    const T d2 = ((hy0 - hy_im) - hx0) + hx_jm;
-                    x2[0] = (lxBe && kp) ? bEk0 * d0 : T(0);
-                    x2[1] = (lyBe && kp) ? bEk1 * d1 : T(0);
-                    x2[2] = lzBe ? bEk2 * d2 : T(0);
-                    x2[3] = lxBh ? -(bH0 * c0) : T(0);
-                    x2[4] = lyBh ? -(bH1 * c1) : T(0);
-                    x2[5] = kp ? -(bH2 * c2) : T(0);
-                }
-                T *ro = rout + gB + (int64_t)k * D.plane;
-#pragma unroll
-                for (int c = 0; c < 6; ++c) {
-                    const T bv = B0[c * G::PL + sB];
-                    T v = a * bv + beta * xb[c];
-                    if (mode != 1) v = v + sc * (x2[c] + e2 * P0[c * G::PL + sB]);
-                    ro[c * D.cs] = v;
-                }
-            }
-            __syncthreads();
-            if (tid == 0 && p + S < nplanes) {
-                const uint32_t L = lcount + p + S;
-                issue((int)(L % S), L, x0, y0, kb - 1 + p + S);
-            }
-        }
-        lcount += nplanes;
-    }
-}
-
-// ---------------------------------------------------------------------------------------
-// K2v: fp32 Newton pair, two x-adjacent points per thread (float2), own values in registers
-// ---------------------------------------------------------------------------------------
 // Tile 64 x 8.  Phase A: thread (pi, jj < BY) computes u_e(k+1) AND u_h(k) on the pair
 // (x0+2pi, x0+2pi+1) of row y0+jj -- the same pair whose w'(k), y(k) it updates in phase B, so
 // its own w(k), u_e(k), u_e(k+1), u_h(k), u_h(k-1) never leave registers.  The halo rows are
@@ -1720,262 +1287,6 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
 }
 
 // ---------------------------------------------------------------------------------------
-// K2r: the Newton pair with one point set and register-carried own values
-// ---------------------------------------------------------------------------------------
-// Every thread owns one point of U = [x0-1, x0+BX] x [y0-1, y0+BY] ((BX+2) x (BY+2)) and
-// computes there u_e(k+1) if the point is in E = [x0, x0+BX] x [y0, y0+BY] and u_h(k) if it is
-// in H = [x0-1, x0+BX-1] x [y0-1, y0+BY-1].  Tile points are threads 0 .. BX*BY-1 (whole
-// 32-wide rows); the 2-cell-wide halo frame follows.  Phase B of a tile thread takes w(k),
-// u_e(k), u_e(k+1), u_h(k), u_h(k-1) at its own point from registers and reads only the four
-// i+1/j+1 neighbours of u_e(k) and the four i-1/j-1 neighbours of u_h(k) from shared memory.
-// Rings: u_e 2 planes, u_h 1 plane (its phase-B readers finish before the next phase A).
-template <typename T, int BX, int BY>
-struct GeoU {
-    static constexpr int XU = BX + 2, YU = BY + 2, RU = XU * YU;
-    static constexpr int NTHR = ((RU + 31) / 32) * 32;
-};
-
-template <typename T, int EM, bool HA, int BX, int BY, int S>
-__global__ void __launch_bounds__(GeoU<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) pair_r_kernel(
-    const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
-    const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
-    T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode) {
-    pdl_sync();
-    using G = Geo<T, BX, BY>;
-    using U = GeoU<T, BX, BY>;
-    using SL = StageL<T, EM, HA, G>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    T *stages = reinterpret_cast<T *>(smem_raw);
-    T *UE = stages + S * SL::SZ;                         // [2][3][RU]
-    T *UH = UE + 2 * 3 * U::RU;                          // [3][RU]
-    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(UH + 3 * U::RU) + 15) & ~uintptr_t(15));
-    const int tid = threadIdx.x;
-    // own point (ui, uj) in U coordinates: global (x0 - 1 + ui, y0 - 1 + uj)
-    int ui, uj;
-    {
-        constexpr int NT = BX * BY, ROW = BX + 2;
-        if (tid < NT) { ui = 1 + tid % BX; uj = 1 + tid / BX; }
-        else if (tid < NT + ROW) { ui = tid - NT; uj = 0; }
-        else if (tid < NT + 2 * ROW) { ui = tid - NT - ROW; uj = BY + 1; }
-        else if (tid < NT + 2 * ROW + BY) { ui = 0; uj = 1 + (tid - NT - 2 * ROW); }
-        else { ui = BX + 1; uj = 1 + (tid - NT - 2 * ROW - BY); }
-    }
-    const bool has = tid < U::RU;
-    const bool isE = has && ui >= 1 && uj >= 1;          // ui <= BX+1, uj <= BY+1 always
-    const bool isH = has && ui <= BX && uj <= BY;
-    const bool isT = tid < BX * BY;
-    const int r = uj * U::XU + ui;                        // ring index
-    const int sS = uj * G::WX + ui - 1 + G::OX;           // stage index
-    T bE0 = cf.cEs[0] * cf.sig, bE1 = cf.cEs[1] * cf.sig, bE2 = cf.cEs[2] * cf.sig;
-    const T bH0 = cf.cHs[0] * cf.sig, bH1 = cf.cHs[1] * cf.sig, bH2 = cf.cHs[2] * cf.sig;
-    if (tid == 0) {
-        for (int s2 = 0; s2 < S; ++s2) mbar_init(&bars[s2], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    uint32_t lcount = 0;
-    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
-        const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
-        const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
-        const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
-        const int nplanes = ke - kb + 2;
-        const int ig = x0 - 1 + ui, jg = y0 - 1 + uj;
-        const bool in = has && ig >= 0 && jg >= 0 && ig < D.nx && jg < D.ny;
-        const bool inE = in && isE, inH = in && isH;
-        const bool lxE = inE && jg > 0, lyE = inE && ig > 0, lzE = inE && ig > 0 && jg > 0;
-        const bool lxH = inH && ig > 0, lyH = inH && jg > 0;
-        const bool doT = in && isT;
-        const int64_t gB = D.idx(doT ? ig : 0, doT ? jg : 0, 0);
-        // carried own-point values (plane k of the current iteration)
-        T hxk = T(0), hyk = T(0), hzk = T(0);      // w_h(k)
-        T exk = T(0), eyk = T(0);                  // w_e(k) (x, y)
-        T uek0 = T(0), uek1 = T(0), uek2 = T(0);   // u_e(k)
-        T uhm0 = T(0), uhm1 = T(0), uhm2 = T(0);   // u_h(k-1)
-        if (tid == 0)
-            for (int p = 0; p < min(S, nplanes); ++p) {
-                const uint32_t L = lcount + p;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                          &tm_cH, x0, y0, kb - 1 + p);
-            }
-        for (int p = 0; p + 1 < nplanes; ++p) {
-            const int k = kb - 1 + p, kk = k + 1;
-            const uint32_t L0 = lcount + p, L1 = L0 + 1;
-            const bool doB = doT && k >= kb;
-            T yv0 = T(0), yv1 = T(0), yv2 = T(0), yv3 = T(0), yv4 = T(0), yv5 = T(0);
-            if (doB && !init) {
-                const T *yp = y + gB + (int64_t)k * D.plane;
-                yv0 = yp[0];
-                yv1 = yp[D.cs];
-                yv2 = yp[2 * D.cs];
-                yv3 = yp[3 * D.cs];
-                yv4 = yp[4 * D.cs];
-                yv5 = yp[5 * D.cs];
-            }
-            if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
-            mbar_wait(&bars[L1 % S], (L1 / S) & 1);
-            const T *P0 = stages + (L0 % S) * SL::SZ;
-            const T *P1 = stages + (L1 % S) * SL::SZ;
-            T *UE1 = UE + (kk & 1) * 3 * U::RU;
-            const T *UE0 = UE + (k & 1) * 3 * U::RU;
-            T bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;
-            if (EM == 1) {
-                if (kk < D.nz) {
-                    bE0 = __ldg(cf.tab + kk) * cf.sig;
-                    bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
-                    bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
-                }
-                if (k >= 0) {
-                    bEk0 = __ldg(cf.tab + k) * cf.sig;
-                    bEk1 = __ldg(cf.tab + D.nz + k) * cf.sig;
-                    bEk2 = __ldg(cf.tab + 2 * D.nz + k) * cf.sig;
-                }
-            }
-            if (p == 0 && has) {                          // w(kb-1) at the own point
-                hxk = P0[3 * G::PL + sS];
-                hyk = P0[4 * G::PL + sS];
-                hzk = P0[5 * G::PL + sS];
-                exk = P0[sS];
-                eyk = P0[G::PL + sS];
-            }
-            // ---- phase A ----
-            const T hx1 = has ? P1[3 * G::PL + sS] : T(0), hy1 = has ? P1[4 * G::PL + sS] : T(0);
-            const T hz1 = has ? P1[5 * G::PL + sS] : T(0);
-            const T ex1 = has ? P1[sS] : T(0), ey1 = has ? P1[G::PL + sS] : T(0);
-            const T ezk = has ? P0[2 * G::PL + sS] : T(0);
-            T ue0 = T(0), ue1 = T(0), ue2 = T(0), uh0 = T(0), uh1 = T(0), uh2 = T(0);
-            if (isE) {   // u_e(k+1) = bE C^T w_h at plane k+1
-                const T *hx = P1 + 3 * G::PL, *hy = P1 + 4 * G::PL, *hz = P1 + 5 * G::PL;
-                const T hz_jm = hz[sS - G::WX], hx_jm = hx[sS - G::WX];
-                const T hz_im = hz[sS - 1], hy_im = hy[sS - 1];
-                const T c0 = ((hz1 - hz_jm) - hy1) + hyk;
-                const T c1 = ((hx1 - hxk) - hz1) + hz_im;
-                const T c2 = ((hy1 - hy_im) - hx1) + hx_jm;
-                const bool vk = kk < D.nz, kp = kk > 0;
-                T w0 = bE0, w1 = bE1, w2 = bE2;
-                if (EM == 2) {
-                    w0 = P1[SL::ST + sS] * cf.sig;
-                    w1 = P1[SL::ST + G::PL + sS] * cf.sig;
-                    w2 = P1[SL::ST + 2 * G::PL + sS] * cf.sig;
-                }
-                ue0 = (lxE && vk && kp) ? w0 * c0 : T(0);
-                ue1 = (lyE && vk && kp) ? w1 * c1 : T(0);
-                ue2 = (lzE && vk) ? w2 * c2 : T(0);
-                UE1[r] = ue0;
-                UE1[U::RU + r] = ue1;
-                UE1[2 * U::RU + r] = ue2;
-            }
-            if (isH) {   // u_h(k) = -bH C w_e at plane k
-                const T *ex = P0, *ey = P0 + G::PL, *ez = P0 + 2 * G::PL;
-                const T ez_jp = ez[sS + G::WX], ex_jp = ex[sS + G::WX];
-                const T ez_ip = ez[sS + 1], ey_ip = ey[sS + 1];
-                const T c0 = ((eyk + ez_jp) - ey1) - ezk;
-                const T c1 = ((ezk + ex1) - ez_ip) - exk;
-                const T c2 = ((exk + ey_ip) - ex_jp) - eyk;
-                const bool vk = k >= 0 && k < D.nz;
-                T g0 = bH0, g1 = bH1, g2 = bH2;
-                if (HA) {
-                    const int ch = SL::ST + SL::CE;
-                    g0 = P0[ch + sS] * cf.sig;
-                    g1 = P0[ch + G::PL + sS] * cf.sig;
-                    g2 = P0[ch + 2 * G::PL + sS] * cf.sig;
-                }
-                uh0 = (lxH && vk) ? -(g0 * c0) : T(0);
-                uh1 = (lyH && vk) ? -(g1 * c1) : T(0);
-                uh2 = (inH && vk && k > 0) ? -(g2 * c2) : T(0);
-                UH[r] = uh0;
-                UH[U::RU + r] = uh1;
-                UH[2 * U::RU + r] = uh2;
-            }
-            __syncthreads();
-            if (doB) {
-                T wn0 = T(0), wn1 = T(0), wn2 = T(0), wn3 = T(0), wn4 = T(0), wn5 = T(0);
-                const T w0 = exk, w1 = eyk, w2 = ezk, w3 = hxk, w4 = hyk, w5 = hzk;
-                if (mode != 1) {
-                    // w'_h(k) = -bH C u_e(k) + e2 w_h
-                    const T uz_jp = UE0[2 * U::RU + r + U::XU], ux_jp = UE0[r + U::XU];
-                    const T uz_ip = UE0[2 * U::RU + r + 1], uy_ip = UE0[U::RU + r + 1];
-                    const T c0 = ((uek1 + uz_jp) - ue1) - uek2;
-                    const T c1 = ((uek2 + ue0) - uz_ip) - uek0;
-                    const T c2 = ((uek0 + uy_ip) - ux_jp) - uek1;
-                    // w'_e(k) = bE C^T u_h(k) + e2 w_e
-                    const T hz_jm = UH[2 * U::RU + r - U::XU], hx_jm = UH[r - U::XU];
-                    const T hz_im = UH[2 * U::RU + r - 1], hy_im = UH[U::RU + r - 1];
-                    const T d0 = ((uh2 - hz_jm) - uh1) + uhm1;
-                    const T d1 = ((uh0 - uhm0) - uh2) + hz_im;
-                    const T d2 = ((uh1 - hy_im) - uh0) + hx_jm;
-                    T be0 = bEk0, be1 = bEk1, be2 = bEk2, bh0 = bH0, bh1 = bH1, bh2 = bH2;
-                    if (EM == 2) {
-                        be0 = P0[SL::ST + sS] * cf.sig;
-                        be1 = P0[SL::ST + G::PL + sS] * cf.sig;
-                        be2 = P0[SL::ST + 2 * G::PL + sS] * cf.sig;
-                    }
-                    if (HA) {
-                        const int ch = SL::ST + SL::CE;
-                        bh0 = P0[ch + sS] * cf.sig;
-                        bh1 = P0[ch + G::PL + sS] * cf.sig;
-                        bh2 = P0[ch + 2 * G::PL + sS] * cf.sig;
-                    }
-                    const bool kp = k > 0, lxBe = jg > 0, lyBe = ig > 0, lzBe = ig > 0 && jg > 0;
-                    wn0 = ((lxBe && kp) ? be0 * d0 : T(0)) + e2 * w0;
-                    wn1 = ((lyBe && kp) ? be1 * d1 : T(0)) + e2 * w1;
-                    wn2 = (lzBe ? be2 * d2 : T(0)) + e2 * w2;
-                    wn3 = ((ig > 0) ? -(bh0 * c0) : T(0)) + e2 * w3;
-                    wn4 = ((jg > 0) ? -(bh1 * c1) : T(0)) + e2 * w4;
-                    wn5 = (kp ? -(bh2 * c2) : T(0)) + e2 * w5;
-                }
-                const int64_t go = gB + (int64_t)k * D.plane;
-                if (mode == 0) {
-                    T *wo = wout + go;
-                    wo[0] = wn0;
-                    wo[D.cs] = wn1;
-                    wo[2 * D.cs] = wn2;
-                    wo[3 * D.cs] = wn3;
-                    wo[4 * D.cs] = wn4;
-                    wo[5 * D.cs] = wn5;
-                }
-                T q0 = (yv0 + a * w0) + b * uek0, q1 = (yv1 + a * w1) + b * uek1;
-                T q2 = (yv2 + a * w2) + b * uek2, q3 = (yv3 + a * w3) + b * uh0;
-                T q4 = (yv4 + a * w4) + b * uh1, q5 = (yv5 + a * w5) + b * uh2;
-                if (mode == 2) {
-                    q0 = q0 + cl * wn0;
-                    q1 = q1 + cl * wn1;
-                    q2 = q2 + cl * wn2;
-                    q3 = q3 + cl * wn3;
-                    q4 = q4 + cl * wn4;
-                    q5 = q5 + cl * wn5;
-                }
-                T *yo = y + go;
-                yo[0] = q0;
-                yo[D.cs] = q1;
-                yo[2 * D.cs] = q2;
-                yo[3 * D.cs] = q3;
-                yo[4 * D.cs] = q4;
-                yo[5 * D.cs] = q5;
-            }
-            // carry plane k+1 -> k
-            hxk = hx1;
-            hyk = hy1;
-            hzk = hz1;
-            exk = ex1;
-            eyk = ey1;
-            uek0 = ue0;
-            uek1 = ue1;
-            uek2 = ue2;
-            uhm0 = uh0;
-            uhm1 = uh1;
-            uhm2 = uh2;
-            __syncthreads();
-            if (tid == 0 && p + S < nplanes) {
-                const uint32_t L = lcount + p + S;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                          &tm_cH, x0, y0, kb - 1 + p + S);
-            }
-        }
-        lcount += nplanes;
-    }
-}
-
-// ---------------------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -2014,14 +1325,18 @@ static int make_map(CUtensorMap *m, const Grid &g, const void *base, int ncomp, 
     return PARAEXP_OK;
 }
 
-static int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
+static int num_sms() {   // of the current device (cached per device)
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    cache[dev] = n;
     return n;
 }
 
@@ -2085,95 +1400,24 @@ static Sched launch_sched(const Grid &g, Sched sch, int grid) {
     return sch;
 }
 
-template <typename T, int EM, bool HA, int BX, int BY, int S, bool ONEBAR>
-struct FusedCfg {
-    using G = Geo<T, BX, BY>;
-    static constexpr int NR = ONEBAR ? 3 : 2;
-    static constexpr size_t lf_smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + NR * 3 * G::RP) * sizeof(T) + 8 * S + 16;
-    static constexpr size_t pair_smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 2 * NR * 3 * G::RP) * sizeof(T) + 8 * S + 16;
-};
-
-// kernel variant: (S = 3, two barriers per plane) by default; PARAEXP_ONEBAR=1 selects
-// (S = 4, one barrier per plane).
-static bool onebar() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PARAEXP_ONEBAR");
-        v = (e && atoi(e) != 0) ? 1 : 0;
-    }
-    return v == 1;
-}
-
-static int env_stages(const char *name, int dflt) {
-    const char *e = getenv(name);
-    const int v = e ? atoi(e) : dflt;
-    return (v >= 2 && v <= 5) ? v : dflt;
-}
-// measured on B200 (tools/kbench.py, 256^3): fp64 pair S = 3, fp32 pair S = 4
-static int pair_stages(bool fp64) {
-    static int v64 = env_stages("PARAEXP_PAIR_S", 3);
-    static int v32 = env_stages("PARAEXP_PAIR_S", 4);
-    return fp64 ? v64 : v32;
-}
-static int lf_stages() {
-    static int v = env_stages("PARAEXP_LF_S", 3);
-    return v;
-}
-
+// occupancy per SM of a kernel at its shared-memory size, cached per (device, kernel): the
+// dynamic shared-memory opt-in (cudaFuncSetAttribute) is per device context, so a grid on a
+// second device gets its own attribute call
 template <typename K>
 static int resident_per_sm(K kern, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_pair(dev, (const void *)kern);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    cache[key] = per_sm;
     return per_sm;
-}
-
-template <typename T, int EM, bool HA, int S, bool ONEBAR, bool TR>
-static int leapfrog_fused_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int nsrc,
-                            const void *q_dev, const std::vector<SrcDev> &hsrc, const TraceDev *tr) {
-    constexpr int BX = 32, BY = 8;
-    using Cfg = FusedCfg<T, EM, HA, BX, BY, S, ONEBAR>;
-    using G = Geo<T, BX, BY>;
-    const Grid &g = *ka.g;
-    auto kern = leapfrog_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR, TR>;
-    static const int per_sm = resident_per_sm(kern, G::NTHR, Cfg::lf_smem);
-    if (per_sm < 1) return fail(PARAEXP_ECUDA, "fused leapfrog kernel does not fit on an SM");
-    const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
-    const int grid = std::min(sch.units, per_sm * num_sms());
-    auto D = make_dev<T>(g);
-    auto cf = make_coef<T, EM, HA>(g, 1.0);
-    CUtensorMap tmE, tmH, tmA, tmB;
-    int rc;
-    if (EM == 2 && (rc = make_map<T>(&tmE, g, g.d_cE_arr, 3, G::WX, G::HY))) return rc;
-    if (HA && (rc = make_map<T>(&tmH, g, g.d_cH_arr, 3, G::WX, G::HY))) return rc;
-    if ((rc = make_map<T>(&tmA, g, bufs[0], 6, G::WX, G::HY))) return rc;
-    if ((rc = make_map<T>(&tmB, g, bufs[1], 6, G::WX, G::HY))) return rc;
-    SrcList sl;
-    sl.n = nsrc;
-    for (int r = 0; r < nsrc && r < 16; ++r) {
-        sl.c[r] = hsrc[r].comp;
-        sl.i[r] = hsrc[r].i;
-        sl.j[r] = hsrc[r].j;
-        sl.k[r] = hsrc[r].k;
-    }
-    cudaStream_t s = (cudaStream_t)ka.stream;
-    TraceDev trm;
-    if (TR) trm = *tr;
-    for (int64_t m = 0; m < nsteps; ++m) {
-        const bool even = (m % 2) == 0;
-        if (TR) {
-            trm.energy = tr->energy ? tr->energy + m : nullptr;
-            trm.probe = tr->probe ? tr->probe + m * tr->np : nullptr;
-            if (!trm.probe) trm.np = 0;
-        }
-        launch_k(kern, grid, G::NTHR, Cfg::lf_smem, s, even ? tmA : tmB, tmE, tmH, D, cf,
-                                                 (T *)(even ? bufs[1] : bufs[0]),
-                                                 ka.static_sched ? sch : launch_sched(g, sch, grid), sl,
-                                                 nsrc ? (const T *)q_dev + m * nsrc : nullptr, trm);
-        ++*ka.launches;
-    }
-    if (nsteps % 2) std::swap(bufs[0], bufs[1]);
-    return check_cuda("leapfrog fused");
 }
 
 // K1r launcher (same schedule and maps as K1)
@@ -2185,7 +1429,7 @@ static int leapfrog_r_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int
     constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 2 * 3 * G::RP) * sizeof(T) + 8 * S + 16;
     const Grid &g = *ka.g;
     auto kern = leapfrog_r_kernel<T, EM, HA, BX, BY, S, TR>;
-    static const int per_sm = resident_per_sm(kern, G::NTHR, smem);
+    const int per_sm = resident_per_sm(kern, G::NTHR, smem);
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "leapfrog_r kernel does not fit on an SM");
     const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
     const int grid = std::min(sch.units, per_sm * num_sms());
@@ -2233,7 +1477,7 @@ static int leapfrog_v_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int
     constexpr size_t smem = (size_t)(S * StageL<float, EM, HA, G>::SZ + 2 * 3 * G::RP) * sizeof(float) + 8 * S + 16;
     const Grid &g = *ka.g;
     auto kern = leapfrog_v_kernel<EM, HA, BY, S, TR>;
-    static const int per_sm = resident_per_sm(kern, G::NTHR, smem);
+    const int per_sm = resident_per_sm(kern, G::NTHR, smem);
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "leapfrog_v kernel does not fit on an SM");
     const Sched sch = make_sched(g, G::BX, BY, per_sm * num_sms());
     const int grid = std::min(sch.units, per_sm * num_sms());
@@ -2272,26 +1516,6 @@ static int leapfrog_v_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int
     return check_cuda("leapfrog_v");
 }
 
-static bool lf_vec_enabled() {   // K1v for fp32 (default); PARAEXP_LF_VEC=0 selects K1r
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PARAEXP_LF_VEC");
-        v = (e && atoi(e) == 0) ? 0 : 1;
-    }
-    return v == 1;
-}
-
-// kernel generation: r (row-aligned, register-carried; default) or the first fused kernels
-// (PARAEXP_KERNEL_V1=1)
-static bool kernels_v1() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PARAEXP_KERNEL_V1");
-        v = (e && atoi(e) != 0) ? 1 : 0;
-    }
-    return v == 1;
-}
-
 int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev *src_dev,
                      int nsrc, const void *q_dev, const TraceDev *tr) {
     if (nsrc > 16) return k_leapfrog_unfused(ka, bufs[0], nsteps, src_dev, nsrc, q_dev, tr);
@@ -2301,42 +1525,25 @@ int k_leapfrog_fused(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const 
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
-        if (!kernels_v1()) {
-            if constexpr (std::is_same<T, float>::value) {
-                if (lf_vec_enabled()) {
-                    if (trace) return leapfrog_v_V<EM, HA, 3, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
-                    return leapfrog_v_V<EM, HA, 3, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
-                }
-            }
+        if constexpr (std::is_same<T, float>::value) {   // K1v: fp32, two points per thread
+            if (trace) return leapfrog_v_V<EM, HA, 3, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
+            return leapfrog_v_V<EM, HA, 3, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
+        } else {                                            // K1r: fp64
             if (trace) return leapfrog_r_V<T, EM, HA, 3, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
             return leapfrog_r_V<T, EM, HA, 3, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
         }
-        if (trace) return leapfrog_fused_V<T, EM, HA, 3, false, true>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
-        if (onebar()) return leapfrog_fused_V<T, EM, HA, 4, true, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
-        if (lf_stages() == 4) return leapfrog_fused_V<T, EM, HA, 4, false, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
-        return leapfrog_fused_V<T, EM, HA, 3, false, false>(ka, bufs, nsteps, nsrc, q_dev, hsrc, tr);
     });
 }
 
-constexpr int kMaxMultiOps = 256;
-// opt-in (PARAEXP_MULTI=1): measured no faster than PDL-overlapped single-op launches at 64^3
-// (6.7 vs 6.4 us per A-application) -- a unit's z-march latency, not the launch, bounds there
-static bool multi_enabled() {
-    static const bool on = [] {
-        const char *e = getenv("PARAEXP_MULTI");
-        return e && atoi(e) != 0;
-    }();
-    return on;
-}
-
-template <typename T, int EM, bool HA, int S, bool ONEBAR>
+// K2 launcher (fp64): one launch per pair op; w ping-pongs between bufs[0] and bufs[2]
+template <typename T, int EM, bool HA, int S>
 static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     constexpr int BX = 32, BY = 8;
-    using Cfg = FusedCfg<T, EM, HA, BX, BY, S, ONEBAR>;
     using G = Geo<T, BX, BY>;
+    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 2 * 2 * 3 * G::RP) * sizeof(T) + 8 * S + 16;
     const Grid &g = *ka.g;
-    auto kern = pair_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR>;
-    static const int per_sm = resident_per_sm(kern, G::NTHR, Cfg::pair_smem);
+    auto kern = pair_fused_kernel<T, EM, HA, BX, BY, S>;
+    const int per_sm = resident_per_sm(kern, G::NTHR, smem);
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "fused pair kernel does not fit on an SM");
     const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
     const int grid = std::min(sch.units, per_sm * num_sms());
@@ -2354,36 +1561,12 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     int init = 1;
     EtDev et;
     if (ka.et) et = *ka.et;
-    const int nops = (int)plan.ops.size();
-    if (multi_enabled() && !ka.et && nops >= 2 && nops <= kMaxMultiOps && grid >= sch.units) {
-        // one wave: the whole substep in ONE cooperative launch (grid barrier between ops)
-        auto kernM = pair_fused_kernel<T, EM, HA, BX, BY, S, ONEBAR, true>;
-        static const int per_smM = resident_per_sm(kernM, G::NTHR, Cfg::pair_smem);
-        if (per_smM >= per_sm) {
-            Grid &GG = const_cast<Grid &>(g);
-            if (!GG.d_ops && (rc = dev_alloc(&GG.d_ops, kMaxMultiOps * sizeof(Op)))) return rc;
-            cudaMemcpyAsync(GG.d_ops, plan.ops.data(), nops * sizeof(Op), cudaMemcpyHostToDevice, s);
-            unsigned *gbar = (unsigned *)((char *)GG.d_sched + 64);
-            cudaMemsetAsync(gbar, 0, sizeof(unsigned), s);
-            launch_coop(kernM, grid, G::NTHR, Cfg::pair_smem, s, tmW, tmE, tmH, D, cf, sp, yy, sch, T(0), T(0),
-                        T(0), T(0), 1, 0, et, tmS, w, (const Op *)GG.d_ops, nops, gbar);
-            ++*ka.launches;
-            for (const Op &op : plan.ops)
-                if (op.kind == 0) std::swap(w, sp);
-            bufs[0] = yy;
-            bufs[1] = w;
-            bufs[2] = sp;
-            bufs[3] = sp2;
-            return check_cuda("poly fused multi");
-        }
-    }
     int opi = 0;
     for (const Op &op : plan.ops) {
         et.op = opi++;
         et.apps = op.kind == 1 ? 1 : 2;
-        launch_k(kern, grid, G::NTHR, Cfg::pair_smem, s, tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a), T(op.b),
-                                                   T(op.e2), T(op.c), init, op.kind, et, tmW, sp, (const Op *)nullptr, 0,
-                                                   (unsigned *)nullptr);
+        launch_k(kern, grid, G::NTHR, smem, s, tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a),
+                 T(op.b), T(op.e2), T(op.c), init, op.kind, et);
         ++*ka.launches;
         if (op.kind == 0) {
             std::swap(w, sp);
@@ -2398,113 +1581,6 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     return check_cuda("poly fused");
 }
 
-static bool pair_r_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PARAEXP_PAIR_R");
-        v = (e && atoi(e) != 0) ? 1 : 0;
-    }
-    return v == 1;
-}
-
-// K2r launcher (same schedule, maps and buffer protocol as K2)
-template <typename T, int EM, bool HA, int S>
-static int poly_r_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
-    constexpr int BX = 32, BY = 8;
-    using G = Geo<T, BX, BY>;
-    using U = GeoU<T, BX, BY>;
-    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 3 * 3 * U::RU) * sizeof(T) + 8 * S + 16;
-    const Grid &g = *ka.g;
-    auto kern = pair_r_kernel<T, EM, HA, BX, BY, S>;
-    static const int per_sm = resident_per_sm(kern, U::NTHR, smem);
-    if (per_sm < 1) return fail(PARAEXP_ECUDA, "pair_r kernel does not fit on an SM");
-    const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
-    const int grid = std::min(sch.units, per_sm * num_sms());
-    auto D = make_dev<T>(g);
-    auto cf = make_coef<T, EM, HA>(g, plan.sigma);
-    CUtensorMap tmE, tmH;
-    int rc;
-    if (EM == 2 && (rc = make_map<T>(&tmE, g, g.d_cE_arr, 3, G::WX, G::HY))) return rc;
-    if (HA && (rc = make_map<T>(&tmH, g, g.d_cH_arr, 3, G::WX, G::HY))) return rc;
-    cudaStream_t s = (cudaStream_t)ka.stream;
-    T *w = (T *)bufs[0], *yy = (T *)bufs[1], *sp = (T *)bufs[2], *sp2 = (T *)bufs[3];
-    CUtensorMap tmW, tmS;
-    if ((rc = make_map<T>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
-    if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
-    int init = 1;
-    for (const Op &op : plan.ops) {
-        launch_k(kern, grid, U::NTHR, smem, s, tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a), T(op.b), T(op.e2), T(op.c),
-                                          init, op.kind);
-        ++*ka.launches;
-        if (op.kind == 0) {
-            std::swap(w, sp);
-            std::swap(tmW, tmS);
-        }
-        init = 0;
-    }
-    bufs[0] = yy;
-    bufs[1] = w;
-    bufs[2] = sp;
-    bufs[3] = sp2;
-    return check_cuda("poly_r");
-}
-
-// K2H launcher: the ops from the innermost (last) to the outermost; bufs[0] = b is read by
-// every step, the nest ping-pongs between bufs[1] and bufs[2]; on return bufs[0] = result.
-template <typename T, int EM, int S>
-static int poly_horner_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
-    constexpr int BX = 32, BY = 8;
-    using G = Geo<T, BX, BY>;
-    using SH = StageH<T, BX, BY>;
-    constexpr size_t smem = (size_t)(S * SH::SZ + 2 * 2 * 3 * G::RP) * sizeof(T) + 8 * S + 16;
-    const Grid &g = *ka.g;
-    auto kern = horner_fused_kernel<T, EM, BX, BY, S>;
-    static const int per_sm = resident_per_sm(kern, G::NTHR, smem);
-    if (per_sm < 1) return fail(PARAEXP_ECUDA, "horner kernel does not fit on an SM");
-    const Sched sch = make_sched(g, BX, BY, per_sm * num_sms());
-    const int grid = std::min(sch.units, per_sm * num_sms());
-    auto D = make_dev<T>(g);
-    auto cf = make_coef<T, EM, false>(g, plan.sigma);
-    cudaStream_t s = (cudaStream_t)ka.stream;
-    void *bb = bufs[0], *r1 = bufs[1], *r2 = bufs[2];
-    CUtensorMap tmB, tm1, tm2;
-    int rc;
-    if ((rc = make_map<T>(&tmB, g, bb, 6, G::WX, G::HY))) return rc;
-    if ((rc = make_map<T>(&tm1, g, r1, 6, G::WX, G::HY))) return rc;
-    if ((rc = make_map<T>(&tm2, g, r2, 6, G::WX, G::HY))) return rc;
-    const int K = (int)plan.ops.size();
-    const CUtensorMap *in = &tmB;
-    void *out = r1;
-    for (int q = K - 1; q >= 0; --q) {
-        const Op &op = plan.ops[q];
-        const T sc = (T)(q == K - 1 ? op.c : 1.0);
-        const int mode = op.kind == 1 ? 1 : 0;
-        launch_k(kern, grid, G::NTHR, smem, s, *in, tmB, D, cf, (T *)out, launch_sched(g, sch, grid), T(op.a), T(op.b),
-                                          T(op.e2), sc, mode);
-        ++*ka.launches;
-        in = out == r1 ? &tm1 : &tm2;
-        out = out == r1 ? r2 : r1;
-    }
-    void *res = out == r1 ? r2 : r1;                     // the last written buffer
-    bufs[0] = res;
-    bufs[1] = bb;
-    bufs[2] = res == r1 ? r2 : r1;
-    return check_cuda("poly horner");
-}
-
-// K2H is opt-in (PARAEXP_HORNER=2|3 stages): on B200 fp64 256^3 it measured 304 (2 stages,
-// 2 CTAs/SM) / 298 (3 stages, 1 CTA/SM) vs K2's 284 us per A-application -- the 25% fewer HBM
-// bytes do not pay for the extra X b stencil and the lower occupancy
-static int horner_stages() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PARAEXP_HORNER");
-        v = e ? atoi(e) : 0;
-        if (v != 0 && v != 2 && v != 3) v = 0;
-    }
-    return v;
-}
-
 // K2v launcher (64 x BY tiles, two points per thread; same buffer protocol as K2)
 template <typename T, int EM, bool HA, int BY, int S>
 static int poly_v_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
@@ -2513,8 +1589,8 @@ static int poly_v_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 3 * 3 * RR) * sizeof(T) + 8 * S + 16;
     const Grid &g = *ka.g;
     auto kern = ka.et ? pair_v_kernel<T, EM, HA, BY, S, true> : pair_v_kernel<T, EM, HA, BY, S, false>;
-    static const int per_sm = resident_per_sm(pair_v_kernel<T, EM, HA, BY, S, true>, G::NTHR, smem);
-    static const int per_sm2 = resident_per_sm(pair_v_kernel<T, EM, HA, BY, S, false>, G::NTHR, smem);
+    const int per_sm = resident_per_sm(pair_v_kernel<T, EM, HA, BY, S, true>, G::NTHR, smem);
+    const int per_sm2 = resident_per_sm(pair_v_kernel<T, EM, HA, BY, S, false>, G::NTHR, smem);
     if (per_sm2 < per_sm) return fail(PARAEXP_ECUDA, "pair_v variants differ in occupancy");
     if (per_sm < 1) return fail(PARAEXP_ECUDA, "pair_v kernel does not fit on an SM");
     const Sched sch = make_sched(g, G::BX, BY, per_sm * num_sms());
@@ -2558,28 +1634,10 @@ int k_poly_substep_fused(const KernelArgs &ka, const Plan &plan, void *bufs[4]) 
         using T = decltype(tT);
         constexpr int EM = decltype(tEM)::value;
         constexpr bool HA = decltype(tHA)::value;
-        if constexpr (EM != 2 && !HA && std::is_same<T, double>::value) {
-            // K2H (nested evaluation, 18 instead of 24 values per pair) unless early
-            // termination needs the forward sum
-            if (!ka.et && horner_stages() == 2) return poly_horner_V<T, EM, 2>(ka, plan, bufs);
-            if (!ka.et && horner_stages() == 3) return poly_horner_V<T, EM, 3>(ka, plan, bufs);
-        }
-        if constexpr (std::is_same<T, float>::value) {
-            if (lf_vec_enabled()) return poly_v_V<float, EM, HA, 8, 3>(ka, plan, bufs);   // K2v (fp32)
-        }
-        // K2r measured slower than K2 on B200 (fp64 306 vs 289 us per A-application: barrier
-        // stalls -- the frame threads idle through phase B); opt-in with PARAEXP_PAIR_R=1
-        if (pair_r_enabled() && !ka.et) {   // K2r has no early-termination path
-            if (pair_stages(sizeof(T) == 8) == 4) return poly_r_V<T, EM, HA, 4>(ka, plan, bufs);
-            return poly_r_V<T, EM, HA, 3>(ka, plan, bufs);
-        }
-        if (onebar()) return poly_fused_V<T, EM, HA, 4, true>(ka, plan, bufs);
-        switch (pair_stages(sizeof(T) == 8)) {
-            case 2: return poly_fused_V<T, EM, HA, 2, false>(ka, plan, bufs);
-            case 4: return poly_fused_V<T, EM, HA, 4, false>(ka, plan, bufs);
-            case 5: return poly_fused_V<T, EM, HA, 5, false>(ka, plan, bufs);
-            default: return poly_fused_V<T, EM, HA, 3, false>(ka, plan, bufs);
-        }
+        if constexpr (std::is_same<T, float>::value)
+            return poly_v_V<float, EM, HA, 8, 3>(ka, plan, bufs);   // K2v: fp32, two points per thread
+        else
+            return poly_fused_V<T, EM, HA, 3>(ka, plan, bufs);      // K2: fp64
     });
 }
 

@@ -238,6 +238,10 @@ void grid_free_device(Grid &G) {
     G.events.clear();
     dev_free(G.d_sched);
     G.d_sched = nullptr;
+    dev_free(G.d_norms);
+    G.d_norms = nullptr;
+    if (G.call_event) dev_event_destroy(G.call_event);
+    G.call_event = G.call_stream = nullptr;
     dev_free(G.d_ops);
     G.d_ops = nullptr;
     G.sched_base = 0;

@@ -66,6 +66,9 @@ struct Grid {
     std::vector<void *> streams; // their cudaStream_t / cudaEvent_t handles (created on demand)
     std::vector<void *> events;
     void *d_ops = nullptr;      // pair-op table of the multi-op (cooperative) pair launch
+    void *d_norms = nullptr;    // per-propagator energy norms of a solve (rho safety net, f. intervals)
+    void *call_event = nullptr; // recorded at the end of every call (stream order across calls)
+    void *call_stream = nullptr;
     void *d_sched = nullptr;    // monotone unit counter of the fused kernels' dynamic schedule
     unsigned long long sched_base = 0;   // host shadow: value of *d_sched before the next launch
     int64_t d_q_cap = 0;

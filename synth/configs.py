@@ -241,6 +241,16 @@ def config_c5(n=128, dtype="f32", nsteps=1024, p=8) -> Workload:
                     u0_seed=5 + n, method="leja", m=64, s=1, eps_A=1e-12)
 
 
+def config_c5s(n=768, dtype="f64", nsteps=1024, p=8) -> Workload:
+    """C5s (an addition, SURVEY 8(d) C5 note): C5's vacuum n^3 with random u0 PLUS one centred
+    GAUSS_PAPER z-edge source (sigma_t = 128 ps), so the particular sweeps are not identically
+    zero and ParaExp does not degenerate to one exp(T A) u0.  Auto Leja plan at eps_A = 1e-10
+    (as C2-C4), n_t = 1024 [P], p in {8, 16, 64}."""
+    src = [Source(2, n // 2, n // 2, n // 2, "gauss_paper", 1.0, 128e-12)]
+    return Workload(f"C5s-{n}-{dtype}-p{p}", n, n, n, 1e-3, dtype, 0.95, nsteps, p,
+                    sources=src, u0_seed=5 + n, method="leja", eps_A=1e-10)
+
+
 def config_wave2d(n_pts=41, k=1.0, nsteps=None, p=8, dt_frac=0.99, dtype="f64") -> Workload:
     """The paper's two-dimensional cylindrical wave (Fig. 2): vacuum PEC box
     L_x = L_y = 20 m, L_z = 1 m ("L_y = 1 m" read as L_z, reading 21), n_x = n_y =

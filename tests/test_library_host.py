@@ -49,6 +49,50 @@ def test_partition_and_schedule():
             assert len(roots) == 1
 
 
+def _makespan(blocks, p, ratio, u0):
+    return max((l - f + 1) + (p - f) * ratio + (ratio if (f == 1 and u0) else 0.0)
+               for f, l in blocks if f >= 1)
+
+
+def _brute_optimum(p, world, ratio, u0):
+    """min over every split of 1..p into at most `world` contiguous non-empty blocks."""
+    import itertools
+    best = math.inf
+    for k in range(1, min(p, world) + 1):
+        for cuts in itertools.combinations(range(2, p + 1), k - 1):
+            starts = (1,) + cuts
+            blocks = [(f, (starts[q + 1] - 1 if q + 1 < k else p)) for q, f in enumerate(starts)]
+            best = min(best, _makespan(blocks, p, ratio, u0))
+    return best
+
+
+@pytest.mark.parametrize("ratio", [0.5, 1.0, 3.0, 7.25])
+@pytest.mark.parametrize("u0", [False, True])
+def test_cost_balanced_schedule_is_optimal(ratio, u0):
+    """paraexp_schedule with a tail ratio: contiguous blocks in rank order that
+    cover 1..p exactly once, the root owns p, and the largest rank cost equals the brute-force
+    optimum over all contiguous splits (never above the equal-share split)."""
+    for p in (1, 2, 3, 5, 8, 11):
+        for world in (1, 2, 3, 4, 8):
+            blocks, roots = [], set()
+            for r in range(world):
+                f, l, root = pe.schedule(p, world, r, ratio, u0)
+                roots.add(root)
+                if f >= 1:
+                    blocks.append((f, l))
+                    if l == p:
+                        assert root == r
+                else:
+                    assert l == -1
+            assert len(roots) == 1
+            cover = [j for f, l in blocks for j in range(f, l + 1)]
+            assert cover == list(range(1, p + 1))              # contiguous, in rank order
+            ms = _makespan(blocks, p, ratio, u0)
+            assert abs(ms - _brute_optimum(p, world, ratio, u0)) < 1e-9, (p, world, blocks)
+            eq = [pe.schedule(p, world, r) for r in range(world)]
+            assert ms <= _makespan([(f, l) for f, l, _ in eq if f >= 1], p, ratio, u0) + 1e-9
+
+
 def test_leja_points_match_oracle():
     assert pe.leja_points(101) == list(fit.leja_points(101))
 

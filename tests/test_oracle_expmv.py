@@ -230,3 +230,19 @@ def test_horner_equals_forward_and_complex(method, m, s):
     ref = np.concatenate([ce, ch])
     for got in (np.concatenate([he, hh]), np.concatenate([fe, fh])):
         assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("method,m,s", [("leja", 16, 3), ("leja", 1, 2), ("taylor", 12, 2), ("leja", 40, 1)])
+def test_pairs_c_loops_equal_numpy(dtype, method, m, s):
+    """The C loops of or_expmv_pairs run expmv_pairs_numpy's recurrence step for step: the
+    same fields (no contraction in the oracle build, so bit-equal up to OpenMP-free order)."""
+    n = (7, 5, 6)
+    g = fit.Grid(*n, d0=1e-3, eps_r=np.random.default_rng(2).uniform(1, 4, 210), dt_frac=0.9,
+                 dtype=dtype)
+    e, h = g.clean(*random_fields(*n, seed=4))
+    plan = fit.make_plan(method, m, s, 12 * g.dt, g.rho_cfl)
+    a = fit.expmv_pairs_numpy(g, plan, e, h, dtype)
+    b = fit.expmv_pairs(g, plan, e, h, dtype)
+    for x, y in zip(a, b):
+        assert np.abs(x - y).max() <= 1e-15 * np.abs(x).max()

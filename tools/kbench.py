@@ -32,8 +32,7 @@ def main():
     cells = w.cells
     print(f"n={n} {dtype} {kernels} chunk={os.environ.get('PARAEXP_ZCHUNK', 'auto')}: "
           f"leapfrog {lf_ms * 1e3:.1f} us/step {12 * es * cells / lf_ms / 1e6:.0f} GB/s | "
-          f"expmv {ex_ms * 1e3:.1f} us/A-app {cells / ex_ms / 1e6:.2f} G A-app/s "
-          f"(PARAEXP_PAIR2={os.environ.get('PARAEXP_PAIR2', '1')})", flush=True)
+          f"expmv {ex_ms * 1e3:.1f} us/A-app {cells / ex_ms / 1e6:.2f} G A-app/s", flush=True)
 
 
 if __name__ == "__main__":
