@@ -177,6 +177,27 @@ __device__ __forceinline__ T stage_bH(const Coef<T, EM, HA> &cf, const T *st, in
     return cf.cHs[c] * cf.sig;
 }
 
+// z-table coefficients (EM == 1, layered materials) of a unit's planes kb-1 .. kb+nplanes-2,
+// scaled by sigma, staged in shared memory once per unit: a per-plane __ldg of the table from
+// global memory sat on the critical path of every plane iteration (ncu: ~8-11% of the warp
+// stall samples of K1r / K2 waited on it -- the streaming y / state traffic evicts the table's
+// lines from L1).  zt[c * ZT_ROW + q] = bE_c at plane kb - 1 + q (0 outside [0, nz)).
+constexpr int ZT_ROW = 132;      // >= max z-chunk (130, make_sched) + 2
+template <typename T, int EM>
+struct ZtL {
+    static constexpr int N = EM == 1 ? 3 * ZT_ROW : 0;
+};
+template <typename T, int EM, bool HA>
+__device__ __forceinline__ void stage_ztab(T *zt, const Coef<T, EM, HA> &cf, int kb, int nplanes, int nz) {
+    if constexpr (EM == 1) {
+        for (int q = threadIdx.x; q < 3 * nplanes; q += blockDim.x) {
+            const int c = q / nplanes, r = q - c * nplanes, kz = kb - 1 + r;
+            zt[c * ZT_ROW + r] = (kz >= 0 && kz < nz) ? __ldg(cf.tab + c * nz + kz) * cf.sig : T(0);
+        }
+        __syncthreads();
+    }
+}
+
 // issue the TMA loads of plane `kz` into stage buffer `dst` (state + coefficient maps)
 template <typename T, int EM, bool HA, typename G>
 __device__ __forceinline__ void issue_plane(T *dst, uint64_t *bar, const CUtensorMap *tm_state,
@@ -246,7 +267,8 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *stages = reinterpret_cast<T *>(smem_raw);
     T *ring = stages + S * SL::SZ;                       // [2][3][EY][EX] e' planes
-    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(ring + 2 * 3 * G::RP) + 15) & ~uintptr_t(15));
+    T *zt = ring + 2 * 3 * G::RP;                         // [3][ZT_ROW] z-table (EM == 1)
+    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(zt + ZtL<T, EM>::N) + 15) & ~uintptr_t(15));
     const int tid = threadIdx.x;
     constexpr int MAIN = BX * G::EY;                      // row-aligned phase-A points
     const bool hasA = tid < G::RP;
@@ -268,6 +290,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
         const int nplanes = ke - kb + 2;
+        stage_ztab<T, EM, HA>(zt, cf, kb, nplanes, D.nz);
         const int iA = x0 + ii, jA = y0 + jj;
         const bool inA = hasA && iA < D.nx && jA < D.ny;
         const bool lxA = inA && jA > 0, lyA = inA && iA > 0, lzA = inA && iA > 0 && jA > 0;
@@ -297,10 +320,10 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
             const T *P1 = stages + (L1 % S) * SL::SZ;
             T *R1 = ring + (kk & 1) * 3 * G::RP;
             const T *R0 = ring + (k & 1) * 3 * G::RP;
-            if (EM == 1 && kk < D.nz) {
-                bE0 = __ldg(cf.tab + kk) * cf.sig;
-                bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
-                bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
+            if (EM == 1) {
+                bE0 = zt[p + 1];
+                bE1 = zt[ZT_ROW + p + 1];
+                bE2 = zt[2 * ZT_ROW + p + 1];
             }
             if (p == 0 && hasA) {                         // h(kb-1) at the own point
                 hxk = P0[3 * G::PL + sA];
@@ -444,7 +467,8 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float *stages = reinterpret_cast<float *>(smem_raw);
     float *ring = stages + S * SL::SZ;                     // [2][3][RP]
-    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(ring + 2 * 3 * G::RP) + 15) & ~uintptr_t(15));
+    float *zt = ring + 2 * 3 * G::RP;                      // [3][ZT_ROW] z-table (EM == 1)
+    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(zt + ZtL<float, EM>::N) + 15) & ~uintptr_t(15));
     const int tid = threadIdx.x;
     const bool hasA = tid < G::NA;
     const bool pair = tid < G::MAIN;
@@ -469,6 +493,7 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
         const int x0 = (tile % sch.tiles_x) * G::BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
         const int nplanes = ke - kb + 2;
+        stage_ztab<float, EM, HA>(zt, cf, kb, nplanes, D.nz);
         const int ia = x0 + ii, jA = y0 + jj, ib = ia + 1;
         const bool rowA = hasA && jA < D.ny;
         const bool inA = rowA && ia < D.nx, inB = pair && rowA && ib < D.nx;
@@ -506,10 +531,10 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
             const float *P1 = stages + (L1 % S) * SL::SZ;
             float *R1 = ring + (kk & 1) * 3 * G::RP;
             const float *R0 = ring + (k & 1) * 3 * G::RP;
-            if (EM == 1 && kk < D.nz) {
-                bE0 = __ldg(cf.tab + kk) * cf.sig;
-                bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
-                bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
+            if (EM == 1) {
+                bE0 = zt[p + 1];
+                bE1 = zt[ZT_ROW + p + 1];
+                bE2 = zt[2 * ZT_ROW + p + 1];
             }
             if (p == 0 && hasA) {                           // h(kb-1) at the own points
                 if (pair) {
@@ -693,7 +718,8 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
     T *stages = reinterpret_cast<T *>(smem_raw);
     T *UE = stages + S * SL::SZ;                         // [NR][3][EY][EX]: u_e at (ii, jj)
     T *UH = UE + NR * 3 * G::RP;                         // [NR][3][EY][EX]: u_h at (ii-1, jj-1)
-    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(UH + NR * 3 * G::RP) + 15) & ~uintptr_t(15));
+    T *zt = UH + NR * 3 * G::RP;                         // [3][ZT_ROW] z-table (EM == 1)
+    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(zt + ZtL<T, EM>::N) + 15) & ~uintptr_t(15));
     const int tid = threadIdx.x;
     const bool hasA = tid < G::RP;
     // row-aligned phase-A mapping: warps cover whole 32-wide rows, the +1 halo column last
@@ -720,6 +746,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
         const int nplanes = ke - kb + 2;
+        stage_ztab<T, EM, HA>(zt, cf, kb, nplanes, D.nz);
         // phase-A validity (k-independent parts)
         const int iE = x0 + ii, jE = y0 + jj;             // u_e point
         const bool inE = hasA && iE < D.nx && jE < D.ny;
@@ -762,16 +789,12 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
             T *UH0 = UH + ((k + NR) % NR) * 3 * G::RP;    // u_h(k)
             T bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;         // coefficients at plane k (phase B)
             if (EM == 1) {
-                if (kk < D.nz) {
-                    bE0 = __ldg(cf.tab + kk) * cf.sig;
-                    bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
-                    bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
-                }
-                if (k >= 0) {
-                    bEk0 = __ldg(cf.tab + k) * cf.sig;
-                    bEk1 = __ldg(cf.tab + D.nz + k) * cf.sig;
-                    bEk2 = __ldg(cf.tab + 2 * D.nz + k) * cf.sig;
-                }
+                bE0 = zt[p + 1];
+                bE1 = zt[ZT_ROW + p + 1];
+                bE2 = zt[2 * ZT_ROW + p + 1];
+                bEk0 = zt[p];
+                bEk1 = zt[ZT_ROW + p];
+                bEk2 = zt[2 * ZT_ROW + p];
             }
             if (hasA) {
                 // u_e(k+1) = bE .* C^T w_h
@@ -977,7 +1000,8 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
     T *stages = reinterpret_cast<T *>(smem_raw);
     T *UE = stages + S * SL::SZ;                        // [2][3][RR]
     T *UH = UE + 2 * 3 * RR;                            // [3][RR]
-    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(UH + 3 * RR) + 15) & ~uintptr_t(15));
+    T *zt = UH + 3 * RR;                                  // [3][ZT_ROW] z-table (EM == 1)
+    uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(zt + ZtL<T, EM>::N) + 15) & ~uintptr_t(15));
     const int tid = threadIdx.x;
     const bool pair = tid < 32 * (BY + 1);
     const bool single = !pair && tid < 32 * (BY + 1) + (BY + 1);
@@ -1006,6 +1030,7 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
         const int x0 = (tile % sch.tiles_x) * G::BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
         const int nplanes = ke - kb + 2;
+        stage_ztab<T, EM, HA>(zt, cf, kb, nplanes, D.nz);
         // global coordinates and validity of the E / H points (a = left, b = right)
         const int iEa = x0 + xE, jE = y0 + yE, iHa = x0 + xH, jH = y0 + yH;
         const bool act = pair || single;
@@ -1045,16 +1070,12 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
             const T *UE0 = UE + (k & 1) * 3 * RR;
             T bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;
             if (EM == 1) {
-                if (kk < D.nz) {
-                    bE0 = __ldg(cf.tab + kk) * cf.sig;
-                    bE1 = __ldg(cf.tab + D.nz + kk) * cf.sig;
-                    bE2 = __ldg(cf.tab + 2 * D.nz + kk) * cf.sig;
-                }
-                if (k >= 0) {
-                    bEk0 = __ldg(cf.tab + k) * cf.sig;
-                    bEk1 = __ldg(cf.tab + D.nz + k) * cf.sig;
-                    bEk2 = __ldg(cf.tab + 2 * D.nz + k) * cf.sig;
-                }
+                bE0 = zt[p + 1];
+                bE1 = zt[ZT_ROW + p + 1];
+                bE2 = zt[2 * ZT_ROW + p + 1];
+                bEk0 = zt[p];
+                bEk1 = zt[ZT_ROW + p];
+                bEk2 = zt[2 * ZT_ROW + p];
             }
             if (p == 0 && act) {                            // w(kb-1) own values
                 if (pair) {
@@ -1348,7 +1369,7 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
     s.tiles_y = (g.ny + BY - 1) / BY;
     s.ntiles = s.tiles_x * s.tiles_y;
     double best = 1e300;
-    int bc = g.nz;
+    int bc = std::min(g.nz, ZT_ROW - 2);
     // L2 reuse: in the dynamic unit order a y-neighbour tile (tiles_x units later) starts
     // about tiles_x * chunk / resident planes later; keep that within ~4 planes so its halo
     // rows are still in L2 (measured at 768^3 fp64: chunk 48-64 beats the unconstrained 154
@@ -1362,6 +1383,7 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
         // 10.3 us vs chunk 8 12.3 us per leapfrog step, 32^3 chunk 1 6.2 vs 12.3 us)
         if (ch < std::min(g.nz, 8) && nch > 1 && units > resident) continue;
         if (ch > cap && ch > 8) continue;
+        if (ch > ZT_ROW - 2) continue;       // the staged z-table holds chunk + 2 planes
         const double waves = units / resident;
         const double eff_waves = std::ceil(waves);
         // cost ~ rounds * (chunk + 2 halo planes)
@@ -1371,7 +1393,7 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
             bc = ch;
         }
     }
-    if (const char *ev = getenv("PARAEXP_ZCHUNK")) bc = std::max(1, std::min(g.nz, atoi(ev)));
+    if (const char *ev = getenv("PARAEXP_ZCHUNK")) bc = std::max(1, std::min(std::min(g.nz, ZT_ROW - 2), atoi(ev)));
     s.chunk = bc;
     s.nchunks = (g.nz + bc - 1) / bc;
     s.units = s.ntiles * s.nchunks;
@@ -1426,7 +1448,7 @@ static int leapfrog_r_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int
                         const std::vector<SrcDev> &hsrc, const TraceDev *tr) {
     constexpr int BX = 32, BY = 8;
     using G = Geo<T, BX, BY>;
-    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 2 * 3 * G::RP) * sizeof(T) + 8 * S + 16;
+    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 2 * 3 * G::RP + ZtL<T, EM>::N) * sizeof(T) + 8 * S + 16;
     const Grid &g = *ka.g;
     auto kern = leapfrog_r_kernel<T, EM, HA, BX, BY, S, TR>;
     const int per_sm = resident_per_sm(kern, G::NTHR, smem);
@@ -1474,7 +1496,7 @@ static int leapfrog_v_V(const KernelArgs &ka, void *bufs[2], int64_t nsteps, int
                         const std::vector<SrcDev> &hsrc, const TraceDev *tr) {
     constexpr int BY = 8;
     using G = GeoV<BY>;
-    constexpr size_t smem = (size_t)(S * StageL<float, EM, HA, G>::SZ + 2 * 3 * G::RP) * sizeof(float) + 8 * S + 16;
+    constexpr size_t smem = (size_t)(S * StageL<float, EM, HA, G>::SZ + 2 * 3 * G::RP + ZtL<float, EM>::N) * sizeof(float) + 8 * S + 16;
     const Grid &g = *ka.g;
     auto kern = leapfrog_v_kernel<EM, HA, BY, S, TR>;
     const int per_sm = resident_per_sm(kern, G::NTHR, smem);
@@ -1540,7 +1562,7 @@ template <typename T, int EM, bool HA, int S>
 static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     constexpr int BX = 32, BY = 8;
     using G = Geo<T, BX, BY>;
-    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 2 * 2 * 3 * G::RP) * sizeof(T) + 8 * S + 16;
+    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 2 * 2 * 3 * G::RP + ZtL<T, EM>::N) * sizeof(T) + 8 * S + 16;
     const Grid &g = *ka.g;
     auto kern = pair_fused_kernel<T, EM, HA, BX, BY, S>;
     const int per_sm = resident_per_sm(kern, G::NTHR, smem);
@@ -1586,7 +1608,7 @@ template <typename T, int EM, bool HA, int BY, int S>
 static int poly_v_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     using G = GeoW<T, BY>;
     constexpr int RR = 68 * (BY + 1);
-    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 3 * 3 * RR) * sizeof(T) + 8 * S + 16;
+    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 3 * 3 * RR + ZtL<T, EM>::N) * sizeof(T) + 8 * S + 16;
     const Grid &g = *ka.g;
     auto kern = ka.et ? pair_v_kernel<T, EM, HA, BY, S, true> : pair_v_kernel<T, EM, HA, BY, S, false>;
     const int per_sm = resident_per_sm(pair_v_kernel<T, EM, HA, BY, S, true>, G::NTHR, smem);
