@@ -690,6 +690,30 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
     }
 }
 
+// K2 stage: the w box of StageL plus the y tile (6 x BY x BX, no halo) of the same plane, so
+// that the Newton sum y(k) arrives by TMA with w(k), S - 1 planes ahead of its use.  (Loaded
+// by the threads themselves, y(k) was on the critical path: ncu put 23% of K2's warp-stall
+// samples on the first use of y, and 28% on the barrier that waited for those warps.)
+template <typename T, int EM, bool HA, typename G>
+struct StageP {
+    static constexpr int YOFF = StageL<T, EM, HA, G>::SZ;
+    static constexpr int YT = 6 * G::BX * G::BY;             // multiple of 128 B for 32 x 8 tiles
+    static constexpr int SZ = YOFF + YT;
+};
+template <typename T, int EM, bool HA, typename G>
+__device__ __forceinline__ void issue_plane_y(T *dst, uint64_t *bar, const CUtensorMap *tm_state,
+                                              const CUtensorMap *tm_cE, const CUtensorMap *tm_cH,
+                                              const CUtensorMap *tm_y, int x0, int y0, int kz, bool with_y) {
+    using SL = StageL<T, EM, HA, G>;
+    constexpr uint32_t wbytes = (uint32_t)(NComp<T, EM, HA>::value * G::PL * sizeof(T));
+    constexpr uint32_t ybytes = (uint32_t)(StageP<T, EM, HA, G>::YT * sizeof(T));
+    mbar_expect_tx(bar, wbytes + (with_y ? ybytes : 0u));
+    tma_load_4d(dst, tm_state, bar, x0 - G::OX, y0 - 1, kz, 0);
+    if (EM == 2) tma_load_4d(dst + SL::ST, tm_cE, bar, x0 - G::OX, y0 - 1, kz, 0);
+    if (HA) tma_load_4d(dst + SL::ST + SL::CE, tm_cH, bar, x0 - G::OX, y0 - 1, kz, 0);
+    if (with_y) tma_load_4d(dst + StageP<T, EM, HA, G>::YOFF, tm_y, bar, x0, y0, kz, 0);
+}
+
 // ---------------------------------------------------------------------------------------
 // K2: fused Newton pair  u = X w ; y <- (init?0:y) + a w + b u ; [w' = X u + e2 w]
 // ---------------------------------------------------------------------------------------
@@ -700,8 +724,9 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
 template <typename T, int EM, bool HA, int BX, int BY, int S>
 __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) pair_fused_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
-    const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
-    T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
+    const __grid_constant__ CUtensorMap tm_cH, const __grid_constant__ CUtensorMap tm_y, Dev<T> D,
+    Coef<T, EM, HA> cf, T *__restrict__ wout, T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init,
+    int mode, EtDev et) {
     pdl_sync();
     using G = Geo<T, BX, BY>;
     if (et.norms && et_skip(et)) {                        // early termination (f2)
@@ -712,13 +737,14 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
         return;
     }
     double dacc = 0.0, yacc = 0.0;                        // ||delta y||^2, ||y||^2 (energy norm)
+    using SP = StageP<T, EM, HA, G>;
     using SL = StageL<T, EM, HA, G>;
     constexpr int NR = 2;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *stages = reinterpret_cast<T *>(smem_raw);
-    T *UE = stages + S * SL::SZ;                         // [NR][3][EY][EX]: u_e at (ii, jj)
-    T *UH = UE + NR * 3 * G::RP;                         // [NR][3][EY][EX]: u_h at (ii-1, jj-1)
-    T *zt = UH + NR * 3 * G::RP;                         // [3][ZT_ROW] z-table (EM == 1)
+    T *UE = stages + S * SP::SZ;                         // [NR][3][EY][EX]: u_e at (ii, jj)
+    T *UH = UE + NR * 3 * G::RP;                         // [3][EY][EX]: u_h(k) at (ii-1, jj-1), one plane
+    T *zt = UH + 3 * G::RP;                              // [3][ZT_ROW] z-table (EM == 1)
     uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(zt + ZtL<T, EM>::N) + 15) & ~uintptr_t(15));
     const int tid = threadIdx.x;
     const bool hasA = tid < G::RP;
@@ -760,33 +786,24 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
         const bool lxBe = jB > 0, lyBe = iB > 0, lzBe = iB > 0 && jB > 0;
         const bool lxBh = iB > 0, lyBh = jB > 0;
         const int64_t gB = D.idx(inB ? iB : 0, inB ? jB : 0, 0);
+        // own-point u_h(k-1) (x, y) carried from the previous plane (the u_h ring holds one plane)
+        T hxm = T(0), hym = T(0);
         if (tid == 0)
             for (int p = 0; p < min(S, nplanes); ++p) {
-                const uint32_t L = lcount + p;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                          &tm_cH, x0, y0, kb - 1 + p);
+                const uint32_t L = lcount + p, kz = kb - 1 + p;
+                issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
+                                            &tm_y, x0, y0, kz, !init && kz >= kb && kz < ke);
             }
         for (int p = 0; p + 1 < nplanes; ++p) {
             const int k = kb - 1 + p, kk = k + 1;
             const uint32_t L0 = lcount + p, L1 = L0 + 1;
             const bool doB = k >= kb && inB;
-            // prefetch y(k) for the own point (consumed after the halo phase)
-            T yv0 = T(0), yv1 = T(0), yv2 = T(0), yv3 = T(0), yv4 = T(0), yv5 = T(0);
-            if (doB && !init) {
-                const T *yp = y + gB + (int64_t)k * D.plane;
-                yv0 = yp[0];
-                yv1 = yp[D.cs];
-                yv2 = yp[2 * D.cs];
-                yv3 = yp[3 * D.cs];
-                yv4 = yp[4 * D.cs];
-                yv5 = yp[5 * D.cs];
-            }
             if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
             mbar_wait(&bars[L1 % S], (L1 / S) & 1);
-            const T *P0 = stages + (L0 % S) * SL::SZ;    // w plane k
-            const T *P1 = stages + (L1 % S) * SL::SZ;    // w plane k+1
+            const T *P0 = stages + (L0 % S) * SP::SZ;    // w plane k (+ y(k))
+            const T *P1 = stages + (L1 % S) * SP::SZ;    // w plane k+1
             T *UE1 = UE + (kk % NR) * 3 * G::RP;           // u_e(k+1)
-            T *UH0 = UH + ((k + NR) % NR) * 3 * G::RP;    // u_h(k)
+            T *UH0 = UH;                                   // u_h(k)
             T bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;         // coefficients at plane k (phase B)
             if (EM == 1) {
                 bE0 = zt[p + 1];
@@ -838,11 +855,26 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
                 }
             }
             __syncthreads();
+            T hx0 = T(0), hy0 = T(0);
+            if (hasB) {                                          // own u_h(k) (x, y)
+                hx0 = UH0[rh];
+                hy0 = UH0[G::RP + rh];
+            }
             if (doB) {
                 const T *UE0 = UE + (k % NR) * 3 * G::RP;        // u_e(k)
-                const T *UHm = UH + ((k - 1 + NR) % NR) * 3 * G::RP; // u_h(k-1)
                 const T ux0 = UE0[re], uy0 = UE0[G::RP + re], uz0 = UE0[2 * G::RP + re];
-                const T hx0 = UH0[rh], hy0 = UH0[G::RP + rh], hz0 = UH0[2 * G::RP + rh];
+                const T hz0 = UH0[2 * G::RP + rh];
+                // y(k) at the own point, staged with w(k) by TMA (0 for the first op, init)
+                const T *YS = P0 + SP::YOFF;
+                T yv0 = T(0), yv1 = T(0), yv2 = T(0), yv3 = T(0), yv4 = T(0), yv5 = T(0);
+                if (!init) {
+                    yv0 = YS[tid];
+                    yv1 = YS[G::NT + tid];
+                    yv2 = YS[2 * G::NT + tid];
+                    yv3 = YS[3 * G::NT + tid];
+                    yv4 = YS[4 * G::NT + tid];
+                    yv5 = YS[5 * G::NT + tid];
+                }
                 const T w0 = P0[sB], w1 = P0[G::PL + sB], w2 = P0[2 * G::PL + sB];
                 const T w3 = P0[3 * G::PL + sB], w4 = P0[4 * G::PL + sB], w5 = P0[5 * G::PL + sB];
                 const int64_t go = gB + (int64_t)k * D.plane;
@@ -858,7 +890,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
                     // w'_e(k) = bE C^T u_h + e2 w_e
                     const T hz_jm = UH0[2 * G::RP + rh - G::EX], hx_jm = UH0[rh - G::EX];
                     const T hz_im = UH0[2 * G::RP + rh - 1], hy_im = UH0[G::RP + rh - 1];
-                    const T hy_km = UHm[G::RP + rh], hx_km = UHm[rh];
+                    const T hy_km = hym, hx_km = hxm;
                     const T d0 = ((hz0 - hz_jm) - hy0) + hy_km;
                     const T d1 = ((hx0 - hx_km) - hz0) + hz_im;
                     const T d2 = ((hy0 - hy_im) - hx0) + hx_jm;
@@ -932,11 +964,13 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
                 yo[4 * D.cs] = y4;
                 yo[5 * D.cs] = y5;
             }
+            hxm = hx0;
+            hym = hy0;
             __syncthreads();
             if (tid == 0 && p + S < nplanes) {
-                const uint32_t L = lcount + p + S;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                          &tm_cH, x0, y0, kb - 1 + p + S);
+                const uint32_t L = lcount + p + S, kz = kb - 1 + p + S;
+                issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
+                                            &tm_y, x0, y0, kz, !init && kz >= kb && kz < ke);
             }
         }
         lcount += nplanes;
@@ -1562,7 +1596,7 @@ template <typename T, int EM, bool HA, int S>
 static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     constexpr int BX = 32, BY = 8;
     using G = Geo<T, BX, BY>;
-    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 2 * 2 * 3 * G::RP + ZtL<T, EM>::N) * sizeof(T) + 8 * S + 16;
+    constexpr size_t smem = (size_t)(S * StageP<T, EM, HA, G>::SZ + 3 * 3 * G::RP + ZtL<T, EM>::N) * sizeof(T) + 8 * S + 16;
     const Grid &g = *ka.g;
     auto kern = pair_fused_kernel<T, EM, HA, BX, BY, S>;
     const int per_sm = resident_per_sm(kern, G::NTHR, smem);
@@ -1577,9 +1611,10 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     if (HA && (rc = make_map<T>(&tmH, g, g.d_cH_arr, 3, G::WX, G::HY))) return rc;
     cudaStream_t s = (cudaStream_t)ka.stream;
     T *w = (T *)bufs[0], *yy = (T *)bufs[1], *sp = (T *)bufs[2], *sp2 = (T *)bufs[3];
-    CUtensorMap tmW, tmS;   // maps of the two ping-pong w buffers
+    CUtensorMap tmW, tmS, tmY;   // maps of the two ping-pong w buffers and of y (tile box)
     if ((rc = make_map<T>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
     if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
+    if ((rc = make_map<T>(&tmY, g, yy, 6, BX, BY))) return rc;
     int init = 1;
     EtDev et;
     if (ka.et) et = *ka.et;
@@ -1587,8 +1622,8 @@ static int poly_fused_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     for (const Op &op : plan.ops) {
         et.op = opi++;
         et.apps = op.kind == 1 ? 1 : 2;
-        launch_k(kern, grid, G::NTHR, smem, s, tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), T(op.a),
-                 T(op.b), T(op.e2), T(op.c), init, op.kind, et);
+        launch_k(kern, grid, G::NTHR, smem, s, tmW, tmE, tmH, tmY, D, cf, sp, yy, launch_sched(g, sch, grid),
+                 T(op.a), T(op.b), T(op.e2), T(op.c), init, op.kind, et);
         ++*ka.launches;
         if (op.kind == 0) {
             std::swap(w, sp);
