@@ -694,10 +694,14 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
 // that the Newton sum y(k) arrives by TMA with w(k), S - 1 planes ahead of its use.  (Loaded
 // by the threads themselves, y(k) was on the critical path: ncu put 23% of K2's warp-stall
 // samples on the first use of y, and 28% on the barrier that waited for those warps.)
+// Only for the scalar / z-table materials: with per-edge coefficient boxes in the stage as well
+// (EM == 2, HA) the y tile would cost the second resident CTA per SM, so there the threads keep
+// loading y(k) themselves at the top of the plane iteration.
 template <typename T, int EM, bool HA, typename G>
 struct StageP {
+    static constexpr bool Y = EM != 2 && !HA;               // y staged by TMA
     static constexpr int YOFF = StageL<T, EM, HA, G>::SZ;
-    static constexpr int YT = 6 * G::BX * G::BY;             // multiple of 128 B for 32 x 8 tiles
+    static constexpr int YT = Y ? 6 * G::BX * G::BY : 0;    // multiple of 128 B for 32 x 8 / 64 x 8 tiles
     static constexpr int SZ = YOFF + YT;
 };
 template <typename T, int EM, bool HA, typename G>
@@ -707,11 +711,11 @@ __device__ __forceinline__ void issue_plane_y(T *dst, uint64_t *bar, const CUten
     using SL = StageL<T, EM, HA, G>;
     constexpr uint32_t wbytes = (uint32_t)(NComp<T, EM, HA>::value * G::PL * sizeof(T));
     constexpr uint32_t ybytes = (uint32_t)(StageP<T, EM, HA, G>::YT * sizeof(T));
-    mbar_expect_tx(bar, wbytes + (with_y ? ybytes : 0u));
+    mbar_expect_tx(bar, wbytes + ((StageP<T, EM, HA, G>::Y && with_y) ? ybytes : 0u));
     tma_load_4d(dst, tm_state, bar, x0 - G::OX, y0 - 1, kz, 0);
     if (EM == 2) tma_load_4d(dst + SL::ST, tm_cE, bar, x0 - G::OX, y0 - 1, kz, 0);
     if (HA) tma_load_4d(dst + SL::ST + SL::CE, tm_cH, bar, x0 - G::OX, y0 - 1, kz, 0);
-    if (with_y) tma_load_4d(dst + StageP<T, EM, HA, G>::YOFF, tm_y, bar, x0, y0, kz, 0);
+    if (StageP<T, EM, HA, G>::Y && with_y) tma_load_4d(dst + StageP<T, EM, HA, G>::YOFF, tm_y, bar, x0, y0, kz, 0);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -798,6 +802,17 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
             const int k = kb - 1 + p, kk = k + 1;
             const uint32_t L0 = lcount + p, L1 = L0 + 1;
             const bool doB = k >= kb && inB;
+            // y(k) of the own point: staged by TMA (SP::Y), else loaded here, consumed in phase B
+            T yv0 = T(0), yv1 = T(0), yv2 = T(0), yv3 = T(0), yv4 = T(0), yv5 = T(0);
+            if (!SP::Y && doB && !init) {
+                const T *yp = y + gB + (int64_t)k * D.plane;
+                yv0 = yp[0];
+                yv1 = yp[D.cs];
+                yv2 = yp[2 * D.cs];
+                yv3 = yp[3 * D.cs];
+                yv4 = yp[4 * D.cs];
+                yv5 = yp[5 * D.cs];
+            }
             if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
             mbar_wait(&bars[L1 % S], (L1 / S) & 1);
             const T *P0 = stages + (L0 % S) * SP::SZ;    // w plane k (+ y(k))
@@ -864,10 +879,8 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
                 const T *UE0 = UE + (k % NR) * 3 * G::RP;        // u_e(k)
                 const T ux0 = UE0[re], uy0 = UE0[G::RP + re], uz0 = UE0[2 * G::RP + re];
                 const T hz0 = UH0[2 * G::RP + rh];
-                // y(k) at the own point, staged with w(k) by TMA (0 for the first op, init)
-                const T *YS = P0 + SP::YOFF;
-                T yv0 = T(0), yv1 = T(0), yv2 = T(0), yv3 = T(0), yv4 = T(0), yv5 = T(0);
-                if (!init) {
+                if (SP::Y && !init) {      // y(k) at the own point, staged with w(k) by TMA
+                    const T *YS = P0 + SP::YOFF;
                     yv0 = YS[tid];
                     yv1 = YS[G::NT + tid];
                     yv2 = YS[2 * G::NT + tid];
@@ -995,15 +1008,15 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
 // y0..y0+BY), u_h 1 plane (rows y0-1..y0+BY-1, stored at row + 1).  Phase B reads only the
 // j+1 / i+2 neighbours of u_e(k) and the j-1 / i-1 neighbours of u_h(k).
 // geometry of the two-points-per-thread pair kernel for T = float / double (64 x BY tiles)
-template <typename T, int BY>
+template <typename T, int BY_>
 struct GeoW {
-    static constexpr int BX = 64;
+    static constexpr int BX = 64, BY = BY_;
     static constexpr int VEC = 16 / (int)sizeof(T);
     static constexpr int OX = VEC;                          // TMA x start x0 - OX (16 B aligned)
     static constexpr int WX = ((OX + BX + 1 + VEC - 1) / VEC) * VEC;   // covers x0-1 .. x0+64
-    static constexpr int HY = BY + 2;
+    static constexpr int HY = BY_ + 2;
     static constexpr int PL = WX * HY;
-    static constexpr int NTHR = ((32 * (BY + 1) + (BY + 1) + 31) / 32) * 32;
+    static constexpr int NTHR = ((32 * (BY_ + 1) + (BY_ + 1) + 31) / 32) * 32;
 };
 template <typename T> struct Vec2;
 template <> struct Vec2<float> {
@@ -1018,12 +1031,14 @@ template <> struct Vec2<double> {
 template <typename T, int EM, bool HA, int BY, int S, bool ET>
 __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pair_v_kernel(
     const __grid_constant__ CUtensorMap tm_state, const __grid_constant__ CUtensorMap tm_cE,
-    const __grid_constant__ CUtensorMap tm_cH, Dev<T> D, Coef<T, EM, HA> cf, T *__restrict__ wout,
-    T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init, int mode, EtDev et) {
+    const __grid_constant__ CUtensorMap tm_cH, const __grid_constant__ CUtensorMap tm_y, Dev<T> D,
+    Coef<T, EM, HA> cf, T *__restrict__ wout, T *__restrict__ y, Sched sch, T a, T b, T e2, T cl, int init,
+    int mode, EtDev et) {
     pdl_sync();
     using G = GeoW<T, BY>;
     using V2 = typename Vec2<T>::type;
     using SL = StageL<T, EM, HA, G>;
+    using SP = StageP<T, EM, HA, G>;                        // + the y tile of the plane (TMA)
     constexpr int RX = 68, RR = RX * (BY + 1);              // ring row pitch, ring plane
     if (ET && et.norms && et_skip(et)) {                          // early termination (f2)
         if (sch.ctr && blockIdx.x == 0 && threadIdx.x == 0)
@@ -1032,7 +1047,7 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
     }
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *stages = reinterpret_cast<T *>(smem_raw);
-    T *UE = stages + S * SL::SZ;                        // [2][3][RR]
+    T *UE = stages + S * SP::SZ;                        // [2][3][RR]
     T *UH = UE + 2 * 3 * RR;                            // [3][RR]
     T *zt = UH + 3 * RR;                                  // [3][ZT_ROW] z-table (EM == 1)
     uint64_t *bars = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(zt + ZtL<T, EM>::N) + 15) & ~uintptr_t(15));
@@ -1080,26 +1095,26 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
         T uma0 = T(0), umb0 = T(0), uma1 = T(0), umb1 = T(0), uma2 = T(0), umb2 = T(0);   // u_h(k-1)
         if (tid == 0)
             for (int p = 0; p < min(S, nplanes); ++p) {
-                const uint32_t L = lcount + p;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                              &tm_cH, x0, y0, kb - 1 + p);
+                const uint32_t L = lcount + p, kz = kb - 1 + p;
+                issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
+                                            &tm_y, x0, y0, kz, !init && kz >= kb && kz < ke);
             }
         for (int p = 0; p + 1 < nplanes; ++p) {
             const int k = kb - 1 + p, kk = k + 1;
             const uint32_t L0 = lcount + p, L1 = L0 + 1;
             const bool doB = doT && k >= kb;
-            V2 yv[6];
+            V2 yv[6];                                   // y(k) of the own pair
 #pragma unroll
             for (int c = 0; c < 6; ++c) yv[c] = Vec2<T>::make(T(0), T(0));
-            if (doB && !init) {
+            if (!SP::Y && doB && !init) {               // else staged with w(k) by TMA
                 const T *yp = y + gB + (int64_t)k * D.plane;
 #pragma unroll
                 for (int c = 0; c < 6; ++c) yv[c] = ld2(yp + c * D.cs);
             }
             if (p == 0) mbar_wait(&bars[L0 % S], (L0 / S) & 1);
             mbar_wait(&bars[L1 % S], (L1 / S) & 1);
-            const T *P0 = stages + (L0 % S) * SL::SZ;   // plane k
-            const T *P1 = stages + (L1 % S) * SL::SZ;   // plane k+1
+            const T *P0 = stages + (L0 % S) * SP::SZ;   // plane k (+ y(k))
+            const T *P1 = stages + (L1 % S) * SP::SZ;   // plane k+1
             T *UE1 = UE + (kk & 1) * 3 * RR;
             const T *UE0 = UE + (k & 1) * 3 * RR;
             T bEk0 = bE0, bEk1 = bE1, bEk2 = bE2;
@@ -1234,6 +1249,10 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
             // ---- phase B: w'(k), y(k) on the own tile pair ----
             if (doB) {
                 const bool inB = inEb;                      // right point inside the grid
+                if (SP::Y && !init) {                       // y(k), staged with w(k) by TMA
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) yv[c] = ld2(P0 + SP::YOFF + c * (G::BX * BY) + yE * G::BX + xE);
+                }
                 T wn[12];
 #pragma unroll
                 for (int c = 0; c < 12; ++c) wn[c] = T(0);
@@ -1323,9 +1342,9 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
             uma0 = va0; umb0 = vb0; uma1 = va1; umb1 = vb1; uma2 = va2; umb2 = vb2;
             __syncthreads();
             if (tid == 0 && p + S < nplanes) {
-                const uint32_t L = lcount + p + S;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                              &tm_cH, x0, y0, kb - 1 + p + S);
+                const uint32_t L = lcount + p + S, kz = kb - 1 + p + S;
+                issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
+                                            &tm_y, x0, y0, kz, !init && kz >= kb && kz < ke);
             }
         }
         lcount += nplanes;
@@ -1643,7 +1662,7 @@ template <typename T, int EM, bool HA, int BY, int S>
 static int poly_v_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     using G = GeoW<T, BY>;
     constexpr int RR = 68 * (BY + 1);
-    constexpr size_t smem = (size_t)(S * StageL<T, EM, HA, G>::SZ + 3 * 3 * RR + ZtL<T, EM>::N) * sizeof(T) + 8 * S + 16;
+    constexpr size_t smem = (size_t)(S * StageP<T, EM, HA, G>::SZ + 3 * 3 * RR + ZtL<T, EM>::N) * sizeof(T) + 8 * S + 16;
     const Grid &g = *ka.g;
     auto kern = ka.et ? pair_v_kernel<T, EM, HA, BY, S, true> : pair_v_kernel<T, EM, HA, BY, S, false>;
     const int per_sm = resident_per_sm(pair_v_kernel<T, EM, HA, BY, S, true>, G::NTHR, smem);
@@ -1660,9 +1679,10 @@ static int poly_v_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     if (HA && (rc = make_map<T>(&tmH, g, g.d_cH_arr, 3, G::WX, G::HY))) return rc;
     cudaStream_t s = (cudaStream_t)ka.stream;
     T *w = (T *)bufs[0], *yy = (T *)bufs[1], *sp = (T *)bufs[2], *sp2 = (T *)bufs[3];
-    CUtensorMap tmW, tmS;
+    CUtensorMap tmW, tmS, tmY;
     if ((rc = make_map<T>(&tmW, g, w, 6, G::WX, G::HY))) return rc;
     if ((rc = make_map<T>(&tmS, g, sp, 6, G::WX, G::HY))) return rc;
+    if ((rc = make_map<T>(&tmY, g, yy, 6, G::BX, BY))) return rc;
     int init = 1;
     EtDev et;
     if (ka.et) et = *ka.et;
@@ -1670,7 +1690,7 @@ static int poly_v_V(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
     for (const Op &op : plan.ops) {
         et.op = opi++;
         et.apps = op.kind == 1 ? 1 : 2;
-        launch_k(kern, grid, G::NTHR, smem, s, tmW, tmE, tmH, D, cf, sp, yy, launch_sched(g, sch, grid), (T)op.a,
+        launch_k(kern, grid, G::NTHR, smem, s, tmW, tmE, tmH, tmY, D, cf, sp, yy, launch_sched(g, sch, grid), (T)op.a,
                                           (T)op.b, (T)op.e2, (T)op.c, init, op.kind, et);
         ++*ka.launches;
         if (op.kind == 0) {
