@@ -232,6 +232,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-serial", action="store_true")
     ap.add_argument("--p", type=int, default=0, help="override the workload's sub-interval count")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e pass (secondary lines)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -323,39 +324,43 @@ def main():
         ms, cu, launches = ms_local, float(cu_local), launches_local
     value = cu / (ms * 1e-3)
 
-    # ---- e2e: the same C-ABI call with HOST buffers (pinned): the library copies u0 in and
-    # (e_out, h_out) out inside the call, inside the timed region ----
-    e_host = torch.empty(3 * grid.npts, dtype=tdt, pin_memory=True)
-    h_host = torch.empty_like(e_host)
-    u0_host = None
-    if u0 is not None:
-        u0_host = (u0[0].cpu().pin_memory(), u0[1].cpu().pin_memory())
-    barrier()
-    torch.cuda.synchronize()
-    e2e0 = torch.cuda.Event(enable_timing=True)
-    e2e1 = torch.cuda.Event(enable_timing=True)
-    e2e0.record(stream)
-    cu_e2e = 0
-    h2d = d2h = 0
-    q_bytes = w.nsteps * len(w.sources) * (8 if w.dtype == "f64" else 4)
-    for _ in range(args.steps):
-        if u0_host is not None:
-            h2d += 2 * u0_host[0].numel() * u0_host[0].element_size()
-        st = pe.solve(grid, w.nsteps, w.p, u0=u0_host, e_out=e_host, h_out=h_host, **kw)
-        h2d += q_bytes           # the library uploads the source amplitude table every call
-        cu_e2e += st["cell_updates"]
-        if rank == st["root"]:
-            d2h += 2 * e_host.numel() * e_host.element_size()
-    e2e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    ms_e2e = e2e0.elapsed_time(e2e1)
-    if world > 1:
-        t = torch.tensor([ms_e2e, cu_e2e, h2d, d2h], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
-        s2 = t[1:].clone()
-        dist.all_reduce(s2)
-        ms_e2e, cu_e2e, h2d, d2h = float(t[0]), float(s2[0]), float(s2[1]), float(s2[2])
+    e2e_out = None
+    if not args.no_e2e:
+        # ---- e2e: the same C-ABI call with HOST buffers (pinned): the library copies u0 in and
+        # (e_out, h_out) out inside the call, inside the timed region ----
+        e_host = torch.empty(3 * grid.npts, dtype=tdt, pin_memory=True)
+        h_host = torch.empty_like(e_host)
+        u0_host = None
+        if u0 is not None:
+            u0_host = (u0[0].cpu().pin_memory(), u0[1].cpu().pin_memory())
+        barrier()
+        torch.cuda.synchronize()
+        e2e0 = torch.cuda.Event(enable_timing=True)
+        e2e1 = torch.cuda.Event(enable_timing=True)
+        e2e0.record(stream)
+        cu_e2e = 0
+        h2d = d2h = 0
+        q_bytes = w.nsteps * len(w.sources) * (8 if w.dtype == "f64" else 4)
+        for _ in range(args.steps):
+            if u0_host is not None:
+                h2d += 2 * u0_host[0].numel() * u0_host[0].element_size()
+            st = pe.solve(grid, w.nsteps, w.p, u0=u0_host, e_out=e_host, h_out=h_host, **kw)
+            h2d += q_bytes           # the library uploads the source amplitude table every call
+            cu_e2e += st["cell_updates"]
+            if rank == st["root"]:
+                d2h += 2 * e_host.numel() * e_host.element_size()
+        e2e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_e2e = e2e0.elapsed_time(e2e1)
+        if world > 1:
+            t = torch.tensor([ms_e2e, cu_e2e, h2d, d2h], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+            s2 = t[1:].clone()
+            dist.all_reduce(s2)
+            ms_e2e, cu_e2e, h2d, d2h = float(t[0]), float(s2[0]), float(s2[1]), float(s2[2])
+        e2e_out = {"value": cu_e2e / (ms_e2e * 1e-3), "unit": "cell-updates/s",
+                   "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)}
 
     # ---- serial leapfrog over the same interval on 1 GPU (speedup denominator) ----
     serial_ms = None
@@ -425,8 +430,7 @@ def main():
                     "leapfrog_steps_per_solve": stats[-1]["leapfrog_steps"],
                     "a_applications_per_solve": stats[-1]["a_applications"]},
         "roofline": roofline,
-        "e2e": {"value": cu_e2e / (ms_e2e * 1e-3), "unit": "cell-updates/s",
-                "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)},
+        "e2e": e2e_out,
         "gpu_launches": launches,
         "clocks": clocks,
     }
