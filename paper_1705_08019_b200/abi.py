@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libparaexp.so")
+# PARAEXP_LIBRARY_VARIANT=debug loads the bounds-checked build (build.py --debug)
+LIB_PATH = os.path.join(_HERE, "libparaexp_debug.so" if os.environ.get("PARAEXP_LIBRARY_VARIANT") == "debug"
+                        else "libparaexp.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"paraexp: {LIB_PATH} not built -- run `python -m paper_1705_08019_b200.build` "

@@ -47,7 +47,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
     const uint32_t a = smem_u32(bar);
+#ifdef PARAEXP_DEBUG_CHECKS
+    uint64_t spins = 0;
+#endif
     while (!done) {
+#ifdef PARAEXP_DEBUG_CHECKS
+        PE_CHECK(++spins < (1ull << 28), "mbarrier wait never completed (TMA byte count / phase)");
+#endif
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -141,6 +147,16 @@ __device__ __forceinline__ int grab_unit(const Sched &sch, int prev) {
     }
     __syncthreads();
     return s_unit;
+}
+
+// Lookahead grab of the NEXT unit by thread 0 alone (no barrier), used by the kernels that
+// prefetch the next unit's first planes while the current unit drains (cross-unit pipelining):
+// the same counter as grab_unit (each CTA still ends with exactly one failing grab) or the
+// static stride.
+__device__ __forceinline__ int grab_next_t0(const Sched &sch, int cur) {
+    if (!sch.ctr) return cur + (int)gridDim.x;
+    const long long d = (long long)(atomicAdd(sch.ctr, 1ull) - sch.base);
+    return (d < 0 || d > 0x7fffffffLL) ? 0x7fffffff : (int)d;
 }
 
 struct SrcList {
@@ -285,11 +301,19 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
     __syncthreads();
     uint32_t lcount = 0;
     double eacc = 0.0;
-    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
+    // cross-unit pipelining (as in K2): thread 0 issues the next unit's first planes into the
+    // stage slots the draining unit frees
+    __shared__ int s_next;
+    int pre = 0;
+    int unit = grab_unit(sch, -1);
+    while (unit < sch.units) {
         const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
         const int nplanes = ke - kb + 2;
+        const int pre_cur = pre;
+        pre = 0;
+        int nxt = 0x7fffffff, nx0 = 0, ny0 = 0, nkb = 0, nke = 0;
         stage_ztab<T, EM, HA>(zt, cf, kb, nplanes, D.nz);
         const int iA = x0 + ii, jA = y0 + jj;
         const bool inA = hasA && iA < D.nx && jA < D.ny;
@@ -306,7 +330,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
         T hxk = T(0), hyk = T(0), hzk = T(0), ek0 = T(0), ek1 = T(0), ek2 = T(0);
         T g0 = bH0, g1 = bH1, g2 = bH2;                    // cH at the own point, plane k (HA)
         if (tid == 0)
-            for (int p = 0; p < min(S, nplanes); ++p) {
+            for (int p = pre_cur; p < min(S, nplanes); ++p) {
                 const uint32_t L = lcount + p;
                 issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
                                           &tm_cH, x0, y0, kb - 1 + p);
@@ -360,11 +384,13 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
                             if (sc == 1) e1 = e1 - qv;
                             if (sc == 2) e2 = e2 - qv;
                         }
+                PE_CHECK(rA >= 0 && rA < G::RP && sA >= G::WX && sA + 1 < G::PL, "K1r ring / stage index");
                 R1[rA] = e0;
                 R1[G::RP + rA] = e1;
                 R1[2 * G::RP + rA] = e2;
                 if (wrA && vk && kk >= kb && kk < ke) {
                     T *o = oA + (int64_t)kk * D.plane;
+                    PE_CHECK(D.in_state((o - out) + 2 * D.cs), "K1r e store");
                     o[0] = e0;
                     o[D.cs] = e1;
                     o[2 * D.cs] = e2;
@@ -398,6 +424,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
                 const T n1 = lyB ? hyk - g1 * c1 : hyk;
                 const T n2 = k > 0 ? hzk - g2 * c2 : hzk;
                 T *o = oA + (int64_t)k * D.plane + 3 * D.cs;
+                PE_CHECK(D.in_state((o - out) + 2 * D.cs) && iA < D.nx, "K1r h store");
                 o[0] = n0;
                 o[D.cs] = n1;
                 o[2 * D.cs] = n2;
@@ -415,13 +442,37 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
             ek1 = e1;
             ek2 = e2;
             __syncthreads();
-            if (tid == 0 && p + S < nplanes) {
+            if (tid == 0) {
                 const uint32_t L = lcount + p + S;
-                issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                          &tm_cH, x0, y0, kb - 1 + p + S);
+                if (p + S < nplanes) {
+                    const int kz = kb - 1 + p + S;
+                    issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
+                                                x0, y0, kz);
+                } else {
+                    if (p + S == nplanes) {                   // the slots start to free: next unit
+                        nxt = grab_next_t0(sch, unit);
+                        s_next = nxt;
+                        if (nxt < sch.units) {
+                            const int nt = nxt % sch.ntiles, nc = nxt / sch.ntiles;
+                            nx0 = (nt % sch.tiles_x) * BX;
+                            ny0 = (nt / sch.tiles_x) * BY;
+                            nkb = nc * sch.chunk;
+                            nke = min(nkb + sch.chunk, D.nz);
+                        }
+                    }
+                    const int q = p + S - nplanes;            // plane q of the next unit
+                    if (nxt < sch.units && q < nke - nkb + 2) {
+                        const int kz = nkb - 1 + q;
+                        issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
+                                                    nx0, ny0, kz);
+                        pre = q + 1;
+                    }
+                }
             }
         }
         lcount += nplanes;
+        if (S == 2) __syncthreads();                          // s_next written in the last iteration
+        unit = s_next;
     }
     if (TR && tr.energy) {
         const double sum = block_sum(eacc);
@@ -488,11 +539,19 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
     auto st2 = [](float *p, float a, float b) { *reinterpret_cast<float2 *>(p) = make_float2(a, b); };
     uint32_t lcount = 0;
     double eacc = 0.0;
-    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
+    // cross-unit pipelining (as in K2): thread 0 issues the next unit's first planes into the
+    // stage slots the draining unit frees
+    __shared__ int s_next;
+    int pre = 0;
+    int unit = grab_unit(sch, -1);
+    while (unit < sch.units) {
         const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
         const int x0 = (tile % sch.tiles_x) * G::BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
         const int nplanes = ke - kb + 2;
+        const int pre_cur = pre;
+        pre = 0;
+        int nxt = 0x7fffffff, nx0 = 0, ny0 = 0, nkb = 0, nke = 0;
         stage_ztab<float, EM, HA>(zt, cf, kb, nplanes, D.nz);
         const int ia = x0 + ii, jA = y0 + jj, ib = ia + 1;
         const bool rowA = hasA && jA < D.ny;
@@ -517,7 +576,7 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
         float ea0 = 0.f, eb0 = 0.f, ea1 = 0.f, eb1 = 0.f, ea2 = 0.f, eb2 = 0.f;
         float g0a = bH0, g1a = bH1, g2a = bH2, g0b = bH0, g1b = bH1, g2b = bH2;
         if (tid == 0)
-            for (int p = 0; p < min(S, nplanes); ++p) {
+            for (int p = pre_cur; p < min(S, nplanes); ++p) {
                 const uint32_t L = lcount + p;
                 issue_plane<float, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
                                               &tm_cH, x0, y0, kb - 1 + p);
@@ -616,6 +675,7 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
                 }
                 if (wrA && vk && kk >= kb && kk < ke) {
                     float *o = oA + (int64_t)kk * D.plane;
+                    PE_CHECK(D.in_state((o - out) + 2 * D.cs + 1) && ((o - out) & 1) == 0, "K1v e store");
                     st2(o, na0, nb0);                     // b beyond nx lands in the zero x-padding
                     st2(o + D.cs, na1, nb1);
                     st2(o + 2 * D.cs, na2, nb2);
@@ -659,6 +719,7 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
                 const float nya = lyA2 ? hya - g1a * c1a : hya, nyb = lyA2 ? hyb - g1b * c1b : hyb;
                 const float nza = kp ? hza - g2a * c2a : hza, nzb = kp ? hzb - g2b * c2b : hzb;
                 float *o = oA + (int64_t)k * D.plane + 3 * D.cs;
+                PE_CHECK(D.in_state((o - out) + 2 * D.cs + 1), "K1v h store");
                 st2(o, nxa, inB ? nxb : 0.f);
                 st2(o + D.cs, nya, inB ? nyb : 0.f);
                 st2(o + 2 * D.cs, nza, inB ? nzb : 0.f);
@@ -676,13 +737,37 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
             hxa = h1xa; hxb = h1xb; hya = h1ya; hyb = h1yb; hza = h1za; hzb = h1zb;
             ea0 = na0; eb0 = nb0; ea1 = na1; eb1 = nb1; ea2 = na2; eb2 = nb2;
             __syncthreads();
-            if (tid == 0 && p + S < nplanes) {
+            if (tid == 0) {
                 const uint32_t L = lcount + p + S;
-                issue_plane<float, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE,
-                                              &tm_cH, x0, y0, kb - 1 + p + S);
+                if (p + S < nplanes) {
+                    const int kz = kb - 1 + p + S;
+                    issue_plane<float, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
+                                                x0, y0, kz);
+                } else {
+                    if (p + S == nplanes) {                   // the slots start to free: next unit
+                        nxt = grab_next_t0(sch, unit);
+                        s_next = nxt;
+                        if (nxt < sch.units) {
+                            const int nt = nxt % sch.ntiles, nc = nxt / sch.ntiles;
+                            nx0 = (nt % sch.tiles_x) * G::BX;
+                            ny0 = (nt / sch.tiles_x) * BY;
+                            nkb = nc * sch.chunk;
+                            nke = min(nkb + sch.chunk, D.nz);
+                        }
+                    }
+                    const int q = p + S - nplanes;            // plane q of the next unit
+                    if (nxt < sch.units && q < nke - nkb + 2) {
+                        const int kz = nkb - 1 + q;
+                        issue_plane<float, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
+                                                    nx0, ny0, kz);
+                        pre = q + 1;
+                    }
+                }
             }
         }
         lcount += nplanes;
+        if (S == 2) __syncthreads();                          // s_next written in the last iteration
+        unit = s_next;
     }
     if (TR && tr.energy) {
         const double sum = block_sum(eacc);
@@ -771,11 +856,20 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
     }
     __syncthreads();
     uint32_t lcount = 0;
-    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
+    // cross-unit pipelining: while a unit drains (its last S - 1 plane iterations issue no
+    // refills), thread 0 grabs the next unit and issues that unit's first planes into the
+    // freed stage slots, so the next unit starts on planes already in flight
+    __shared__ int s_next;
+    int pre = 0;                                          // (thread 0) planes of `unit` already issued
+    int unit = grab_unit(sch, -1);
+    while (unit < sch.units) {
         const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
         const int x0 = (tile % sch.tiles_x) * BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
         const int nplanes = ke - kb + 2;
+        const int pre_cur = pre;
+        pre = 0;
+        int nxt = 0x7fffffff, nx0 = 0, ny0 = 0, nkb = 0, nke = 0;   // (thread 0) the next unit
         stage_ztab<T, EM, HA>(zt, cf, kb, nplanes, D.nz);
         // phase-A validity (k-independent parts)
         const int iE = x0 + ii, jE = y0 + jj;             // u_e point
@@ -793,7 +887,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
         // own-point u_h(k-1) (x, y) carried from the previous plane (the u_h ring holds one plane)
         T hxm = T(0), hym = T(0);
         if (tid == 0)
-            for (int p = 0; p < min(S, nplanes); ++p) {
+            for (int p = pre_cur; p < min(S, nplanes); ++p) {
                 const uint32_t L = lcount + p, kz = kb - 1 + p;
                 issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
                                             &tm_y, x0, y0, kz, !init && kz >= kb && kz < ke);
@@ -844,6 +938,8 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
                         u1 = (lyE && vk && kp) ? bE1 * c1 : T(0);
                         u2 = (lzE && vk) ? bE2 * c2 : T(0);
                     }
+                    PE_CHECK(rA >= 0 && rA < G::RP && sE >= G::WX + 1 && sE < G::PL && sH >= 0 && sH + G::WX + 1 < G::PL,
+                             "K2 ring / stage index");
                     UE1[rA] = u0;
                     UE1[G::RP + rA] = u1;
                     UE1[2 * G::RP + rA] = u2;
@@ -928,6 +1024,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
                     wn5 = (kp ? -(bh2 * c2) : T(0)) + e2 * w5;
                     if (mode == 0) {
                         T *wo = wout + go;
+                        PE_CHECK(D.in_state(go + 5 * D.cs) && iB < D.nx && jB < D.ny, "K2 w' store");
                         wo[0] = wn0;
                         wo[D.cs] = wn1;
                         wo[2 * D.cs] = wn2;
@@ -970,6 +1067,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
                         }
                 }
                 T *yo = y + go;
+                PE_CHECK(D.in_state(go + 5 * D.cs), "K2 y store");
                 yo[0] = y0;
                 yo[D.cs] = y1;
                 yo[2 * D.cs] = y2;
@@ -980,13 +1078,37 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
             hxm = hx0;
             hym = hy0;
             __syncthreads();
-            if (tid == 0 && p + S < nplanes) {
-                const uint32_t L = lcount + p + S, kz = kb - 1 + p + S;
-                issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
-                                            &tm_y, x0, y0, kz, !init && kz >= kb && kz < ke);
+            if (tid == 0) {
+                const uint32_t L = lcount + p + S;
+                if (p + S < nplanes) {
+                    const int kz = kb - 1 + p + S;
+                    issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
+                                                &tm_y, x0, y0, kz, !init && kz >= kb && kz < ke);
+                } else {
+                    if (p + S == nplanes) {                   // the slots start to free: next unit
+                        nxt = grab_next_t0(sch, unit);
+                        s_next = nxt;
+                        if (nxt < sch.units) {
+                            const int nt = nxt % sch.ntiles, nc = nxt / sch.ntiles;
+                            nx0 = (nt % sch.tiles_x) * BX;
+                            ny0 = (nt / sch.tiles_x) * BY;
+                            nkb = nc * sch.chunk;
+                            nke = min(nkb + sch.chunk, D.nz);
+                        }
+                    }
+                    const int q = p + S - nplanes;            // plane q of the next unit
+                    if (nxt < sch.units && q < nke - nkb + 2) {
+                        const int kz = nkb - 1 + q;
+                        issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                                    &tm_cH, &tm_y, nx0, ny0, kz, !init && kz >= nkb && kz < nke);
+                        pre = q + 1;
+                    }
+                }
             }
         }
         lcount += nplanes;
+        if (S == 2) __syncthreads();                          // s_next written in the last iteration
+        unit = s_next;
     }
     if (et.norms) {
         const double ds = block_sum(dacc);
@@ -1074,11 +1196,19 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
     auto st2 = [](T *p, T u, T v) { *reinterpret_cast<V2 *>(p) = Vec2<T>::make(u, v); };
     double dacc = 0.0, yacc = 0.0;
     uint32_t lcount = 0;
-    for (int unit = grab_unit(sch, -1); unit < sch.units; unit = grab_unit(sch, unit)) {
+    // cross-unit pipelining (as in K2): thread 0 issues the next unit's first planes into the
+    // stage slots the draining unit frees
+    __shared__ int s_next;
+    int pre = 0;
+    int unit = grab_unit(sch, -1);
+    while (unit < sch.units) {
         const int tile = unit % sch.ntiles, chunk = unit / sch.ntiles;
         const int x0 = (tile % sch.tiles_x) * G::BX, y0 = (tile / sch.tiles_x) * BY;
         const int kb = chunk * sch.chunk, ke = min(kb + sch.chunk, D.nz);
         const int nplanes = ke - kb + 2;
+        const int pre_cur = pre;
+        pre = 0;
+        int nxt = 0x7fffffff, nx0 = 0, ny0 = 0, nkb = 0, nke = 0;
         stage_ztab<T, EM, HA>(zt, cf, kb, nplanes, D.nz);
         // global coordinates and validity of the E / H points (a = left, b = right)
         const int iEa = x0 + xE, jE = y0 + yE, iHa = x0 + xH, jH = y0 + yH;
@@ -1094,7 +1224,7 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
         T uea0 = T(0), ueb0 = T(0), uea1 = T(0), ueb1 = T(0), uea2 = T(0), ueb2 = T(0);   // u_e(k)
         T uma0 = T(0), umb0 = T(0), uma1 = T(0), umb1 = T(0), uma2 = T(0), umb2 = T(0);   // u_h(k-1)
         if (tid == 0)
-            for (int p = 0; p < min(S, nplanes); ++p) {
+            for (int p = pre_cur; p < min(S, nplanes); ++p) {
                 const uint32_t L = lcount + p, kz = kb - 1 + p;
                 issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
                                             &tm_y, x0, y0, kz, !init && kz >= kb && kz < ke);
@@ -1304,6 +1434,7 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
                     }
                 }
                 const int64_t go = gB + (int64_t)k * D.plane;
+                PE_CHECK(D.in_state(go + 5 * D.cs + 1) && (go & 1) == 0, "K2v w' / y store");
                 if (mode == 0) {
 #pragma unroll
                     for (int c = 0; c < 6; ++c) st2(wout + go + c * D.cs, wn[c], wn[6 + c]);
@@ -1341,13 +1472,37 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
             uea0 = ua0; ueb0 = ub0; uea1 = ua1; ueb1 = ub1; uea2 = ua2; ueb2 = ub2;
             uma0 = va0; umb0 = vb0; uma1 = va1; umb1 = vb1; uma2 = va2; umb2 = vb2;
             __syncthreads();
-            if (tid == 0 && p + S < nplanes) {
-                const uint32_t L = lcount + p + S, kz = kb - 1 + p + S;
-                issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
-                                            &tm_y, x0, y0, kz, !init && kz >= kb && kz < ke);
+            if (tid == 0) {
+                const uint32_t L = lcount + p + S;
+                if (p + S < nplanes) {
+                    const int kz = kb - 1 + p + S;
+                    issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
+                                                &tm_y, x0, y0, kz, !init && kz >= kb && kz < ke);
+                } else {
+                    if (p + S == nplanes) {                   // the slots start to free: next unit
+                        nxt = grab_next_t0(sch, unit);
+                        s_next = nxt;
+                        if (nxt < sch.units) {
+                            const int nt = nxt % sch.ntiles, nc = nxt / sch.ntiles;
+                            nx0 = (nt % sch.tiles_x) * G::BX;
+                            ny0 = (nt / sch.tiles_x) * BY;
+                            nkb = nc * sch.chunk;
+                            nke = min(nkb + sch.chunk, D.nz);
+                        }
+                    }
+                    const int q = p + S - nplanes;            // plane q of the next unit
+                    if (nxt < sch.units && q < nke - nkb + 2) {
+                        const int kz = nkb - 1 + q;
+                        issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE,
+                                                    &tm_cH, &tm_y, nx0, ny0, kz, !init && kz >= nkb && kz < nke);
+                        pre = q + 1;
+                    }
+                }
             }
         }
         lcount += nplanes;
+        if (S == 2) __syncthreads();                          // s_next written in the last iteration
+        unit = s_next;
     }
     if (ET && et.norms) {
         const double ds = block_sum(dacc);
@@ -1427,7 +1582,9 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
     // about tiles_x * chunk / resident planes later; keep that within ~4 planes so its halo
     // rows are still in L2 (measured at 768^3 fp64: chunk 48-64 beats the unconstrained 154
     // by 4%)
-    const int cap = std::max(8, (int)(4.0 * resident / std::max(1, s.tiles_x)));
+    // and at most 48 planes: measured with the dynamic order (C5 vacuum, K1r fp64): 640^3 chunk
+    // 32-48 4.27 ms vs the cost model's pick 5.01 ms; 384^3 0.87 vs 0.99 ms
+    const int cap = std::min(48, std::max(8, (int)(4.0 * resident / std::max(1, s.tiles_x))));
     for (int ch = 1; ch <= g.nz; ++ch) {
         const int nch = (g.nz + ch - 1) / ch;
         const double units = (double)s.ntiles * nch;
@@ -1435,7 +1592,7 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
         // L2-resident grids, where a unit's time is latency: measured at 64^3 fp64 chunk 4
         // 10.3 us vs chunk 8 12.3 us per leapfrog step, 32^3 chunk 1 6.2 vs 12.3 us)
         if (ch < std::min(g.nz, 8) && nch > 1 && units > resident) continue;
-        if (ch > cap && ch > 8) continue;
+        if (ch > cap) continue;
         if (ch > ZT_ROW - 2) continue;       // the staged z-table holds chunk + 2 planes
         const double waves = units / resident;
         const double eff_waves = std::ceil(waves);

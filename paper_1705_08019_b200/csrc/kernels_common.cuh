@@ -15,9 +15,31 @@ namespace pe {
 //   h_x live iff i>0;  h_y iff j>0;  h_z iff k>0                         (box-normal faces)
 // Interior PEC cells are encoded by cE = 0 (material mode ARRAY only).
 template <typename T>
+// ---- debug checks: built into libparaexp_debug.so (python paper_1705_08019_b200/build.py --debug,
+// -DPARAEXP_DEBUG_CHECKS); compute-sanitizer is closed on this GPU pool, so out-of-range global
+// stores, ring / stage indices out of their shared-memory planes and mbarrier waits that never
+// complete trap with a message instead.  Compiled out of the product library.
+#ifdef PARAEXP_DEBUG_CHECKS
+#include <cstdio>
+#define PE_CHECK(cond, what)                                                                        \
+    do {                                                                                            \
+        if (!(cond)) {                                                                              \
+            printf("paraexp debug check failed: %s at %s:%d (block %d, thread %d)\n", what, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                   \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#else
+#define PE_CHECK(cond, what) \
+    do {                     \
+    } while (0)
+#endif
+
 struct Dev {
     int nx, ny, nz;
     int64_t px, plane, cs;
+    // a store of components [c0, c0 + n) at element offset `off` of a state vector stays inside it
+    __host__ __device__ __forceinline__ bool in_state(int64_t off) const { return off >= 0 && off < 6 * cs; }
     __host__ __device__ __forceinline__ int64_t idx(int i, int j, int k) const {
         return (int64_t)i + px * ((int64_t)j + (int64_t)ny * k);
     }
