@@ -64,6 +64,13 @@ def workload(name):
     raise SystemExit(f"unknown workload {name}")
 
 
+def set_p(w, p):
+    """--p: override the workload's sub-interval count (and the -p<k> suffix of its name)."""
+    import re
+    w.p = p
+    w.name = re.sub(r"-p\d+$", "", w.name) + f"-p{p}"
+
+
 def hbm_peak():
     try:
         d = json.load(open(PEAKS_FILE))
@@ -200,7 +207,7 @@ def run_reference(args, rank, world):
     steps = []
     cb = None
     if args.p:
-        w.p = args.p
+        set_p(w, args.p)
     for it in range(args.warmup + args.steps):
         r = cpu_baseline(w, single_thread=False)
         if it >= args.warmup:
@@ -252,7 +259,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = workload(args.workload)
     if args.p:
-        w.p = args.p
+        set_p(w, args.p)
     grid = pe.Grid.from_workload(w, device=local, kernels=args.kernels)
     stream = torch.cuda.current_stream(local)
     info = grid.info(compute_rho_pow=True, stream=stream.cuda_stream)

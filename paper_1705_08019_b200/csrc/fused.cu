@@ -134,6 +134,7 @@ struct Sched {
     // exactly units + gridDim (every CTA ends with one failing grab); base is its start.
     unsigned long long *ctr;
     unsigned long long base;
+    int lookahead;   // cross-unit prefetch of the next unit's first planes (PARAEXP_NO_LOOKAHEAD=1: off)
 };
 
 // unit loop: static stride (ctr == nullptr) or dynamic grabs; uniform per CTA
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, 3) leapfrog_r_kernel(
                         }
                     }
                     const int q = p + S - nplanes;            // plane q of the next unit
-                    if (nxt < sch.units && q < nke - nkb + 2) {
+                    if (sch.lookahead && nxt < sch.units && q < nke - nkb + 2) {
                         const int kz = nkb - 1 + q;
                         issue_plane<T, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
                                                     nx0, ny0, kz);
@@ -756,7 +757,7 @@ __global__ void __launch_bounds__(GeoV<BY>::NTHR, 3) leapfrog_v_kernel(
                         }
                     }
                     const int q = p + S - nplanes;            // plane q of the next unit
-                    if (nxt < sch.units && q < nke - nkb + 2) {
+                    if (sch.lookahead && nxt < sch.units && q < nke - nkb + 2) {
                         const int kz = nkb - 1 + q;
                         issue_plane<float, EM, HA, G>(stages + (L % S) * SL::SZ, &bars[L % S], &tm_state, &tm_cE, &tm_cH,
                                                     nx0, ny0, kz);
@@ -1097,7 +1098,7 @@ __global__ void __launch_bounds__(Geo<T, BX, BY>::NTHR, sizeof(T) == 8 ? 2 : 3) 
                         }
                     }
                     const int q = p + S - nplanes;            // plane q of the next unit
-                    if (nxt < sch.units && q < nke - nkb + 2) {
+                    if (sch.lookahead && nxt < sch.units && q < nke - nkb + 2) {
                         const int kz = nkb - 1 + q;
                         issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE,
                                                     &tm_cH, &tm_y, nx0, ny0, kz, !init && kz >= nkb && kz < nke);
@@ -1491,7 +1492,7 @@ __global__ void __launch_bounds__(GeoW<T, BY>::NTHR, sizeof(T) == 8 ? 1 : 2) pai
                         }
                     }
                     const int q = p + S - nplanes;            // plane q of the next unit
-                    if (nxt < sch.units && q < nke - nkb + 2) {
+                    if (sch.lookahead && nxt < sch.units && q < nke - nkb + 2) {
                         const int kz = nkb - 1 + q;
                         issue_plane_y<T, EM, HA, G>(stages + (L % S) * SP::SZ, &bars[L % S], &tm_state, &tm_cE,
                                                     &tm_cH, &tm_y, nx0, ny0, kz, !init && kz >= nkb && kz < nke);
@@ -1582,9 +1583,10 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
     // about tiles_x * chunk / resident planes later; keep that within ~4 planes so its halo
     // rows are still in L2 (measured at 768^3 fp64: chunk 48-64 beats the unconstrained 154
     // by 4%)
-    // and at most 48 planes: measured with the dynamic order (C5 vacuum, K1r fp64): 640^3 chunk
-    // 32-48 4.27 ms vs the cost model's pick 5.01 ms; 384^3 0.87 vs 0.99 ms
-    const int cap = std::min(48, std::max(8, (int)(4.0 * resident / std::max(1, s.tiles_x))));
+    // and at most 32 planes: measured with the dynamic order (C5 vacuum, K1r fp64): 640^3 chunk
+    // 32-48 4.27 ms vs the cost model's pick (88) 5.01 ms; 384^3 0.87 vs 0.99 ms; at 768^3 ncu
+    // read 1.5x the algorithmic bytes with chunks 48-74 and 1.15x with 24 (L2 hit rate 35 -> 45%)
+    const int cap = std::min(32, std::max(8, (int)(4.0 * resident / std::max(1, s.tiles_x))));
     for (int ch = 1; ch <= g.nz; ++ch) {
         const int nch = (g.nz + ch - 1) / ch;
         const double units = (double)s.ntiles * nch;
@@ -1608,6 +1610,8 @@ static Sched make_sched(const Grid &g, int BX, int BY, int resident) {
     s.nchunks = (g.nz + bc - 1) / bc;
     s.units = s.ntiles * s.nchunks;
     s.ctr = nullptr;
+    s.lookahead = 1;
+    if (const char *ev = getenv("PARAEXP_NO_LOOKAHEAD")) s.lookahead = atoi(ev) == 0;
     s.base = 0;
     return s;
 }
