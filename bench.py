@@ -136,19 +136,26 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------
-TRAFFIC_FILES = {("expmv_pair", "C3-f64-p8"): "profiles/r1_ncu_full_pair_c3_f64.json",
-                 ("leapfrog", "C3-f64-p8"): "profiles/r1_ncu_full_leapfrog_c3_f64.json"}
+# committed `ncu --set full` summaries (tools/ncu_kernels.sh + tools/ncu_summary.py) of the
+# current kernels on the bench grids: (file, kernel-name substring); the pair entry is the
+# non-initial op (the first op of a substep does not read y)
+TRAFFIC_FILES = {("expmv_pair", "C3-f64-p8"): ("profiles/r2_ncu_full_f64_256.json", "pair_fused"),
+                 ("leapfrog", "C3-f64-p8"): ("profiles/r2_ncu_full_f64_256.json", "leapfrog_r"),
+                 ("expmv_pair", "C3-f32-p8"): ("profiles/r2_ncu_full_f32_256.json", "pair_v"),
+                 ("leapfrog", "C3-f32-p8"): ("profiles/r2_ncu_full_f32_256.json", "leapfrog_v")}
 
 
 def committed_traffic(kernel, w):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from the
     committed `ncu --set full` summary of the same kernel on the same grid (or None)."""
-    path = TRAFFIC_FILES.get((kernel, w.name))
+    path, sub = TRAFFIC_FILES.get((kernel, w.name), (None, None))
     if not path or not os.path.exists(os.path.join(ROOT, path)):
         return None, None
-    d = json.load(open(os.path.join(ROOT, path)))
-    vals = [x["dram_bytes"] for x in d]
-    return sum(vals) / len(vals), path
+    d = [x for x in json.load(open(os.path.join(ROOT, path))) if sub in x["kernel"]]
+    if not d:
+        return None, None
+    return (max(x["dram_bytes"] for x in d) if kernel == "expmv_pair"
+            else sum(x["dram_bytes"] for x in d) / len(d)), path
 
 
 def _oracle_sample(fit, g, w, nlf):

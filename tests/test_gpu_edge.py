@@ -90,12 +90,16 @@ def test_rho_pow_bounds():
     assert 0.6 * inf2["rho_cfl"] < inf2["rho_pow"] < 0.85 * inf2["rho_cfl"]
 
 
-def test_nccl_path_one_rank(monkeypatch):
+@pytest.mark.parametrize("window", ["0", "1"])
+def test_nccl_path_one_rank(monkeypatch, window):
     """a8 on one GPU: a one-rank NCCL communicator with the collectives forced on
     (PARAEXP_FORCE_COLLECTIVES: ncclReduce of W, ncclAllReduce of the trace rows,
-    ncclBroadcast of the output) gives the same result as the communicator-free solve."""
+    ncclBroadcast of the output) gives the same result as the communicator-free solve; with
+    PARAEXP_NCCL_WINDOW=1 the reduce goes through the ncclMemAlloc'd buffer registered with
+    ncclCommWindowRegister (symmetric)."""
     import torch
     monkeypatch.setenv("PARAEXP_FORCE_COLLECTIVES", "1")
+    monkeypatch.setenv("PARAEXP_NCCL_WINDOW", window)
     n = (24, 16, 9)
     og = fit.Grid(*n, d0=1e-3, dt_frac=0.9)
     lg = pe.Grid(*n, d0=1e-3, dt_frac=0.9)
