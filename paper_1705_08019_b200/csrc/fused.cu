@@ -181,19 +181,6 @@ struct StageL {
     static constexpr int SZ = ST + CE + CH;
 };
 
-template <typename T, int EM, bool HA, typename G>
-__device__ __forceinline__ T stage_bE(const Coef<T, EM, HA> &cf, const T *st, int c, int kk, int sidx) {
-    if (EM == 2) return st[StageL<T, EM, HA, G>::ST + c * G::PL + sidx] * cf.sig;
-    if (EM == 1) return __ldg(cf.tab + c * cf.nz + kk) * cf.sig;
-    return cf.cEs[c] * cf.sig;
-}
-template <typename T, int EM, bool HA, typename G>
-__device__ __forceinline__ T stage_bH(const Coef<T, EM, HA> &cf, const T *st, int c, int sidx) {
-    using SL = StageL<T, EM, HA, G>;
-    if (HA) return st[SL::ST + SL::CE + c * G::PL + sidx] * cf.sig;
-    return cf.cHs[c] * cf.sig;
-}
-
 // z-table coefficients (EM == 1, layered materials) of a unit's planes kb-1 .. kb+nplanes-2,
 // scaled by sigma, staged in shared memory once per unit: a per-plane __ldg of the table from
 // global memory sat on the critical path of every plane iteration (ncu: ~8-11% of the warp

@@ -242,8 +242,6 @@ void grid_free_device(Grid &G) {
     G.d_norms = nullptr;
     if (G.call_event) dev_event_destroy(G.call_event);
     G.call_event = G.call_stream = nullptr;
-    dev_free(G.d_ops);
-    G.d_ops = nullptr;
     G.sched_base = 0;
     for (void *q : G.kry) dev_free(q);
     G.kry.clear();

@@ -65,7 +65,6 @@ struct Grid {
     std::vector<void *> conc;   // state buffers of concurrently swept sub-intervals
     std::vector<void *> streams; // their cudaStream_t / cudaEvent_t handles (created on demand)
     std::vector<void *> events;
-    void *d_ops = nullptr;      // pair-op table of the multi-op (cooperative) pair launch
     void *d_norms = nullptr;    // per-propagator energy norms of a solve (rho safety net, f. intervals)
     void *call_event = nullptr; // recorded at the end of every call (stream order across calls)
     void *call_stream = nullptr;

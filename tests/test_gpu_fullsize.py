@@ -21,7 +21,7 @@ import numpy as np
 import pytest
 
 import paper_1705_08019_b200 as pe
-from gpu_util import TOL, rel_l2
+from gpu_util import TOL, max_abs_rel, rel_l2
 from oracle import fit
 from synth import config_c3, config_c4, config_c5
 
@@ -100,6 +100,8 @@ def _compare(got_e, got_h, ref, og, w, lo, slo, shi, dtype, what):
     tol = TOL[dtype]
     assert np.linalg.norm(re) > 0 and np.linalg.norm(rh) > 0, what
     assert ee <= tol and eh <= tol, f"{what}: rel-L2 e={ee:.3e} h={eh:.3e} (tol {tol})"
+    me, mh = max_abs_rel(ge, re), max_abs_rel(gh, rh)
+    assert me <= 100 * tol and mh <= 100 * tol, f"{what}: max-abs e={me:.3e} h={mh:.3e}"
     return ee, eh
 
 
