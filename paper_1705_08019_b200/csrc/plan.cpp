@@ -296,24 +296,51 @@ static int make_plan_uncached(int method, int m, int s, double eps_A, double tau
     }
     const double tr = tau * rho;
     if (m == 0) {
-        static const int leja_c[] = {8, 12, 16, 20, 24, 32, 40, 48, 56, 64, 72, 80, 88, 100, 120, 150};
-        static const int tay_c[] = {4, 8, 12, 16, 20, 24, 32, 40, 48};
-        const int *c = method == PARAEXP_LEJA ? leja_c : tay_c;
-        const int nc = method == PARAEXP_LEJA ? 16 : 9;
-        long best = -1;
-        for (int q = 0; q < nc; ++q) {
-            const double th = theta_m(method, c[q], eps_A);
-            if (!(th > 0)) continue;
-            const long sq = s > 0 ? s : std::max(1L, (long)std::ceil(tr / th));
-            if (s > 0 && sq * th < tr) continue;
-            const long cost = sq * c[q];
-            if (best < 0 || cost < best) {
-                best = cost;
-                out.m = c[q];
-                out.s = (int)sq;
+        if (method == PARAEXP_LEJA) {
+            // every admissible degree (even m in [8, 150], reading 16): for each substep count s
+            // from the fewest possible (theta_150) upwards, the smallest m whose per-substep
+            // criterion holds at theta = tau rho / s (bisection over m on poly_error, one
+            // polynomial per probe); keep the least m * s (the A-applications of the plan)
+            const int mmax = PARAEXP_MAX_DEGREE;
+            const double thmax = theta_m(method, mmax, eps_A);
+            if (!(thmax > 0)) return fail(PARAEXP_EINVAL, "no degree satisfies eps_A");
+            const long s0 = s > 0 ? s : std::max(1L, (long)std::ceil(tr / thmax));
+            if (s > 0 && s0 * thmax < tr) return fail(PARAEXP_EINVAL, "no degree satisfies eps_A at the given s");
+            long best = -1;
+            for (long sq = s0; sq <= (s > 0 ? s0 : s0 + 4); ++sq) {
+                const double th = tr / (double)sq;
+                auto ok = [&](int mm) { return poly_error(method, mm, th) <= eps_A * th; };
+                int lo = 4, hi = mmax / 2;                       // m = 2 * half
+                if (!ok(2 * hi)) continue;
+                while (lo < hi) {
+                    const int mid = (lo + hi) / 2;
+                    if (ok(2 * mid)) hi = mid; else lo = mid + 1;
+                }
+                const long cost = sq * 2 * lo;
+                if (best < 0 || cost < best) {
+                    best = cost;
+                    out.m = 2 * lo;
+                    out.s = (int)sq;
+                }
             }
+            if (best < 0) return fail(PARAEXP_EINVAL, "no degree satisfies eps_A at the given s");
+        } else {
+            static const int tay_c[] = {4, 8, 12, 16, 20, 24, 32, 40, 48};
+            long best = -1;
+            for (int q = 0; q < 9; ++q) {
+                const double th = theta_m(method, tay_c[q], eps_A);
+                if (!(th > 0)) continue;
+                const long sq = s > 0 ? s : std::max(1L, (long)std::ceil(tr / th));
+                if (s > 0 && sq * th < tr) continue;
+                const long cost = sq * tay_c[q];
+                if (best < 0 || cost < best) {
+                    best = cost;
+                    out.m = tay_c[q];
+                    out.s = (int)sq;
+                }
+            }
+            if (best < 0) return fail(PARAEXP_EINVAL, "no degree satisfies eps_A at the given s");
         }
-        if (best < 0) return fail(PARAEXP_EINVAL, "no degree satisfies eps_A at the given s");
     } else {
         out.m = m;
         if (s > 0) {

@@ -126,12 +126,19 @@ def test_theta_reference_table():
         assert abs(pe.theta("leja", m, tol) / v - 1) < 0.01
 
 
-def test_auto_plan_minimises_cost():
-    tau, rho, tol = 1.0, 300.0, 1e-10
-    p = pe.plan_host("leja", 0, 0, tol, tau, rho)
-    best = min((mm * max(1, math.ceil(tau * rho / pe.theta("leja", mm, tol))), mm)
+@pytest.mark.parametrize("tr", [300.0, 121.6])
+def test_auto_plan_minimises_cost(tr):
+    """The auto plan (reading 16) satisfies the criterion (s theta_m >= tau rho), is minimal in
+    m at its s, and costs no more A-applications than any degree of a coarse reference list."""
+    tau, tol = 1.0, 1e-10
+    p = pe.plan_host("leja", 0, 0, tol, tau, tr)
+    m, s_ = p["m"], p["s"]
+    assert m % 2 == 0 and 8 <= m <= 150
+    assert s_ * pe.theta("leja", m, tol) >= tau * tr
+    assert m == 8 or s_ * pe.theta("leja", m - 2, tol) < tau * tr
+    best = min(mm * max(1, math.ceil(tau * tr / pe.theta("leja", mm, tol)))
                for mm in [8, 12, 16, 20, 24, 32, 40, 48, 56, 64, 72, 80, 88, 100, 120, 150])
-    assert p["m"] * p["s"] == best[0]
+    assert m * s_ <= best
 
 
 @pytest.mark.parametrize("wl", ["c1", "c3small", "random", "pec"])
