@@ -42,7 +42,8 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        _lib = ctypes.CDLL(build())
+        # ORACLE_SO: an alternative build of the same C file (tools/asan_host.sh: ASan/UBSan)
+        _lib = ctypes.CDLL(os.environ.get("ORACLE_SO") or build())
         dp = ctypes.POINTER(ctypes.c_double)
         up = ctypes.POINTER(ctypes.c_ubyte)
         lp = ctypes.POINTER(ctypes.c_long)
