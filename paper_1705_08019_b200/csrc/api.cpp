@@ -1460,6 +1460,9 @@ static int solve_finish_dev(Grid &G, const SolveCtx &c, const KernelArgs &ka, Ev
                             paraexp_stats &S, SolveBufs &b) {
     int rc;
     nvtxRangePushA("paraexp_finish");
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop;
     if (c.tail_mode == PARAEXP_TAIL_EXP) {
         if ((rc = k_axpy_comps(ka, b.P, b.W, 1.0, 0, 3))) return rc;       // e_out = e_p + W_e
         void *bufs[4] = {b.W, b.X[0], b.X[1], b.X[2]};
@@ -1473,7 +1476,6 @@ static int solve_finish_dev(Grid &G, const SolveCtx &c, const KernelArgs &ka, Ev
     } else {
         if ((rc = k_axpy(ka, b.P, b.W, 1.0))) return rc;
     }
-    nvtxRangePop();
     return PARAEXP_OK;
 }
 

@@ -140,7 +140,7 @@ def _run_leapfrog_expmv(w, dtype, nlf, m, centers, half=6, seed=11, t0=0.0):
     torch.cuda.empty_cache()
 
 
-def _run_solve(w, dtype, nsteps, p, m, centers, half=5, seed=13):
+def _run_solve(w, dtype, nsteps, p, m, centers, half=5, seed=13, t0=0.0):
     """full-grid CUDA paraexp_solve (random u0 + the workload's sources, fixed Leja plan
     (m, s = 1) per sub-interval) vs the oracle's sequential Algorithm 1 on sub-grids"""
     import torch
@@ -149,7 +149,7 @@ def _run_solve(w, dtype, nsteps, p, m, centers, half=5, seed=13):
     lg = pe.Grid.from_workload(w, dtype=dtype)
     e0, h0 = _dev_fields(w, seed, dtype)
     eo, ho = torch.zeros_like(e0), torch.zeros_like(h0)
-    st = pe.solve(lg, nsteps, p, w.sources, u0=(e0, h0), method="leja", m=m, s=1, rho=rho,
+    st = pe.solve(lg, nsteps, p, w.sources, t0=t0, u0=(e0, h0), method="leja", m=m, s=1, rho=rho,
                   e_out=eo, h_out=ho)
     torch.cuda.synchronize()
     assert st["leapfrog_steps"] == nsteps
@@ -161,7 +161,7 @@ def _run_solve(w, dtype, nsteps, p, m, centers, half=5, seed=13):
         og = _sub_grid(w, lo, hi, dt, dtype)
         u0 = (_extract(e0, w, lo, hi), _extract(h0, w, lo, hi))
         src = _sub_sources(og, w, lo, hi)
-        ref = fit.paraexp(og, src, 0.0, nsteps, p, lambda tau: fit.make_plan("leja", m, 1, tau, rho),
+        ref = fit.paraexp(og, src, t0, nsteps, p, lambda tau: fit.make_plan("leja", m, 1, tau, rho),
                           u0=u0, rho=rho, dtype=dtype)
         _compare(eo, ho, ref, og, w, lo, slo, shi, dtype, f"{w.name} solve {dtype} centre {c}")
     del e0, h0, eo, ho
@@ -191,6 +191,17 @@ def test_c4_fullsize_spiral():
     port = (w.sources[0].i, w.sources[0].j, 5)
     _run_leapfrog_expmv(w, "f64", 40, 16, [port, (256, 256, 10)], t0=150e-12)
     _run_solve(w, "f64", 16, 8, 4, [port])
+
+
+def test_c4_fullsize_longer_horizon():
+    """C4 with the port current at its peak (t0 = 200 ps, GAUSS_SINE delay 254.6 ps): 180
+    leapfrog steps + a degree-16 substep, and a p = 8 solve over 120 steps (every sub-interval
+    and tail), sampled at the port -- a domain of dependence of ~200 cells in x and y, the
+    whole height in z."""
+    w = config_c4(nsteps=200)
+    port = (w.sources[0].i, w.sources[0].j, 5)
+    _run_leapfrog_expmv(w, "f64", 180, 16, [port], half=4, t0=200e-12)
+    _run_solve(w, "f64", 120, 8, 8, [port], half=4, t0=200e-12)
 
 
 @pytest.mark.parametrize("n,dtype", [(768, "f32"), (512, "f64")])
