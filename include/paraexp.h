@@ -63,7 +63,7 @@ enum { PARAEXP_F64 = 0, PARAEXP_F32 = 1 };
 enum { PARAEXP_SRC_ZERO = 0, PARAEXP_SRC_GAUSS_PAPER = 1, PARAEXP_SRC_GAUSS_SINE = 2,
        PARAEXP_SRC_SINE = 3 };
 enum { PARAEXP_TAYLOR = 0, PARAEXP_LEJA = 1, PARAEXP_KRYLOV = 2 };
-enum { PARAEXP_TAIL_EXP = 0, PARAEXP_TAIL_LEAPFROG = 1 };
+enum { PARAEXP_TAIL_EXP = 0, PARAEXP_TAIL_LEAPFROG = 1, PARAEXP_TAIL_EXP_LPT = 2 };
 enum { PARAEXP_MAT_SCALAR = 0, PARAEXP_MAT_ZTABLE = 1, PARAEXP_MAT_ARRAY = 2 };
 enum { PARAEXP_KERNELS_AUTO = 0, PARAEXP_KERNELS_UNFUSED = 1, PARAEXP_KERNELS_FUSED = 2 };
 
@@ -364,6 +364,13 @@ int paraexp_partition(int64_t nsteps, int32_t p, int64_t *bounds);
  * later ranks.  Host-only. */
 int paraexp_schedule(int32_t p, int32_t world, int32_t rank, double tail_ratio, int32_t has_u0,
                      int32_t *first, int32_t *last, int32_t *root);
+/* Schedule (B), tail_mode PARAEXP_TAIL_EXP_LPT: owner[j] (j = 1..p) = rank of sub-interval j
+ * and its independent tail, owner[0] = rank of the u0 tail (-1 if has_u0 == 0); job j costs
+ * one sweep + (p - j) propagators, job 0 p propagators (propagator = tail_ratio sweeps); jobs
+ * in decreasing cost (ties: lower j) go to the least-loaded rank (ties: lower rank).
+ * *root = owner[p].  Host-only. */
+int paraexp_schedule_lpt(int32_t p, int32_t world, double tail_ratio, int32_t has_u0, int32_t *owner,
+                         int32_t *root);
 /* Symmetrised Leja sequence xi'_0..xi'_{count-1} on [-1,1] (reading 14). */
 int paraexp_leja_points(int32_t count, double *xi);
 /* Plan without a grid: tau and rho given, dt used only for sigma (may be 1). */

@@ -14,12 +14,13 @@ import numpy as np
 
 from . import abi
 from .abi import (EDIVERGED, EINVAL, ENOTSUP, EOVERFLOW, F32, F64, KERNELS_AUTO, KERNELS_FUSED,  # noqa
-                  KERNELS_UNFUSED, KRYLOV, LEJA, TAIL_EXP, TAIL_LEAPFROG, TAYLOR, ParaexpError, check)
+                  KERNELS_UNFUSED, KRYLOV, LEJA, TAIL_EXP, TAIL_EXP_LPT, TAIL_LEAPFROG, TAYLOR, ParaexpError,
+                  check)
 
 __all__ = ["Grid", "Comm", "leapfrog", "leapfrog_trace", "expmv", "expmv_plan", "solve", "solve_trace",
            "solve_block", "solve_finish",
            "optimal_tolerance",
-           "partition", "schedule",
+           "partition", "schedule", "schedule_lpt",
            "leja_points", "plan_host", "theta", "version", "make_sources", "ParaexpError"]
 
 _DT = {"f64": F64, "f32": F32}
@@ -275,6 +276,15 @@ def schedule(p: int, world: int, rank: int, tail_ratio: float = 0.0, has_u0: boo
     return f.value, l.value, r.value
 
 
+def schedule_lpt(p: int, world: int, tail_ratio: float = 1.0, has_u0: bool = False) -> tuple:
+    """paraexp_schedule_lpt: (owner list [owner of u0 tail, owner of 1, ..., owner of p], root)."""
+    o = (C.c_int32 * (p + 1))()
+    r = C.c_int32()
+    check(abi.lib.paraexp_schedule_lpt(int(p), int(world), float(tail_ratio), int(bool(has_u0)), o,
+                                       C.byref(r)), "paraexp_schedule_lpt")
+    return list(o), r.value
+
+
 class Comm:
     """paraexp_comm_*: the library's own NCCL communicator.  The 128-byte id is created on
     rank 0 and broadcast with torch.distributed (plumbing only)."""
@@ -318,7 +328,8 @@ class Comm:
 
 
 def _tail_mode(tail_mode):
-    return tail_mode if isinstance(tail_mode, int) else {"exp": TAIL_EXP, "leapfrog": TAIL_LEAPFROG}[tail_mode]
+    return tail_mode if isinstance(tail_mode, int) else {"exp": TAIL_EXP, "leapfrog": TAIL_LEAPFROG,
+                                                         "exp_lpt": TAIL_EXP_LPT}[tail_mode]
 
 
 def solve(grid: Grid, nsteps: int, p: int, sources=None, t0: float = 0.0, method="leja", m=0,

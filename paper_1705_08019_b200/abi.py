@@ -25,7 +25,7 @@ WCFL = 1
 F64, F32 = 0, 1
 SRC_ZERO, SRC_GAUSS_PAPER, SRC_GAUSS_SINE, SRC_SINE = 0, 1, 2, 3
 TAYLOR, LEJA, KRYLOV = 0, 1, 2
-TAIL_EXP, TAIL_LEAPFROG = 0, 1
+TAIL_EXP, TAIL_LEAPFROG, TAIL_EXP_LPT = 0, 1, 2
 MAT_SCALAR, MAT_ZTABLE, MAT_ARRAY = 0, 1, 2
 KERNELS_AUTO, KERNELS_UNFUSED, KERNELS_FUSED = 0, 1, 2
 MAX_DEGREE = 150
@@ -122,6 +122,8 @@ _sigs = {
     "paraexp_partition": (C.c_int, [C.c_int64, C.c_int32, C.POINTER(C.c_int64)]),
     "paraexp_schedule": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32,
                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "paraexp_schedule_lpt": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_int32, C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_int32)]),
     "paraexp_solve_block": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(paraexp_source), C.c_int32,
                                       C.c_double, C.c_int64, C.c_int32, C.POINTER(paraexp_expmv_opts),
                                       C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -575,6 +575,7 @@ static int opts_plan(Grid &G, double tau, const paraexp_expmv_opts *o, double rh
 // > 0), never for Krylov (norm-preserving by construction) or when rho is already rho_cfl.
 static void schedule_blocks(int p, int world, double ratio, bool u0, std::vector<int> &F,
                             std::vector<int> &L, int &root);
+static void schedule_lpt(int p, int world, double ratio, bool u0, std::vector<int> &owner, int &root);
 static int ensure_norms(Grid &G);
 
 static bool rho_check_on(const Grid &G, const paraexp_expmv_opts *o, double rho) {
@@ -793,6 +794,17 @@ int paraexp_schedule(int32_t p, int32_t world, int32_t rank, double tail_ratio, 
     pe::schedule_blocks(p, world, tail_ratio, has_u0 != 0, F, L, r);
     if (first) *first = F[rank];
     if (last) *last = L[rank];
+    if (root) *root = r;
+    return PARAEXP_OK;
+}
+
+int paraexp_schedule_lpt(int32_t p, int32_t world, double tail_ratio, int32_t has_u0, int32_t *owner,
+                         int32_t *root) {
+    if (p < 1 || world < 1 || !owner) return pe::fail(PARAEXP_EINVAL, "bad schedule arguments");
+    std::vector<int> o;
+    int r = 0;
+    pe::schedule_lpt(p, world, tail_ratio, has_u0 != 0, o, r);
+    for (int j = 0; j <= p; ++j) owner[j] = o[j];
     if (root) *root = r;
     return PARAEXP_OK;
 }
@@ -1043,6 +1055,11 @@ struct SolveCtx {
     std::map<int64_t, Plan> plans;
     Plan half;
     const paraexp_expmv_opts *opts = nullptr;
+    // tail_mode EXP_LPT: the sub-intervals this rank owns (ascending) and whether it owns the
+    // u0 tail (job 0)
+    std::vector<int> owned;
+    bool owns_u0 = false;
+    bool exp_tails() const { return tail_mode != PARAEXP_TAIL_LEAPFROG; }
 };
 
 struct SolveBufs {
@@ -1126,6 +1143,30 @@ static void schedule_blocks(int p, int world, double ratio, bool u0, std::vector
         if (L[r] == p) root = r;
 }
 
+// Schedule (B) of SURVEY 8(e), kept as a comparison: the paper's literal structure, one
+// independent tail per sub-interval, longest-processing-time-first.  Job j
+// (1..p) costs one sweep + (p - j) propagators; job 0 (the u0 tail, if present) p propagators.
+// Jobs in decreasing cost (ties: lower j first) go to the least-loaded rank (ties: lower
+// rank).  owner[j] = rank of job j (owner[0] = -1 without u0); root = owner[p].
+static void schedule_lpt(int p, int world, double ratio, bool u0, std::vector<int> &owner, int &root) {
+    owner.assign(p + 1, -1);
+    std::vector<std::pair<double, int>> jobs;
+    if (u0) jobs.push_back({p * std::max(ratio, 0.0), 0});
+    for (int j = 1; j <= p; ++j) jobs.push_back({1.0 + (p - j) * std::max(ratio, 0.0), j});
+    std::stable_sort(jobs.begin(), jobs.end(), [](const std::pair<double, int> &a, const std::pair<double, int> &b) {
+        return a.first > b.first || (a.first == b.first && a.second < b.second);
+    });
+    std::vector<double> load(world, 0.0);
+    for (const auto &jb : jobs) {
+        int r = 0;
+        for (int q = 1; q < world; ++q)
+            if (load[q] < load[r]) r = q;
+        owner[jb.second] = r;
+        load[r] += jb.first;
+    }
+    root = owner[p];
+}
+
 // ---- debug fault injection (PARAEXP_DEBUG_NAN=particular:<i> | tail:<i>) --
 // Writes one NaN into a live interior e_x entry after sub-interval i's particular sweep or
 // after propagator E_i, so the tests can check that EDIVERGED / EOVERFLOW name interval i.
@@ -1162,7 +1203,8 @@ static int solve_prepare(Grid &G, paraexp_comm_view comm, int rank, int world,
                          bool has_u0, void *stream, paraexp_stats &S, SolveCtx &c) {
     if (p < 1 || nsteps < p) return fail(PARAEXP_EINVAL, "need p >= 1 and nsteps >= p");
     if (p > 1000) return fail(PARAEXP_EINVAL, "p > 1000 not supported");
-    if (tail_mode != PARAEXP_TAIL_EXP && tail_mode != PARAEXP_TAIL_LEAPFROG) return fail(PARAEXP_EINVAL, "bad tail mode");
+    if (tail_mode != PARAEXP_TAIL_EXP && tail_mode != PARAEXP_TAIL_LEAPFROG && tail_mode != PARAEXP_TAIL_EXP_LPT)
+        return fail(PARAEXP_EINVAL, "bad tail mode");
     if (world < 1 || rank < 0 || rank >= world) return fail(PARAEXP_EINVAL, "bad rank / world");
     c.nsteps = nsteps;
     c.p = p;
@@ -1179,15 +1221,26 @@ static int solve_prepare(Grid &G, paraexp_comm_view comm, int rank, int world,
     if (comm.bcast_rho && (rc = comm.bcast_rho(comm.ctx, &c.rho, stream))) return rc;
     const int mode = opts ? opts->rho_check : 0;
     const bool explicit_rho = opts && opts->rho > 0;
-    c.rho_check = tail_mode == PARAEXP_TAIL_EXP && !(opts && opts->method == PARAEXP_KRYLOV) &&
+    c.rho_check = c.exp_tails() && !(opts && opts->method == PARAEXP_KRYLOV) &&
                   (mode > 0 || (mode == 0 && !explicit_rho)) && c.rho < G.rho_cfl;
     c.auto_plan = !(opts && opts->m > 0);
     if ((rc = build_plans(G, c))) return rc;
     c.ratio = tail_ratio(c);
-    std::vector<int> F, L;
-    schedule_blocks(p, world, c.ratio, has_u0, F, L, c.root);
-    c.first = F[rank];
-    c.last = L[rank];
+    if (tail_mode == PARAEXP_TAIL_EXP_LPT) {
+        std::vector<int> owner;
+        schedule_lpt(p, world, c.ratio, has_u0, owner, c.root);
+        c.owned.clear();
+        for (int j = 1; j <= p; ++j)
+            if (owner[j] == rank) c.owned.push_back(j);
+        c.owns_u0 = has_u0 && owner[0] == rank;
+        c.first = c.owned.empty() ? 0 : c.owned.front();
+        c.last = c.owned.empty() ? -1 : c.owned.back();
+    } else {
+        std::vector<int> F, L;
+        schedule_blocks(p, world, c.ratio, has_u0, F, L, c.root);
+        c.first = F[rank];
+        c.last = L[rank];
+    }
     S.first_interval = c.first;
     S.last_interval = c.last;
     S.root = c.root;
@@ -1382,6 +1435,86 @@ static int solve_block_dev(Grid &G, const SolveCtx &c, int nsrc, const void *e0,
     return k_check_finite_async(ka, b.W, dflag + p + 1);
 }
 
+// tail_mode EXP_LPT (schedule B, reading 34): this rank's jobs of the paper's literal parfor --
+// for each owned j, v_j by leapfrog from zero, its seed s_j and its OWN tail E_p..E_{j+1} s_j
+// (PAPER:358-365), summed into W; the u0 tail E_p..E_1 u0 if the rank owns job 0.  Same flags
+// and norms as solve_block_dev (the propagator norms accumulate over the rank's tails).
+static int solve_block_lpt_dev(Grid &G, const SolveCtx &c, int nsrc, const void *e0, const void *h0,
+                               const KernelArgs &ka, Events &ev, paraexp_stats &S, SolveBufs &b,
+                               bool &host_io) {
+    const NanHook hook;
+    const int p = c.p;
+    void *stream = ka.stream;
+    const size_t sbytes = (size_t)G.L.state_elems() * G.esize();
+    int rc;
+    b.P = G.ws[0];
+    b.W = G.ws[1];
+    b.X[0] = G.ws[2];
+    b.X[1] = G.ws[3];
+    b.X[2] = G.ws[4];
+    int *dflag = (int *)G.d_flag;
+    double *norms = (double *)G.d_norms;
+    if ((rc = dev_memset_async(dflag, 0, sizeof(int) * (p + 2), stream))) return rc;
+    if ((rc = dev_memset_async(norms, 0, sizeof(double) * 2 * (p + 1), stream))) return rc;
+    bool W_valid = false;
+    auto propagate = [&](int i) -> int {              // P <- E_i P
+        nvtxRangePushA("propagate");
+        int r = PARAEXP_OK;
+        if (c.rho_check) r = k_dot_M_async(ka, b.P, b.P, norms + 2 * i, G.dt);
+        if (!r) {
+            void *bufs[4] = {b.P, b.X[0], b.X[1], b.X[2]};
+            r = run_plan(ka, c.plans.at(c.B[i] - c.B[i - 1]), bufs, &S, &ev);
+            b.P = bufs[0];
+            b.X[0] = bufs[1];
+            b.X[1] = bufs[2];
+            b.X[2] = bufs[3];
+        }
+        if (!r && hook.tail == i) r = inject_nan(G, b.P, stream);
+        if (!r) r = k_dot_M_async(ka, b.P, b.P, norms + 2 * i + 1, G.dt);
+        nvtxRangePop();
+        return r;
+    };
+    auto add_to_W = [&]() -> int {
+        if (W_valid) return k_axpy(ka, b.W, b.P, 1.0);
+        W_valid = true;
+        return dev_memcpy_d2d_async(b.W, b.P, sbytes, stream);
+    };
+    if (c.owns_u0) {                                   // job 0: E_p..E_1 u0
+        const int id = ev.open(1);
+        if ((rc = pack_any(ka, G, e0, h0, b.P, &host_io))) return rc;
+        for (int i = 1; i <= p; ++i)
+            if ((rc = propagate(i))) return rc;
+        if ((rc = add_to_W())) return rc;
+        ev.close(id);
+    }
+    for (int j : c.owned) {
+        const int64_t M = c.B[j] - c.B[j - 1];
+        int id = ev.open(0);
+        if ((rc = dev_memset_async(b.P, 0, sbytes, stream))) return rc;
+        void *bufs[2] = {b.P, b.X[0]};
+        const size_t qoff = (size_t)c.B[j - 1] * nsrc * G.esize();
+        const int id5 = ev.open(5);
+        if ((rc = k_leapfrog(ka, bufs, M, (const SrcDev *)G.d_src, nsrc, (const char *)G.d_q + qoff))) return rc;
+        ev.close(id5);
+        if (bufs[0] != b.P) std::swap(b.P, b.X[0]);
+        S.leapfrog_steps += M;
+        S.curl_applications += 2 * M;
+        if (hook.particular == j && (rc = inject_nan(G, b.P, stream))) return rc;
+        if ((rc = k_check_finite_async(ka, b.P, dflag + j))) return rc;
+        ev.close(id);
+        if (j < p) {                                   // seed and its own tail to T_p
+            id = ev.open(1);
+            if ((rc = k_sync(ka, b.P))) return rc;
+            for (int i = j + 1; i <= p; ++i)
+                if ((rc = propagate(i))) return rc;
+            if ((rc = add_to_W())) return rc;
+            ev.close(id);
+        }
+    }
+    if (!W_valid && (rc = dev_memset_async(b.W, 0, sbytes, stream))) return rc;
+    return k_check_finite_async(ka, b.W, dflag + p + 1);
+}
+
 // Read back the block's device flags and propagator norms (synchronises `stream`).
 // Returns EDIVERGED / EOVERFLOW naming the first failing sub-interval, or sets *violation when
 // a propagator changed the energy norm by more than its tolerance (rho too small: the
@@ -1401,7 +1534,9 @@ static int block_status(const Grid &G, const SolveCtx &c, void *stream, paraexp_
         }
     *violation = false;
     *max_dev = 0;
-    const int fprop = c.first >= 1 ? (c.first == 1 && c.has_u0 ? 1 : c.first + 1) : p + 1;
+    // first propagator this rank applied (Horner: from its block's start; LPT: its first tail)
+    int fprop = c.first >= 1 ? (c.first == 1 && c.has_u0 ? 1 : c.first + 1) : p + 1;
+    if (c.tail_mode == PARAEXP_TAIL_EXP_LPT) fprop = c.owns_u0 ? 1 : (c.first >= 1 ? c.first + 1 : p + 1);
     for (int i = fprop; i <= p; ++i) {
         const double after = nrm[2 * i + 1];
         if (!std::isfinite(after)) {
@@ -1434,7 +1569,9 @@ static int solve_block_checked(Grid &G, SolveCtx &c, int nsrc, const void *e0, c
     int rc;
     nvtxRangePushA("paraexp_block");
     for (int attempt = 0; attempt < 2; ++attempt) {
-        if ((rc = solve_block_dev(G, c, nsrc, e0, h0, tr, ka, ev, S, b, host_io))) break;
+        rc = c.tail_mode == PARAEXP_TAIL_EXP_LPT ? solve_block_lpt_dev(G, c, nsrc, e0, h0, ka, ev, S, b, host_io)
+                                                 : solve_block_dev(G, c, nsrc, e0, h0, tr, ka, ev, S, b, host_io);
+        if (rc) break;
         bool viol = false;
         double dev = 0;
         if ((rc = block_status(G, c, ka.stream, S, &viol, &dev))) break;
@@ -1463,7 +1600,7 @@ static int solve_finish_dev(Grid &G, const SolveCtx &c, const KernelArgs &ka, Ev
     struct Pop {
         ~Pop() { nvtxRangePop(); }
     } pop;
-    if (c.tail_mode == PARAEXP_TAIL_EXP) {
+    if (c.exp_tails()) {
         if ((rc = k_axpy_comps(ka, b.P, b.W, 1.0, 0, 3))) return rc;       // e_out = e_p + W_e
         void *bufs[4] = {b.W, b.X[0], b.X[1], b.X[2]};
         if ((rc = run_plan(ka, c.half, bufs, nullptr, &ev))) return rc;     // exp(dt/2 A) W
@@ -1652,7 +1789,8 @@ int paraexp_solve_finish(paraexp_grid *grid, const paraexp_expmv_opts *opts, int
     Grid &G = grid->g;
     if (G.device < 0) return fail(PARAEXP_ENOTSUP, "host-only grid");
     if (!w_e || !w_h || !v_e || !v_h || !e_out || !h_out) return fail(PARAEXP_EINVAL, "null field pointer");
-    if (tail_mode != PARAEXP_TAIL_EXP && tail_mode != PARAEXP_TAIL_LEAPFROG) return fail(PARAEXP_EINVAL, "bad tail mode");
+    if (tail_mode != PARAEXP_TAIL_EXP && tail_mode != PARAEXP_TAIL_LEAPFROG && tail_mode != PARAEXP_TAIL_EXP_LPT)
+        return fail(PARAEXP_EINVAL, "bad tail mode");
     paraexp_stats local{};
     paraexp_stats &S = st ? *st : local;
     S = paraexp_stats();

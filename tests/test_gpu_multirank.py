@@ -58,7 +58,9 @@ def _virtual_solve(lg, world, p, src, u0, rho, tail_mode="exp"):
             owned += list(range(st["first_interval"], st["last_interval"] + 1))
         We += w[0]
         Wh += w[1]
-    assert sorted(owned) == list(range(1, p + 1)) and len(roots) == 1
+    assert len(roots) == 1
+    if tail_mode != "exp_lpt":                 # contiguous blocks cover 1..p exactly once
+        assert sorted(owned) == list(range(1, p + 1))
     eo, ho = z(), z()
     pe.solve_finish(lg, (We, Wh), v, eo, ho, rho=rho, tail_mode=tail_mode)
     torch.cuda.synchronize()
@@ -77,6 +79,24 @@ def test_virtual_ranks_match_oracle(dtype, p):
         assert_parity(got, ref, dtype, f"world={world} p={p}")
         ee, eh = (np.abs(g - r).max() / np.abs(r).max() for g, r in zip(got, ref))
         assert ee <= 10 * TOL[dtype] and eh <= 10 * TOL[dtype], (world, p, ee, eh)   # max-abs
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("p", [5, 8])
+def test_lpt_independent_tails_match_oracle(dtype, p):
+    """Schedule (B): independent tails assigned longest-processing-time-first (tail_mode
+    EXP_LPT) -- virtual ranks and the single-GPU solve against the oracle's independent-tail
+    sum (a different association from Horner's)."""
+    og, lg, src, u0 = _setup(dtype)
+    rho = og.rho_cfl
+    ref = fit.paraexp(og, src, 0.0, NSTEPS, p, lambda tau: fit.make_plan("leja", M_FIX, S_FIX, tau, rho),
+                      u0=u0, rho=rho, dtype=dtype, sum_mode="independent")
+    for world in (1, 2, 3, 8):
+        got = _virtual_solve(lg, world, p, src, u0, rho, tail_mode="exp_lpt")
+        assert_parity(got, ref, dtype, f"LPT world={world} p={p}")
+    got = lib_solve(lg, NSTEPS, p, src, u0=u0, m=M_FIX, s=S_FIX, rho=rho, tail_mode="exp_lpt")
+    assert_parity(got[:2], ref, dtype, f"LPT solve p={p}")
+    assert got[2]["a_applications"] >= (p - 1) * p // 2 * M_FIX * S_FIX   # sum_j (p - j) propagators
 
 
 def test_virtual_ranks_leapfrog_tails_equal_serial_leapfrog():

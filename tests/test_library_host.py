@@ -93,6 +93,27 @@ def test_cost_balanced_schedule_is_optimal(ratio, u0):
             assert ms <= _makespan([(f, l) for f, l, _ in eq if f >= 1], p, ratio, u0) + 1e-9
 
 
+@pytest.mark.parametrize("ratio", [0.5, 2.6, 16.0])
+@pytest.mark.parametrize("u0", [False, True])
+def test_lpt_schedule(ratio, u0):
+    """Schedule (B) (paraexp_schedule_lpt): every job exactly once, the root owns
+    sub-interval p, and the makespan obeys Graham's LPT bound (4/3 - 1/(3 world)) x the lower
+    bound max(total / world, largest job)."""
+    for p in (1, 2, 5, 8, 17, 64):
+        for world in (1, 2, 3, 8):
+            owner, root = pe.schedule_lpt(p, world, ratio, u0)
+            assert len(owner) == p + 1 and root == owner[p]
+            assert (owner[0] == -1) != u0 and all(0 <= o < world for o in owner[1:])
+            cost = {j: 1.0 + (p - j) * ratio for j in range(1, p + 1)}
+            if u0:
+                cost[0] = p * ratio
+            load = [0.0] * world
+            for j, c in cost.items():
+                load[owner[j]] += c
+            lb = max(sum(cost.values()) / world, max(cost.values()))
+            assert max(load) <= (4.0 / 3.0 - 1.0 / (3 * world)) * lb + 1e-9, (p, world, load, lb)
+
+
 def test_leja_points_match_oracle():
     assert pe.leja_points(101) == list(fit.leja_points(101))
 
