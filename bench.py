@@ -247,6 +247,8 @@ def main():
     ap.add_argument("--no-serial", action="store_true")
     ap.add_argument("--p", type=int, default=0, help="override the workload's sub-interval count")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e pass (secondary lines)")
+    ap.add_argument("--tail-mode", default="exp", choices=["exp", "exp_lpt"],
+                    help="schedule (A) blocks + Horner tails (default) or (B) independent tails, LPT")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -287,7 +289,8 @@ def main():
     tdt = grid.torch_dtype()
     e_out = torch.zeros(3 * grid.npts, dtype=tdt, device=f"cuda:{local}")
     h_out = torch.zeros_like(e_out)
-    kw = dict(sources=w.sources, method=w.method, m=w.m, s=w.s, eps_A=w.eps_A, comm=comm)
+    kw = dict(sources=w.sources, method=w.method, m=w.m, s=w.s, eps_A=w.eps_A, comm=comm,
+              tail_mode=args.tail_mode)
     u0 = None
     if w.u0_seed is not None:
         import numpy as np
@@ -433,6 +436,7 @@ def main():
                    "nsteps": w.nsteps, "p": w.p, "method": w.method, "eps_A": w.eps_A,
                    "rho": stats[-1]["rho"], "m": stats[-1]["m"], "s_per_subinterval": stats[-1]["s_first"],
                    "material_mode": info["material_mode"], "kernels": args.kernels,
+                   "schedule": "blocks+horner" if args.tail_mode == "exp" else "independent tails, LPT",
                    "parallelism": f"paraexp time-parallel x{world}",
                    "l2": (f"inputs larger than L2 ({6 * w.cells * es / 1e6:.0f} MB per state vector "
                           f"vs 126 MB L2), no flush" if 6 * w.cells * es > 126e6 else

@@ -174,3 +174,20 @@ def test_c_example_runs(tmp_path):
     assert out.returncode == 0, out.stderr
     rel = float(re.search(r"= ([0-9.e+-]+)\s*$", out.stdout.strip()).group(1))
     assert 0 < rel < 2.0, out.stdout
+
+
+@pytest.mark.parametrize("world", [1, 3, 8])
+def test_c_ranks_example(tmp_path, world):
+    """examples/ranks_solve.c: paraexp_solve_block per (simulated) rank into HOST buffers, a host
+    sum, paraexp_solve_finish -- equals the one-call paraexp_solve to summation order."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_1705_08019_b200")
+    exe = tmp_path / "ranks_solve"
+    subprocess.check_call(["gcc", "-std=c11", "-O2", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "examples", "ranks_solve.c"), "-L", libdir,
+                           "-l:libparaexp.so", f"-Wl,-rpath,{libdir}", "-lm", "-o", str(exe)])
+    out = subprocess.run([str(exe), str(world)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.count("rank ") == world

@@ -7,7 +7,9 @@ and timed with CUDA events on the launching stream; the modelled wall time is
 
 with T_finish measured (paraexp_solve_finish on the root) and T_reduce = bytes of W / the
 measured 8-rank all-reduce bus bandwidth of this pool (725 GB/s, B200_PROFILING.md; a reduce
-moves at most that).  The G = 1 row is the measured single-GPU solve.  Printed as JSON lines.
+moves at most that).  The G = 1 row is the measured single-GPU solve.  Both schedules of
+SURVEY 8(e): (A) cost-balanced contiguous blocks with Horner tails (the default) and (B)
+independent tails, longest-processing-time-first (tail_mode EXP_LPT).  Printed as JSON lines.
 Usage: python tools/model_scaling.py [workload] [p ...]   (default c3 8 64)"""
 import json
 import os
@@ -49,13 +51,14 @@ def main():
         serial = s0.elapsed_time(s1)
         print(json.dumps({"workload": w.name, "p": p, "G": 1, "kind": "measured", "wall_ms": st1["ms_total"],
                           "serial_leapfrog_ms": serial, "speedup": serial / st1["ms_total"]}), flush=True)
-        for G in (2, 4, 8):
+        for G, sched in [(g_, sc) for sc in ("blocks", "lpt") for g_ in (2, 4, 8)]:
+            tm = "exp" if sched == "blocks" else "exp_lpt"
             blocks = []
             v = (z(), z())
             We, Wh = z(), z()
             for r in range(G):
                 wv = (z(), z())
-                st = pe.solve_block(g, r, G, w.nsteps, p, wv, rho=rho, v=v, **kw)
+                st = pe.solve_block(g, r, G, w.nsteps, p, wv, rho=rho, v=v, tail_mode=tm, **kw)
                 blocks.append({"rank": r, "first": st["first_interval"], "last": st["last_interval"],
                                "ms": st["ms_total"], "leapfrog_steps": st["leapfrog_steps"],
                                "a_applications": st["a_applications"]})
@@ -65,7 +68,7 @@ def main():
             t_red = wbytes / (BUS_GBS * 1e9) * 1e3
             crit = max(b["ms"] for b in blocks)
             wall = crit + t_red + fin["ms_total"]
-            print(json.dumps({"workload": w.name, "p": p, "G": G, "kind": "model", "wall_ms": wall,
+            print(json.dumps({"workload": w.name, "p": p, "G": G, "kind": "model", "schedule": sched, "wall_ms": wall,
                               "critical_block_ms": crit, "reduce_ms_model": t_red, "finish_ms": fin["ms_total"],
                               "serial_leapfrog_ms": serial, "speedup": serial / wall, "blocks": blocks,
                               "rho": rho, "rho_pow": info["rho_pow"]}), flush=True)
