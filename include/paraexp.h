@@ -303,8 +303,10 @@ void paraexp_comm_destroy(paraexp_comm *comm);
  *   e_out, h_out  device, canonical; written on the root, or on every rank when
  *            broadcast_out != 0 (one ncclBroadcast).  Output convention equals
  *            paraexp_leapfrog from (e0, h0 - cH/2 C e0): (e^(n), h^(n+1/2)).
- * With a communicator the call waits for its stream while polling ncclCommGetAsyncError
- * (a failed peer => the communicator is aborted, ENCCL).
+ * With a communicator the ranks all-reduce their blocks' status before the reduce (a rank
+ * whose block failed makes every rank return: EDIVERGED "another rank's block failed" on
+ * the others), and the call waits for its stream while polling ncclCommGetAsyncError (a
+ * failed peer => the communicator is aborted, ENCCL).
  * Errors: EINVAL (p < 1, nsteps < p), ENOTSUP, EDIVERGED (particular sweep of
  *         stats.fail_interval non-finite) / EOVERFLOW (propagator E_{fail_interval}
  *         produced a non-finite field), ENCCL, ECUDA.  Synchronises `stream` before

@@ -750,6 +750,22 @@ int comm_allreduce_trace(paraexp_comm *comm, const pe::TraceDev &tr, int p, void
     return rc;
 }
 
+// max over ranks of a local failure flag (one int, ncclAllReduce max): returns 1 if any rank
+// failed, 0 if none, or a negative error code if the collective itself failed
+int comm_status_any(paraexp_comm *comm, const pe::Grid &G, bool failed, void *stream) {
+    const int kNcclInt32 = 2, kNcclMax = 2;
+    int *d = (int *)G.d_flag + 1020;               // past the per-sub-interval flags (p <= 1000)
+    const int v = failed ? 1 : 0;
+    int rc = pe::dev_memcpy_h2d_async(d, &v, sizeof(int), stream);
+    if (rc) return rc;
+    if ((rc = nccl_check(g_nccl.AllReduce(d, d, 1, kNcclInt32, kNcclMax, comm->comm, (cudaStream_t)stream),
+                         "ncclAllReduce(status)"))) return rc;
+    if ((rc = comm_wait(comm, stream))) return rc;
+    int any = 0;
+    if ((rc = pe::dev_memcpy_d2h(&any, d, sizeof(int), stream))) return rc;
+    return any;
+}
+
 int comm_bcast_state(paraexp_comm *comm, const pe::Grid &G, void *P, int root, void *stream) {
     const int dt = G.dtype == PARAEXP_F64 ? kNcclF64 : kNcclF32;
     return nccl_check(g_nccl.Broadcast(P, P, (size_t)G.L.state_elems(), dt, root, comm->comm,
@@ -1706,7 +1722,17 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
     const int idt = ev.open(4);
     bool host_io = false;       // host-pointer fields (staged copies; the call syncs anyway)
     SolveBufs b;
-    if ((rc = solve_block_checked(G, c, nsrc, e0, h0, tr, ka, ev, S, b, host_io))) return rc;
+    rc = solve_block_checked(G, c, nsrc, e0, h0, tr, ka, ev, S, b, host_io);
+    // the ranks agree on the blocks' status before the reduce: a rank whose block failed
+    // (divergence, overflow, allocation) would otherwise leave its peers waiting in ncclReduce
+    if (coll) {
+        const int rc2 = comm_status_any(comm, G, rc != PARAEXP_OK, stream);
+        if (rc) return rc;
+        if (rc2 < 0) return rc2;
+        if (rc2 > 0) return fail(PARAEXP_EDIVERGED, "another rank's block failed (status all-reduce)");
+    } else if (rc) {
+        return rc;
+    }
 
     // a8: sum the tails onto the root
     if (coll) {

@@ -256,3 +256,25 @@ def test_calls_on_different_streams_are_ordered():
     pe.expmv(lg, 30 * og.dt, te, th, m=M_FIX, s=3, rho=og.rho_cfl, stream=s2.cuda_stream)
     torch.cuda.synchronize()
     assert_parity((to_host(te), to_host(th)), ref, "f64", "two streams")
+
+
+def test_failed_block_reported_through_the_status_allreduce(monkeypatch):
+    """With a communicator, the ranks all-reduce their blocks' status before the W reduce (a
+    failed rank would otherwise leave its peers waiting in ncclReduce): a one-rank NCCL
+    communicator with the collectives forced on still reports the divergence and its
+    sub-interval, and the communicator stays usable."""
+    og, lg, src, u0 = _setup("f64")
+    monkeypatch.setenv("PARAEXP_FORCE_COLLECTIVES", "1")
+    comm = pe.Comm(0, 1, 0, id_bytes=pe.Comm.unique_id())
+    try:
+        monkeypatch.setenv("PARAEXP_DEBUG_NAN", "particular:2")
+        with pytest.raises(pe.ParaexpError) as ei:
+            lib_solve(lg, 60, 6, src, u0=u0, m=M_FIX, s=S_FIX, rho=og.rho_cfl, comm=comm)
+        assert ei.value.code == pe.EDIVERGED and ei.value.stats["fail_interval"] == 2
+        monkeypatch.delenv("PARAEXP_DEBUG_NAN")
+        got = lib_solve(lg, 60, 6, src, u0=u0, m=M_FIX, s=S_FIX, rho=og.rho_cfl, comm=comm)
+        ref = fit.paraexp(og, src, 0.0, 60, 6, lambda tau: fit.make_plan("leja", M_FIX, S_FIX, tau, og.rho_cfl),
+                          u0=u0, rho=og.rho_cfl)
+        assert_parity(got[:2], ref, "f64", "after a failed solve")
+    finally:
+        comm.close()
