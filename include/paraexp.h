@@ -298,7 +298,13 @@ void paraexp_comm_destroy(paraexp_comm *comm);
  *      e_out = e_p + W_e,   h_out = h_p + [exp(dt/2 A) W]_h.
  * = paraexp_solve_block on every rank, a sum of the blocks' W, paraexp_solve_finish on the
  * root.  tail_mode PARAEXP_TAIL_LEAPFROG propagates the staggered seeds with leapfrog
- * instead (debug identity: equals serial leapfrog).
+ * instead (debug identity: equals serial leapfrog).  tail_mode
+ * PARAEXP_TAIL_EXP_LPT is schedule (B) of SURVEY 8(e), kept as a comparison: the paper's
+ * literal structure, one independent exp tail per sub-interval (E_p..E_{j+1} s_j, and
+ * E_p..E_1 u0 as a job of its own), jobs assigned longest-processing-time-first
+ * (paraexp_schedule_lpt); the result equals EXP's up to summation order, with
+ * sum_j (p - j) propagators of work instead of Horner's at most p per rank.  Traces need
+ * tail_mode EXP.
  *   e0, h0   same-time initial value u0 at t0 (device, canonical) or NULL => 0
  *   e_out, h_out  device, canonical; written on the root, or on every rank when
  *            broadcast_out != 0 (one ncclBroadcast).  Output convention equals
@@ -321,7 +327,8 @@ int paraexp_solve(paraexp_grid *grid, paraexp_comm *comm, const paraexp_source *
  * PAPER:358-365 for the block paraexp_schedule gives `rank` of `world`), for callers that
  * sum the blocks themselves (MPI, gloo, or several virtual ranks on one GPU).
  *   w_e, w_h  out (device or host, canonical): this rank's tails carried to T_p,
- *            W_rank = sum_{owned j < p} E_p..E_{j+1} s_j (+ E_p..E_1 u0 if it owns j = 1);
+ *            W_rank = sum_{owned j < p} E_p..E_{j+1} s_j (+ E_p..E_1 u0 if it owns j = 1,
+ *            or job 0 under PARAEXP_TAIL_EXP_LPT);
  *            zero if the rank owns no sub-interval.  The sum of W_rank over ranks is the
  *            W that paraexp_solve reduces.
  *   v_e, v_h  out on the root only (stats.root == rank; may be NULL elsewhere): the
