@@ -65,7 +65,8 @@ enum { PARAEXP_SRC_ZERO = 0, PARAEXP_SRC_GAUSS_PAPER = 1, PARAEXP_SRC_GAUSS_SINE
 enum { PARAEXP_TAYLOR = 0, PARAEXP_LEJA = 1, PARAEXP_KRYLOV = 2 };
 enum { PARAEXP_TAIL_EXP = 0, PARAEXP_TAIL_LEAPFROG = 1, PARAEXP_TAIL_EXP_LPT = 2 };
 enum { PARAEXP_MAT_SCALAR = 0, PARAEXP_MAT_ZTABLE = 1, PARAEXP_MAT_ARRAY = 2 };
-enum { PARAEXP_KERNELS_AUTO = 0, PARAEXP_KERNELS_UNFUSED = 1, PARAEXP_KERNELS_FUSED = 2 };
+enum { PARAEXP_KERNELS_AUTO = 0, PARAEXP_KERNELS_UNFUSED = 1, PARAEXP_KERNELS_FUSED = 2,
+       PARAEXP_KERNELS_TMA = 3 };
 
 #define PARAEXP_MAX_DEGREE 150
 #define PARAEXP_MAX_SOURCES 64
@@ -83,8 +84,12 @@ enum { PARAEXP_KERNELS_AUTO = 0, PARAEXP_KERNELS_UNFUSED = 1, PARAEXP_KERNELS_FU
  *   dt, dt_frac exactly one > 0: explicit time step in seconds, or a fraction of the
  *               eq:cfl bound dt_CFL.  dt is a grid property: it is baked
  *               into cE = dt*M_eps^-1 and cH = dt*M_nu (reading 24)
- *   kernels     PARAEXP_KERNELS_AUTO (fused z-marching kernels), _UNFUSED (one kernel
- *               per curl half; debugging/parity baseline) or _FUSED
+ *   kernels     PARAEXP_KERNELS_AUTO = _FUSED: the fused kernels chosen by size -- one CTA
+ *               with the state in shared memory (<= 2048 cells fp64 / 4096 fp32), one
+ *               cooperative launch with the state resident in the shared memory of up to
+ *               one CTA per SM (mid-size grids, <= #SMs x 2048 / 4096 cells), else the TMA
+ *               z-marching kernels; _TMA: the TMA z-marching kernels at every size;
+ *               _UNFUSED: one kernel per curl half (debugging / parity baseline)
  * All input arrays are host pointers, read during the call only. */
 typedef struct {
     int32_t nx, ny, nz;

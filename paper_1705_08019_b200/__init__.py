@@ -13,7 +13,7 @@ from typing import Iterable, Optional, Sequence
 import numpy as np
 
 from . import abi
-from .abi import (EDIVERGED, EINVAL, ENOTSUP, EOVERFLOW, F32, F64, KERNELS_AUTO, KERNELS_FUSED,  # noqa
+from .abi import (EDIVERGED, EINVAL, ENOTSUP, EOVERFLOW, F32, F64, KERNELS_AUTO, KERNELS_FUSED, KERNELS_TMA,  # noqa
                   KERNELS_UNFUSED, KRYLOV, LEJA, TAIL_EXP, TAIL_EXP_LPT, TAIL_LEAPFROG, TAYLOR, ParaexpError,
                   check)
 
@@ -24,7 +24,7 @@ __all__ = ["Grid", "Comm", "leapfrog", "leapfrog_trace", "expmv", "expmv_plan", 
            "leja_points", "plan_host", "theta", "version", "make_sources", "ParaexpError"]
 
 _DT = {"f64": F64, "f32": F32}
-_KER = {"auto": KERNELS_AUTO, "unfused": KERNELS_UNFUSED, "fused": KERNELS_FUSED}
+_KER = {"auto": KERNELS_AUTO, "unfused": KERNELS_UNFUSED, "fused": KERNELS_FUSED, "tma": KERNELS_TMA}
 _SRC_KIND = {"zero": 0, "gauss_paper": 1, "gauss_sine": 2, "sine": 3}
 _METHOD = {"taylor": TAYLOR, "leja": LEJA, "krylov": KRYLOV}
 _METHOD_NAME = {v: k for k, v in _METHOD.items()}

@@ -27,7 +27,7 @@ SRC_ZERO, SRC_GAUSS_PAPER, SRC_GAUSS_SINE, SRC_SINE = 0, 1, 2, 3
 TAYLOR, LEJA, KRYLOV = 0, 1, 2
 TAIL_EXP, TAIL_LEAPFROG, TAIL_EXP_LPT = 0, 1, 2
 MAT_SCALAR, MAT_ZTABLE, MAT_ARRAY = 0, 1, 2
-KERNELS_AUTO, KERNELS_UNFUSED, KERNELS_FUSED = 0, 1, 2
+KERNELS_AUTO, KERNELS_UNFUSED, KERNELS_FUSED, KERNELS_TMA = 0, 1, 2, 3
 MAX_DEGREE = 150
 MAX_PROBES = 16
 

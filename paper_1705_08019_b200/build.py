@@ -24,7 +24,7 @@ CUFLAGS = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2",
                   "-I" + os.path.join(HERE, "..", "include")]
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-I/usr/local/cuda/include",
             "-I" + os.path.join(HERE, "..", "include")]
-SOURCES = ["kernels.cu", "fused.cu", "small.cu", "grid.cpp", "plan.cpp", "api.cpp"]
+SOURCES = ["kernels.cu", "fused.cu", "small.cu", "mid.cu", "grid.cpp", "plan.cpp", "api.cpp"]
 HEADERS = ["internal.h", "kernels_common.cuh", "../../include/paraexp.h"]
 
 

@@ -311,7 +311,11 @@ int k_leapfrog(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev
     const bool tracing = tr && (tr->energy || (tr->probe && tr->np > 0));
     if (ka.g->kernels == PARAEXP_KERNELS_FUSED && !tracing && nsrc <= 16 && small_supported(*ka.g))
         return k_leapfrog_small(ka, bufs[0], nsteps, nsrc, q_dev);
-    if (ka.g->kernels == PARAEXP_KERNELS_FUSED && fused_supported(*ka.g))
+    // mid-size grids: one cooperative launch over all SMs (never for concurrently swept
+    // sub-intervals: the launch needs the whole GPU and the grid's exchange buffer)
+    if (ka.g->kernels == PARAEXP_KERNELS_FUSED && !tracing && nsrc <= 16 && !ka.static_sched && mid_supported(*ka.g))
+        return k_leapfrog_mid(ka, bufs[0], nsteps, nsrc, q_dev);
+    if (zmarch_kernels(*ka.g) && fused_supported(*ka.g))
         return k_leapfrog_fused(ka, bufs, nsteps, src_dev, nsrc, q_dev, tr);
     return k_leapfrog_unfused(ka, bufs[0], nsteps, src_dev, nsrc, q_dev, tr);
 }
@@ -341,7 +345,7 @@ static int prepare_trace(const Grid &G, const paraexp_trace *t, TraceDev &tr) {
     return PARAEXP_OK;
 }
 int k_poly_substep(const KernelArgs &ka, const Plan &plan, void *bufs[4]) {
-    if (ka.g->kernels == PARAEXP_KERNELS_FUSED && fused_supported(*ka.g))
+    if (zmarch_kernels(*ka.g) && fused_supported(*ka.g))
         return k_poly_substep_fused(ka, plan, bufs);
     return k_poly_substep_unfused(ka, plan, bufs);
 }

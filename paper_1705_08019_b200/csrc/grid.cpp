@@ -238,6 +238,10 @@ void grid_free_device(Grid &G) {
     G.events.clear();
     dev_free(G.d_sched);
     G.d_sched = nullptr;
+    dev_free(G.d_mid);
+    G.d_mid = nullptr;
+    G.mid_bytes = 0;
+    G.mid_tag = 0;
     dev_free(G.d_norms);
     G.d_norms = nullptr;
     if (G.call_event) dev_event_destroy(G.call_event);
@@ -260,7 +264,7 @@ int grid_create(const paraexp_grid_desc *d, paraexp_grid **out) {
     if (d->dtype != PARAEXP_F64 && d->dtype != PARAEXP_F32) return fail(PARAEXP_EINVAL, "bad dtype");
     if (!d->dx || !d->dy || !d->dz)
         if (!(d->d0 > 0) || !std::isfinite(d->d0)) return fail(PARAEXP_EINVAL, "d0 must be > 0 when spacings are NULL");
-    if (d->kernels < 0 || d->kernels > 2) return fail(PARAEXP_EINVAL, "bad kernels selector");
+    if (d->kernels < 0 || d->kernels > 3) return fail(PARAEXP_EINVAL, "bad kernels selector");
     const int64_t cells = (int64_t)d->nx * d->ny * d->nz;
     if (cells > (int64_t)1 << 33) return fail(PARAEXP_EINVAL, "grid too large");
     paraexp_grid *pg = new (std::nothrow) paraexp_grid();
@@ -284,7 +288,9 @@ int grid_create(const paraexp_grid_desc *d, paraexp_grid **out) {
     G.L.px = (G.nx + align - 1) / align * align;
     G.L.plane = G.L.px * G.ny;
     G.L.cs = G.L.plane * G.nz;
-    G.kernels = d->kernels == PARAEXP_KERNELS_UNFUSED ? PARAEXP_KERNELS_UNFUSED : PARAEXP_KERNELS_FUSED;
+    G.kernels = d->kernels == PARAEXP_KERNELS_UNFUSED ? PARAEXP_KERNELS_UNFUSED
+                : d->kernels == PARAEXP_KERNELS_TMA     ? PARAEXP_KERNELS_TMA
+                                                        : PARAEXP_KERNELS_FUSED;
     if (G.device >= 0) {
         if ((rc = dev_set_device(G.device))) {
             delete pg;

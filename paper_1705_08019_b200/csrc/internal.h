@@ -68,6 +68,9 @@ struct Grid {
     void *d_norms = nullptr;    // per-propagator energy norms of a solve (rho safety net, f. intervals)
     void *call_event = nullptr; // recorded at the end of every call (stream order across calls)
     void *call_stream = nullptr;
+    void *d_mid = nullptr;      // mid.cu: tagged face-exchange lines of the resident kernels
+    int64_t mid_bytes = 0;
+    uint32_t mid_tag = 0;       // next epoch-tag base of a mid launch (0: buffer not zeroed yet)
     void *d_sched = nullptr;    // monotone unit counter of the fused kernels' dynamic schedule
     unsigned long long sched_base = 0;   // host shadow: value of *d_sched before the next launch
     int64_t d_q_cap = 0;
@@ -174,6 +177,14 @@ int k_poly_substep_unfused(const KernelArgs &ka, const Plan &plan, void *bufs[4]
 bool small_supported(const Grid &g);
 int k_leapfrog_small(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc, const void *q_dev);
 int k_poly_small(const KernelArgs &ka, const Plan &plan, void *state);
+// mid-size grids (mid.cu): one cooperative launch per leapfrog sequence, the state resident in
+// the shared memory of up to one CTA per SM, neighbour-only face exchange through L2
+bool mid_supported(const Grid &g);
+int k_leapfrog_mid(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc, const void *q_dev);
+// the TMA z-marching kernels serve this grid (kernels FUSED = auto choice, or TMA only)
+inline bool zmarch_kernels(const Grid &g) {
+    return g.kernels == PARAEXP_KERNELS_FUSED || g.kernels == PARAEXP_KERNELS_TMA;
+}
 // x <- x + alpha y (state-sized), or over components [c0, c1)
 int k_axpy(const KernelArgs &ka, void *x, const void *y, double alpha);
 int k_axpy_comps(const KernelArgs &ka, void *x, const void *y, double alpha, int c0, int c1);

@@ -14,7 +14,7 @@ from synth import (Source, config_c1, config_c2, config_c3, gauss_sine, layered_
                    spiral_pec_cells)
 
 pytestmark = pytest.mark.gpu
-KERNELS = ["unfused", "fused"]
+KERNELS = ["unfused", "fused", "tma"]   # fused = auto choice (small / mid / TMA by size)
 
 
 def _material(kind, n, seed=3):

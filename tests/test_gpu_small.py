@@ -2,7 +2,8 @@
 cells fp64, <= 4096 fp32): one launch per leapfrog sequence and one per polynomial propagator.
 Every material mode (scalar eps, z-table, per-edge eps with interior PEC, non-uniform mesh =
 per-face cH) at and below the size limit, against the oracle at the north_star tolerances; the
-launch counts prove the small path ran.  The same cases with PARAEXP_NO_SMALL=1 run the TMA
+launch counts prove the small path ran.  The same cases with PARAEXP_NO_SMALL=1 (and
+PARAEXP_NO_MID=1, else the mid-size resident leapfrog of mid.cu would take them) run the TMA
 z-marching kernels on the same small grids (subprocess: the switch is read once)."""
 import os
 import subprocess
@@ -93,14 +94,15 @@ def test_small_limits():
     assert_parity((ge, gh), ref, "f64", "17 sources")
     assert st["kernel_launches"] >= 30, st
     lg.close()
-    n = (17, 11, 11)                               # 2057 cells > 2048
+    n = (17, 11, 11)                               # 2057 cells > 2048: the mid kernel (mid.cu)
     og = fit.Grid(*n, d0=1e-3, dt_frac=0.95)
-    lg = pe.Grid(*n, d0=1e-3, dt_frac=0.95)
     e, h = inputs(og, *random_fields(*n, seed=9))
-    ge, gh, st = lib_leapfrog(lg, e, h, 30, [])
-    assert_parity((ge, gh), fit.leapfrog(og, e, h, 30, []), "f64", "2057 cells")
-    assert st["kernel_launches"] >= 30, st
-    lg.close()
+    for kernels, many in (("auto", False), ("tma", True)):
+        lg = pe.Grid(*n, d0=1e-3, dt_frac=0.95, kernels=kernels)
+        ge, gh, st = lib_leapfrog(lg, e, h, 30, [])
+        assert_parity((ge, gh), fit.leapfrog(og, e, h, 30, []), "f64", f"2057 cells {kernels}")
+        assert (st["kernel_launches"] >= 30) == many, st
+        lg.close()
 
 
 SNIPPET = r'''
@@ -114,7 +116,7 @@ print("no-small ok")
 
 
 def test_no_small_parity():
-    env = dict(os.environ, PARAEXP_NO_SMALL="1")
+    env = dict(os.environ, PARAEXP_NO_SMALL="1", PARAEXP_NO_MID="1")
     out = subprocess.run([sys.executable, "-c", SNIPPET.format(root=ROOT)], env=env,
                          capture_output=True, text=True, timeout=800)
     assert out.returncode == 0 and "no-small ok" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]
