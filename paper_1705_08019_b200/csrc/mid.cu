@@ -41,6 +41,7 @@
 #include <cstdio>
 #include <map>
 #include <mutex>
+#include <type_traits>
 
 #include "internal.h"
 #include "kernels_common.cuh"
@@ -154,6 +155,7 @@ __device__ __forceinline__ MidCell mid_cell(const Dev<T> &D, const MidBox &b, in
     }
     MidCell c;
     c.x = i + D.nx * (jj + by * kk);
+    PE_CHECK(jj >= 0 && jj < by && kk >= 0 && kk < bz && c.x < b.nl, "mid cell slot");
     const int j = b.j0 + jj, k = b.k0 + kk;
     g = (int)D.idx(i, j, k);
     c.f = (unsigned)(i > 0) | ((unsigned)(j > 0) << 1) | ((unsigned)(k > 0) << 2) |
@@ -217,6 +219,7 @@ __device__ __forceinline__ void mid_publish(uint4 *sl, const MidGeo &mg, const M
     const int e3 = e2 + ((hi && b.nb[3] >= 0) ? nk : 0);
     for (int l = threadIdx.x; l < e3; l += kMidThreads) {
         const int r = l < e0 ? 0 : l < e1 ? 1 : l < e2 ? 2 : 3;
+        PE_CHECK(l - (r == 0 ? 0 : r == 1 ? e0 : r == 2 ? e1 : e2) < ((r & 1) ? mg.fk : mg.fj) * L, "mid publish index");
         const int ll = l - (r == 0 ? 0 : r == 1 ? e0 : r == 2 ? e1 : e2);
         const int q = ll / L, part = ll - q * L;
         int x;
@@ -254,6 +257,7 @@ template <typename T>
 __device__ __forceinline__ void put_e_faces(uint4 *sl, const MidGeo &mg, const MidCell &c, T e0, T e1, T e2,
                                             unsigned tag) {
     constexpr int L = mid_lines<T>();
+    PE_CHECK((int)(c.fi & 0xffffu) < mg.fj && (int)(c.fi >> 16) < mg.fk, "mid face index");
     if (c.f & F_RJM) put_pair(sl + region_off<T>(mg, 0) + (int)(c.fi & 0xffffu) * L, e0, e2, tag);
     if (c.f & F_RKM) put_pair(sl + region_off<T>(mg, 1) + (int)(c.fi >> 16) * L, e0, e1, tag);
 }
@@ -320,6 +324,7 @@ __device__ __forceinline__ void mid_stage(const uint4 *xb, const MidGeo &mg, con
             }
             const int ll = l - (r == 0 ? 0 : r == 1 ? e0 : r == 2 ? e1 : e2);
             const int stride = (r & 1) ? mg.fk : mg.fj;
+            PE_CHECK(ll >= 0 && ll < stride * L, "mid halo index");
             T *h = r == 0 ? H.h[0] : r == 1 ? H.h[1] : r == 2 ? H.h[2] : H.h[3];
             if (L == 1) {
                 h[ll] = (T)__uint_as_float(v[u].x);
@@ -335,14 +340,14 @@ __device__ __forceinline__ void mid_stage(const uint4 *xb, const MidGeo &mg, con
 // ---- curls with halo neighbours ---------------------------------------------------------------
 // (C^T h) at an owned cell: the j-1 / k-1 neighbours of box-face cells come from the halos;
 // same operands and order as curlT_at
-template <typename T>
+template <typename T, bool REMOTE = true>
 __device__ __forceinline__ void curlT_mid(const T *hx, const T *hy, const T *hz, const MidCell &c, int nx, int pl,
                                           const Halo<T> &H, int fj, int fk, T &c0, T &c1, T &c2) {
     const int x = c.x;
     const unsigned f = c.f;
     const T hx0 = hx[x], hy0 = hy[x], hz0 = hz[x];
     T hz_jm = T(0), hx_jm = T(0), hy_km = T(0), hx_km = T(0), hz_im = T(0), hy_im = T(0);
-    if (f & F_RJM) {
+    if (REMOTE && (f & F_RJM)) {
         const int q = (int)(c.fi & 0xffffu);
         hx_jm = H.h[0][q];
         hz_jm = H.h[0][fj + q];
@@ -350,7 +355,7 @@ __device__ __forceinline__ void curlT_mid(const T *hx, const T *hy, const T *hz,
         hz_jm = hz[x - nx];
         hx_jm = hx[x - nx];
     }
-    if (f & F_RKM) {
+    if (REMOTE && (f & F_RKM)) {
         const int q = (int)(c.fi >> 16);
         hx_km = H.h[1][q];
         hy_km = H.h[1][fk + q];
@@ -369,14 +374,14 @@ __device__ __forceinline__ void curlT_mid(const T *hx, const T *hy, const T *hz,
 
 // (C e) at an owned cell: the j+1 / k+1 neighbours of box-face cells come from the halos;
 // same operands and order as curl_at
-template <typename T>
+template <typename T, bool REMOTE = true>
 __device__ __forceinline__ void curl_mid(const T *ex, const T *ey, const T *ez, const MidCell &c, int nx, int pl,
                                          const Halo<T> &H, int fj, int fk, T &c0, T &c1, T &c2) {
     const int x = c.x;
     const unsigned f = c.f;
     const T ex0 = ex[x], ey0 = ey[x], ez0 = ez[x];
     T ez_jp = T(0), ex_jp = T(0), ey_kp = T(0), ex_kp = T(0), ez_ip = T(0), ey_ip = T(0);
-    if (f & F_RJP) {
+    if (REMOTE && (f & F_RJP)) {
         const int q = (int)(c.fi & 0xffffu);
         ex_jp = H.h[2][q];
         ez_jp = H.h[2][fj + q];
@@ -384,7 +389,7 @@ __device__ __forceinline__ void curl_mid(const T *ex, const T *ey, const T *ez, 
         ez_jp = ez[x + nx];
         ex_jp = ex[x + nx];
     }
-    if (f & F_RKP) {
+    if (REMOTE && (f & F_RKP)) {
         const int q = (int)(c.fi >> 16);
         ex_kp = H.h[3][q];
         ey_kp = H.h[3][fk + q];
@@ -484,12 +489,12 @@ __global__ void __launch_bounds__(kMidThreads, 1)
     __syncthreads();
     mid_publish(mine, mg, b, nx, S, false, true, tag0);   // epoch 0: the initial h faces
     // per-cell updates; `pub` = publish the cell's faces from registers (face pass)
-    auto e_cell = [&](int r, int64_t m, uint4 *sl, unsigned tag) {
+    auto e_cell = [&](int r, int64_t m, uint4 *sl, unsigned tag, auto remote) {
         const MidCell c = opaque(cl[r]);
         const int x = c.x;
         const unsigned f = c.f;
         T c0, c1, c2;
-        curlT_mid(hx, hy, hz, c, nx, pl, H, mg.fj, mg.fk, c0, c1, c2);
+        curlT_mid<T, decltype(remote)::value>(hx, hy, hz, c, nx, pl, H, mg.fj, mg.fk, c0, c1, c2);
         T e[3] = {ex[x], ey[x], ez[x]};
         const T cc[3] = {c0, c1, c2};
 #pragma unroll
@@ -510,12 +515,12 @@ __global__ void __launch_bounds__(kMidThreads, 1)
         ez[x] = e[2];
         if (sl) put_e_faces(sl, mg, c, e[0], e[1], e[2], tag);
     };
-    auto h_cell = [&](int r, uint4 *sl, unsigned tag) {
+    auto h_cell = [&](int r, uint4 *sl, unsigned tag, auto remote) {
         const MidCell c = opaque(cl[r]);
         const int x = c.x;
         const unsigned f = c.f;
         T c0, c1, c2;
-        curl_mid(ex, ey, ez, c, nx, pl, H, mg.fj, mg.fk, c0, c1, c2);
+        curl_mid<T, decltype(remote)::value>(ex, ey, ez, c, nx, pl, H, mg.fj, mg.fk, c0, c1, c2);
         T h[3] = {hx[x], hy[x], hz[x]};
         const T cc[3] = {c0, c1, c2};
 #pragma unroll
@@ -539,10 +544,10 @@ __global__ void __launch_bounds__(kMidThreads, 1)
             uint4 *sl = mine + (size_t)(t & 1u) * mg.slot;
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (cl[r].x < NL && (cl[r].f & F_FACE)) e_cell(r, m, sl, tag0 + t);
+                if (cl[r].x < NL && (cl[r].f & F_FACE)) e_cell(r, m, sl, tag0 + t, std::true_type{});
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (cl[r].x < NL && !(cl[r].f & F_FACE)) e_cell(r, m, nullptr, 0u);
+                if (cl[r].x < NL && !(cl[r].f & F_FACE)) e_cell(r, m, nullptr, 0u, std::false_type{});
         }
         __syncthreads();
         // ---- h half (epoch t + 1): the upper neighbours' e faces
@@ -552,10 +557,10 @@ __global__ void __launch_bounds__(kMidThreads, 1)
             uint4 *sl = mine + (size_t)((t + 1) & 1u) * mg.slot;
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (cl[r].x < NL && (cl[r].f & F_FACE)) h_cell(r, sl, tag0 + t + 1);
+                if (cl[r].x < NL && (cl[r].f & F_FACE)) h_cell(r, sl, tag0 + t + 1, std::true_type{});
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (cl[r].x < NL && !(cl[r].f & F_FACE)) h_cell(r, nullptr, 0u);
+                if (cl[r].x < NL && !(cl[r].f & F_FACE)) h_cell(r, nullptr, 0u, std::false_type{});
         }
         __syncthreads();
     }

@@ -8,7 +8,9 @@ have left GPUs needing a reset").
   result depend on timing and on the schedule.  So the same leapfrog / expmv / solve runs under
   the default dynamic schedule, the static unit order, two forced z-chunks and plain launches
   without programmatic dependent launch must give bit-identical fields (fp64 and fp32, z-table
-  and per-edge materials, fused TMA kernels and the single-CTA small-grid kernels).
+  and per-edge materials; kernels "auto" -- the mid-size resident leapfrog (its face exchange
+  through tagged L2 lines races if the slot protocol is wrong), the TMA pair kernels and the
+  single-CTA small-grid kernels -- and kernels "tma", the TMA z-marching kernels throughout).
 * The same runs through libparaexp_debug.so (build.py --debug: device-side bounds checks on
   every fused-kernel global store and ring / stage index, and a trap on an mbarrier wait that
   never completes) must finish without a failed check and give the same bits."""
@@ -31,10 +33,10 @@ from synth import layered_eps, random_fields, gauss_sine
 out = []
 cases = [((96, 40, 37), "f64", "z"), ((96, 40, 37), "f32", "z"), ((70, 33, 21), "f64", "a"),
          ((130, 24, 19), "f32", "a"), ((12, 10, 8), "f64", "z")]
-for n, dtype, mat in cases:
+for kern, (n, dtype, mat) in [(k, c) for k in ("auto", "tma") for c in cases]:
     cells = n[0] * n[1] * n[2]
     eps = layered_eps(*n, (1.0, 2.2, 4.4)) if mat == "z" else np.random.default_rng(1).uniform(1, 4, cells)
-    g = pe.Grid(*n, d0=1e-3, eps_r=eps, dt_frac=0.95, dtype=dtype)
+    g = pe.Grid(*n, d0=1e-3, eps_r=eps, dt_frac=0.95, dtype=dtype, kernels=kern)
     td = g.torch_dtype()
     e0, h0 = random_fields(*n, seed=3)
     e = torch.tensor(e0, dtype=td, device="cuda:0"); h = torch.tensor(h0, dtype=td, device="cuda:0")
