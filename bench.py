@@ -39,7 +39,7 @@ FALLBACK_HBM_GBS = 6650.0
 
 
 def workload(name):
-    from synth import config_c1, config_c2, config_c3, config_c4, config_c5, config_c5s, config_wave2d
+    from synth import config_c1, config_c2, config_c3, config_c3r, config_c4, config_c5, config_c5s, config_wave2d
     if name == "c3":
         return config_c3("f64", p=8, nsteps=4096)
     if name == "c3-f32":
@@ -52,6 +52,9 @@ def workload(name):
         return config_c1()
     if name == "c4":
         return config_c4()
+    if name.startswith("c3r-"):           # c3r-<k>[-<n>]: C3 with one refined element (an addition)
+        parts = name.split("-")
+        return config_c3r(k=float(parts[1]), n=int(parts[2]) if len(parts) > 2 else 128)
     if name.startswith("wave2d"):          # wave2d[-k]: the paper's 2-D wave, n_t from T = 2e-7 s
         k = float(name.split("-")[1]) if "-" in name else 1.0
         return config_wave2d(41, k)

@@ -9,6 +9,6 @@ and each derives its own coefficients from them.
 """
 from .configs import (  # noqa: F401
     EPS0, MU0, C0, Z0, Source, Workload, SOURCE_KINDS, gauss_sine, layered_eps,
-    config_c1, config_c2, config_c3, config_c4, config_c5, config_c5s, config_wave2d, small_cavity,
+    config_c1, config_c2, config_c3, config_c3r, config_c4, config_c5, config_c5s, config_wave2d, small_cavity,
     random_fields, spiral_pec_cells,
 )

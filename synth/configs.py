@@ -172,6 +172,28 @@ def config_c3(dtype="f64", p=8, nsteps=4096, n=256) -> Workload:
                     sources=src, method="leja", eps_A=1e-10)
 
 
+def config_c3r(k=10.0, n=128, dtype="f64", p=8) -> Workload:
+    """C3 with one locally refined element (an addition, the paper's R(k) mechanism in 3-D,
+    PAPER:708-737): n^3 cells of 1 mm with C3's four z-slabs, the centre column and row of
+    cells refined to dx = dy = 1 mm / k (reading 32, as the 2-D wave), over C3's interval
+    T = 4096 x 0.95 dt_CFL(1 mm) = 7.494 ns at 0.95 of the refined mesh's eq:cfl step (n_t from
+    T, so it grows ~k-fold), GAUSS_PAPER sigma_t = 128 ps on a z-edge off the refined slabs,
+    Leja at eps_A = 1e-10."""
+    eps = layered_eps(n, n, n)
+    d = 1e-3
+    dx = np.full(n, d)
+    dy = np.full(n, d)
+    dz = np.full(n, d)
+    c = n // 2
+    if k != 1.0:
+        dx[c] = d / k
+        dy[c] = d / k
+    t_end = 4096 * 0.95 * d / (C0 * math.sqrt(3.0))
+    src = [Source(2, (5 * n) // 16, (5 * n) // 16, n // 8, "gauss_paper", 1.0, 128e-12)]
+    return Workload(f"C3r-{n}-k{k:g}-{dtype}-p{p}", n, n, n, d, dtype, 0.95, 0, p, eps_r=eps,
+                    sources=src, method="leja", eps_A=1e-10, dx=dx, dy=dy, dz=dz, t_end=t_end)
+
+
 def spiral_pec_cells(nx, ny, nz, k_trace=10, turns=5, width=4, gap=2, outer=160, k_sub=10):
     """Synthetic planar rectangular spiral (C4, [P]): PEC cells in layer k_trace along a
     `turns`-turn rectangular spiral, `width` cells wide with `gap`-cell gaps, outer square

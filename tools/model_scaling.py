@@ -12,6 +12,7 @@ SURVEY 8(e): (A) cost-balanced contiguous blocks with Horner tails (the default)
 independent tails, longest-processing-time-first (tail_mode EXP_LPT).  Printed as JSON lines.
 Usage: python tools/model_scaling.py [workload] [p ...]   (default c3 8 64)"""
 import json
+import math
 import os
 import sys
 
@@ -31,6 +32,8 @@ def main():
     w = workload(name)
     g = pe.Grid.from_workload(w)
     info = g.info(compute_rho_pow=True)
+    if not w.nsteps and w.t_end:            # interval given as T (refined meshes): n_t from dt
+        w.nsteps = int(math.ceil(w.t_end / info["dt"]))
     td = g.torch_dtype()
     z = lambda: torch.zeros(3 * g.npts, dtype=td, device="cuda:0")   # noqa: E731
     kw = dict(sources=w.sources, method=w.method, m=w.m, s=w.s, eps_A=w.eps_A)
@@ -50,7 +53,9 @@ def main():
         torch.cuda.synchronize()
         serial = s0.elapsed_time(s1)
         print(json.dumps({"workload": w.name, "p": p, "G": 1, "kind": "measured", "wall_ms": st1["ms_total"],
-                          "serial_leapfrog_ms": serial, "speedup": serial / st1["ms_total"]}), flush=True)
+                          "serial_leapfrog_ms": serial, "speedup": serial / st1["ms_total"], "nsteps": w.nsteps,
+                          "a_applications": st1["a_applications"], "rho": rho, "rho_cfl": info["rho_cfl"],
+                          "rho_pow": info["rho_pow"]}), flush=True)
         for G, sched in [(g_, sc) for sc in ("blocks", "lpt") for g_ in (2, 4, 8)]:
             tm = "exp" if sched == "blocks" else "exp_lpt"
             blocks = []
