@@ -77,3 +77,31 @@ def test_c5_768_fp64_sampled():
     n = 768
     w = config_c5(n=n, dtype="f64")
     _run_leapfrog_expmv(w, "f64", 20, 64, [(n // 2, n // 3, n - 10), (5, n - 3, 7)], half=4)
+
+
+def test_c3r_refined_full_interval_auto_plan():
+    """C3r (C3 with the centre cell column and row refined to Delta/k; reading 32 in 3-D) at
+    24^3 and k = 10: the whole interval T = 7.49 ns (n_t from T, ~33500 steps at the refined
+    mesh's eq:cfl step), p = 8, on the AUTO plan (K5's rho, planner (m, s)) -- the per-edge /
+    per-face coefficient kernels of the G = 1..8 refined-mesh model, against
+    Algorithm 1 in the oracle with the library's plan."""
+    import math
+    from synth import config_c3r
+    w = config_c3r(k=10.0, n=24)
+    og = fit.Grid.from_workload(w, dtype="f64")
+    lg = pe.Grid.from_workload(w, dtype="f64")
+    nsteps = int(math.ceil(w.t_end / lg.dt))
+    nsteps -= nsteps % w.p
+    # random initial fields beside the source: driven from zero, the PEC cavity ends with the
+    # pulse's large static e (charge) and a ringing h ~1e-6 of it in Z0 units, whose rel-L2
+    # would measure rounding against a near-zero norm (h 2e-10 there, e 2e-13)
+    u0 = og.clean(*random_fields(w.nx, w.ny, w.nz, seed=10))
+    got = lib_solve(lg, nsteps, w.p, w.sources, u0=u0, eps_A=1e-10)
+    st = got[2]
+    assert st["rho_fallback"] == 0 and st["rho"] < 0.5 * og.rho_cfl     # ||A|| far below the CFL bound
+    m, s, rho = st["m"], st["s_first"], st["rho"]
+    ref = fit.paraexp(og, w.sources, 0.0, nsteps, w.p, lambda tau: fit.make_plan("leja", m, s, tau, rho),
+                      u0=u0, rho=rho, dtype="f64")
+    assert_parity(got[:2], ref, "f64", f"C3r k=10 24^3 {nsteps} steps m={m} s={s}")
+    assert_maxabs(got[:2], ref, "f64", "C3r k=10")
+    lg.close()
