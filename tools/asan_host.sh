@@ -15,7 +15,7 @@ for f in grid plan api; do
 done
 gcc -std=c11 $SAN $INC -c $ROOT/tools/host_abi_check.c -o $OUT/check.o || exit 1
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -o $OUT/host_abi_check $OUT/check.o \
-  $B/kernels.cu.o $B/fused.cu.o $B/small.cu.o $OUT/grid.o $OUT/plan.o $OUT/api.o \
+  $B/kernels.cu.o $B/fused.cu.o $B/small.cu.o $B/mid.cu.o $OUT/grid.o $OUT/plan.o $OUT/api.o \
   -cudart static -ldl -lpthread -Xlinker -lasan -Xlinker -lubsan || exit 1
 echo "== host ABI under ASan/UBSan"
 ASAN_OPTIONS=detect_leaks=1 UBSAN_OPTIONS=print_stacktrace=1 $OUT/host_abi_check; r1=$?
