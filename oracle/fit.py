@@ -867,7 +867,8 @@ def norm_A(g: Grid, tol: float = 1e-10) -> float:
 
 
 # ---------------------------------------------------------------------------
-# Planner (reading 16) -- parity unpinned (the paper gives no table)
+# Planner (reading 16) -- no paper table; theta_m pinned by tests/test_oracle_theta.py
+# (series-tail root for Taylor, barycentric interpolant for Leja)
 # ---------------------------------------------------------------------------
 def poly_error(method: str, m: int, theta: float, npts: int = 801) -> float:
     """max_{x in [-theta, theta]} |p(ix) - e^{ix}| for the degree-m interpolant of one
@@ -882,7 +883,8 @@ def poly_error(method: str, m: int, theta: float, npts: int = 801) -> float:
 
 
 def theta_m(method: str, m: int, tol: float) -> float:
-    """Largest theta with max error <= tol*theta (bisection, 40 halvings).  Parity unpinned."""
+    """Largest theta with max error <= tol*theta (bisection, 40 halvings).  Pinned by
+    tests/test_oracle_theta.py (Taylor: the series-tail root; Leja: the barycentric interpolant)."""
     lo, hi = 0.0, float(2 * m + 4)
     for _ in range(40):
         mid = 0.5 * (lo + hi)
