@@ -60,8 +60,9 @@ constexpr int mid_cap() {                // cells per CTA (fp64 1920, fp32 3072)
     return kMidThreads * mid_R<T>();
 }
 
-// flag bits of an owned cell: neighbours exist (i-1, j-1, k-1, i+1, j+1, k+1), e / h live,
-// neighbour across a box face (remote: read from that CTA's exchange face), k in bits 16-31
+// flag bits of an owned cell: neighbours exist (i-1, j-1, k-1, i+1, j+1, k+1), e / h live
+// (bits 6-8 / 9-11), neighbour across a box face (remote: read from the halo of that CTA's
+// face), the cell lies in a face row (bit 16), k in bits 17-31 (so nz < 2^15)
 enum : unsigned {
     F_IM = 1u, F_JM = 2u, F_KM = 4u, F_IP = 8u, F_JP = 16u, F_KP = 32u,
     F_RJM = 1u << 12, F_RKM = 1u << 13, F_RJP = 1u << 14, F_RKP = 1u << 15, F_FACE = 1u << 16
@@ -633,7 +634,7 @@ static bool mid_geo(const Grid &g, MidGeo &mg) {
     const int cap = f64 ? mid_cap<double>() : mid_cap<float>();
     const int64_t cells = (int64_t)g.nx * g.ny * g.nz;
     const int nsm = mid_num_sms();
-    if (cells > (int64_t)cap * nsm) return false;
+    if (cells > (int64_t)cap * nsm || g.nz >= (1 << 15)) return false;   // k in 15 flag bits
     if (!mid_partition(g.nx, g.ny, g.nz, cap, nsm, g.esize(), mg)) return false;
     const int L = f64 ? mid_lines<double>() : mid_lines<float>();
     mg.slot = 2 * (mg.fj + mg.fk) * L;
