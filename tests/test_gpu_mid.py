@@ -114,3 +114,45 @@ def test_mid_vs_tma_same_grid():
     assert_parity(a[:2], b[:2], "f64", "mid vs tma leapfrog")
     lm.close()
     lt.close()
+
+
+def test_mid_two_grids_concurrently():
+    """Two grids stepped at the same time from two host threads on their own streams (each grid
+    owns its exchange lines and tag counter; two cooperative launches may share the GPU): the
+    results are bit-identical to the same runs one after the other."""
+    import threading
+    import torch
+    shapes = [((48, 40, 36), "ztable", "f64"), ((40, 30, 20), "edge", "f32")]
+    grids, fields = [], []
+    for n, mode, dtype in shapes:
+        kw = _grid_kw(mode, n)
+        og = fit.Grid(*n, dt_frac=0.95, dtype=dtype, **kw)
+        grids.append(pe.Grid(*n, dt_frac=0.95, dtype=dtype, **kw))
+        fields.append(inputs(og, *random_fields(*n, seed=21)))
+    src = [[gauss_sine(2, n[0] // 2, n[1] // 2, n[2] // 2, f0=40e9, bw=40e9)] for n, _, _ in shapes]
+    seq = [lib_leapfrog(g, e, h, 800, s)[:2] for g, (e, h), s in zip(grids, fields, src)]
+    out = [None, None]
+
+    def run(q):
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            e, h = fields[q]
+            te = torch.tensor(e, dtype=grids[q].torch_dtype(), device="cuda:0")
+            th = torch.tensor(h, dtype=grids[q].torch_dtype(), device="cuda:0")
+            for _ in range(3):   # several calls: the tag counter advances per launch
+                te.copy_(torch.tensor(e, dtype=grids[q].torch_dtype()))
+                th.copy_(torch.tensor(h, dtype=grids[q].torch_dtype()))
+                pe.leapfrog(grids[q], te, th, 800, src[q], stream=s.cuda_stream)
+            s.synchronize()
+            out[q] = (te.double().cpu().numpy(), th.double().cpu().numpy())
+
+    ts = [threading.Thread(target=run, args=(q,)) for q in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for q in range(2):
+        assert np.array_equal(out[q][0], seq[q][0]) and np.array_equal(out[q][1], seq[q][1]), q
+    for g in grids:
+        g.close()
