@@ -10,7 +10,7 @@ region starts; the working set (815 MB per state vector) exceeds the 126 MB L2, 
 flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W]
-                  [--workload c3|c3-f32|c3-p64|c2|c1|c4|c5-<n>[-f64]|c5s-<n>[-f64]|wave2d[-k]]
+                  [--workload c3|c3-f32|c3-p64|c2|c1|c4|c5-<n>[-f64]|c5s-<n>[-f64]|wave2d[-k]|c3r-<k>[-<n>]]
                   [--p P]
                   [--impl ours|reference] [--no-cpu-baseline]
 

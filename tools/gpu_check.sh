@@ -10,7 +10,7 @@ for w in $what; do case $w in
 tests) timeout 2400 python -m pytest tests -q -m gpu --durations=15 > $out/pytest_gpu.log 2>&1; echo "tests rc=$?" | tee -a $out/rc.txt;;
 tfile=*) timeout 2400 python -m pytest tests/${w#tfile=} -q -m gpu --durations=15 > $out/pytest_${w#tfile=}.log 2>&1; echo "$w rc=$?" | tee -a $out/rc.txt;;
 bench) timeout 900 python bench.py > $out/bench.json 2> $out/bench.err; echo "bench rc=$?" | tee -a $out/rc.txt; tail -1 $out/bench.json;;
-bench32) timeout 900 python bench.py --workload c3f32 > $out/bench32.json 2> $out/bench32.err; echo "bench32 rc=$?" | tee -a $out/rc.txt; tail -1 $out/bench32.json;;
+bench32) timeout 900 python bench.py --workload c3-f32 > $out/bench32.json 2> $out/bench32.err; echo "bench32 rc=$?" | tee -a $out/rc.txt; tail -1 $out/bench32.json;;
 launches) timeout 900 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-serial > $out/plain_short.json 2>&1 && \
   timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-serial > $out/ncu_launch.log 2>&1; echo "launches rc=$?" | tee -a $out/rc.txt;;
