@@ -245,7 +245,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernels", default="auto", choices=["auto", "unfused", "fused"])
+    ap.add_argument("--kernels", default="auto", choices=["auto", "unfused", "fused", "tma"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-serial", action="store_true")
     ap.add_argument("--p", type=int, default=0, help="override the workload's sub-interval count")
