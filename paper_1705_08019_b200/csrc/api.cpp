@@ -311,9 +311,10 @@ int k_leapfrog(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev
     const bool tracing = tr && (tr->energy || (tr->probe && tr->np > 0));
     if (ka.g->kernels == PARAEXP_KERNELS_FUSED && !tracing && nsrc <= 16 && small_supported(*ka.g))
         return k_leapfrog_small(ka, bufs[0], nsteps, nsrc, q_dev);
-    // mid-size grids: one cooperative launch over all SMs (never for concurrently swept
-    // sub-intervals: the launch needs the whole GPU and the grid's exchange buffer)
-    if (ka.g->kernels == PARAEXP_KERNELS_FUSED && !tracing && nsrc <= 16 && !ka.static_sched && mid_supported(*ka.g))
+    // mid-size grids: one cooperative launch per sequence (mid.cu) -- over all SMs, or, for a
+    // concurrently swept sub-interval, over its CTA budget with its own exchange-buffer slot
+    if (ka.g->kernels == PARAEXP_KERNELS_FUSED && !tracing && nsrc <= 16 && (!ka.static_sched || ka.mid_slot > 0) &&
+        mid_supported(*ka.g, ka.mid_max_cta))
         return k_leapfrog_mid(ka, bufs[0], nsteps, nsrc, q_dev);
     if (zmarch_kernels(*ka.g) && fused_supported(*ka.g))
         return k_leapfrog_fused(ka, bufs, nsteps, src_dev, nsrc, q_dev, tr);
@@ -1353,8 +1354,23 @@ static int solve_block_dev(Grid &G, const SolveCtx &c, int nsrc, const void *e0,
     // cannot fill the GPU they run concurrently on side streams, each into its own buffer, and
     // the Horner chain on `stream` consumes them in order as they complete.
     const int nb = first >= 1 ? last - first + 1 : 0;
-    const int nstr = std::min(nb, 8);
-    const bool conc = nb >= 2 && nb <= 64 && concurrent_sweeps(G);
+    int nstr = std::min(nb, 8);
+    bool conc = nb >= 2 && nb <= 64 && concurrent_sweeps(G);
+    // Mid-size grids (mid.cu): a sweep is ONE resident launch instead of one TMA launch per step
+    // (at 32^3 those per-step launches bound the solve by the host's launch rate).  The sweeps
+    // run concurrently on SM partitions -- as many streams (<= 8) as leave each sweep the CTAs
+    // it needs, each stream with its own exchange-buffer slot -- or, if not even two fit,
+    // serially over the whole GPU (unless PARAEXP_CONCURRENT forces the concurrent TMA sweeps).
+    int mid_budget = 0;
+    if (conc && G.kernels == PARAEXP_KERNELS_FUSED && nsrc <= 16 && mid_supported(G)) {
+        const int nsm = device_sm_count();
+        for (int ns = nstr; ns >= 2 && !mid_budget; --ns)
+            if (mid_supported(G, nsm / ns)) {
+                mid_budget = nsm / ns;
+                nstr = ns;
+            }
+        if (!mid_budget && !getenv("PARAEXP_CONCURRENT")) conc = false;
+    }
     std::vector<void *> Pc;
     if (conc) {
         while ((int)G.conc.size() < nb + nstr) {
@@ -1383,6 +1399,10 @@ static int solve_block_dev(Grid &G, const SolveCtx &c, int nsrc, const void *e0,
             KernelArgs kq = ka;
             kq.stream = G.streams[sq];
             kq.static_sched = true;                        // concurrent launches: no shared counter
+            if (mid_budget) {                              // resident sweep on its SM partition
+                kq.mid_slot = 1 + sq;
+                kq.mid_max_cta = mid_budget;
+            }
             if ((rc = dev_memset_async(Pc[q], 0, sbytes, kq.stream))) return rc;
             void *bufs[2] = {Pc[q], scratch[sq]};
             const size_t qoff = (size_t)c.B[i - 1] * nsrc * G.esize();

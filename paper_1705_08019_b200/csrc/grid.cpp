@@ -238,10 +238,12 @@ void grid_free_device(Grid &G) {
     G.events.clear();
     dev_free(G.d_sched);
     G.d_sched = nullptr;
-    dev_free(G.d_mid);
-    G.d_mid = nullptr;
-    G.mid_bytes = 0;
-    G.mid_tag = 0;
+    for (int q = 0; q < Grid::kMidSlots; ++q) {
+        dev_free(G.d_mid[q]);
+        G.d_mid[q] = nullptr;
+        G.mid_bytes[q] = 0;
+        G.mid_tag[q] = 0;
+    }
     dev_free(G.d_norms);
     G.d_norms = nullptr;
     if (G.call_event) dev_event_destroy(G.call_event);

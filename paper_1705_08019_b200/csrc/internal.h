@@ -68,9 +68,13 @@ struct Grid {
     void *d_norms = nullptr;    // per-propagator energy norms of a solve (rho safety net, f. intervals)
     void *call_event = nullptr; // recorded at the end of every call (stream order across calls)
     void *call_stream = nullptr;
-    void *d_mid = nullptr;      // mid.cu: tagged face-exchange lines of the resident kernels
-    int64_t mid_bytes = 0;
-    uint32_t mid_tag = 0;       // next epoch-tag base of a mid launch (0: buffer not zeroed yet)
+    // mid.cu: tagged face-exchange lines of the resident leapfrog, one set per slot (slot 0:
+    // the caller's stream; slots 1..8: concurrently swept sub-intervals), and per slot the next
+    // epoch-tag base of a launch (0: the buffer is not zeroed yet)
+    static constexpr int kMidSlots = 9;
+    void *d_mid[kMidSlots] = {};
+    int64_t mid_bytes[kMidSlots] = {};
+    uint32_t mid_tag[kMidSlots] = {};
     void *d_sched = nullptr;    // monotone unit counter of the fused kernels' dynamic schedule
     unsigned long long sched_base = 0;   // host shadow: value of *d_sched before the next launch
     int64_t d_q_cap = 0;
@@ -141,6 +145,8 @@ struct KernelArgs {
     int64_t *launches;
     const EtDev *et = nullptr;   // per-call early-termination buffers (op/apps set per launch)
     bool static_sched = false;   // launches that run concurrently with others: no shared counter
+    int mid_slot = 0;            // mid.cu exchange-buffer slot (> 0: a concurrent sweep's own)
+    int mid_max_cta = 0;         // mid.cu CTA budget (0: one per SM) for concurrent sweeps
 };
 
 // per-step trace outputs of a leapfrog sequence (f1): device pointers at the row of the
@@ -179,7 +185,8 @@ int k_leapfrog_small(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc
 int k_poly_small(const KernelArgs &ka, const Plan &plan, void *state);
 // mid-size grids (mid.cu): one cooperative launch per leapfrog sequence, the state resident in
 // the shared memory of up to one CTA per SM, neighbour-only face exchange through L2
-bool mid_supported(const Grid &g);
+bool mid_supported(const Grid &g, int max_cta = 0);
+int device_sm_count();
 int k_leapfrog_mid(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc, const void *q_dev);
 // the TMA z-marching kernels serve this grid (kernels FUSED = auto choice, or TMA only)
 inline bool zmarch_kernels(const Grid &g) {

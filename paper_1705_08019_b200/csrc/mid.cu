@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(kMidThreads, 1)
 // ---------------------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------------------
-static int mid_num_sms() {   // of the current device (cached per device)
+int device_sm_count() {   // of the current device (cached per device)
     static std::mutex mu;
     static std::map<int, int> cache;
     int dev = 0;
@@ -629,11 +629,11 @@ static bool mid_partition(int nx, int ny, int nz, int cap, int nsm, size_t esize
     return true;
 }
 
-static bool mid_geo(const Grid &g, MidGeo &mg) {
+static bool mid_geo(const Grid &g, MidGeo &mg, int max_cta) {
     const bool f64 = g.dtype == PARAEXP_F64;
     const int cap = f64 ? mid_cap<double>() : mid_cap<float>();
     const int64_t cells = (int64_t)g.nx * g.ny * g.nz;
-    const int nsm = mid_num_sms();
+    const int nsm = max_cta > 0 ? std::min(max_cta, device_sm_count()) : device_sm_count();
     if (cells > (int64_t)cap * nsm || g.nz >= (1 << 15)) return false;   // k in 15 flag bits
     if (!mid_partition(g.nx, g.ny, g.nz, cap, nsm, g.esize(), mg)) return false;
     const int L = f64 ? mid_lines<double>() : mid_lines<float>();
@@ -642,7 +642,7 @@ static bool mid_geo(const Grid &g, MidGeo &mg) {
     return true;
 }
 
-bool mid_supported(const Grid &g) {
+bool mid_supported(const Grid &g, int max_cta) {
     static const bool off = [] {
         const char *e = getenv("PARAEXP_NO_MID");
         return e && atoi(e) != 0;
@@ -652,35 +652,38 @@ bool mid_supported(const Grid &g) {
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) != cudaSuccess || !coop) return false;
     MidGeo mg;
-    return mid_geo(g, mg);
+    return mid_geo(g, mg, max_cta);
 }
 
 // exchange lines (2 slots per CTA), grid-owned, grown on demand and zeroed (tag 0 is never
 // used); the launch's tag base comes from a per-grid counter so that lines left by earlier
 // launches never match -- on wrap-around the buffer is zeroed again
-static int mid_buffers(Grid &G, const MidGeo &mg, int64_t epochs, void *stream, uint4 **xb, unsigned *tag0) {
+static int mid_buffers(Grid &G, int slot, const MidGeo &mg, int64_t epochs, void *stream, uint4 **xb,
+                       unsigned *tag0) {
+    if (slot < 0 || slot >= Grid::kMidSlots) return fail(PARAEXP_EINVAL, "mid kernels: bad buffer slot");
     const size_t need = (size_t)mg.ncta * mg.xstride * sizeof(uint4);
     int rc;
     bool zero = false;
-    if ((size_t)G.mid_bytes < need) {
-        dev_free(G.d_mid);
-        G.d_mid = nullptr;
-        G.device_bytes -= G.mid_bytes;
-        G.mid_bytes = 0;
-        if ((rc = dev_alloc(&G.d_mid, need))) return rc;
-        G.mid_bytes = (int64_t)need;
+    if ((size_t)G.mid_bytes[slot] < need) {
+        dev_free(G.d_mid[slot]);
+        G.d_mid[slot] = nullptr;
+        G.device_bytes -= G.mid_bytes[slot];
+        G.mid_bytes[slot] = 0;
+        if ((rc = dev_alloc(&G.d_mid[slot], need))) return rc;
+        G.mid_bytes[slot] = (int64_t)need;
         G.device_bytes += (int64_t)need;
         zero = true;
     }
-    if (G.mid_tag == 0 || (uint64_t)G.mid_tag + (uint64_t)epochs + 2 > 0x7fffffffull) zero = true;
+    uint32_t &tag = G.mid_tag[slot];
+    if (tag == 0 || (uint64_t)tag + (uint64_t)epochs + 2 > 0x7fffffffull) zero = true;
     if (zero) {
-        if ((rc = dev_memset_async(G.d_mid, 0, (size_t)G.mid_bytes, stream))) return rc;
-        G.mid_tag = 1;
+        if ((rc = dev_memset_async(G.d_mid[slot], 0, (size_t)G.mid_bytes[slot], stream))) return rc;
+        tag = 1;
     }
     if ((uint64_t)epochs + 2 > 0x7ffffff0ull) return fail(PARAEXP_EINVAL, "mid kernels: too many epochs in one launch");
-    *tag0 = (unsigned)G.mid_tag;
-    G.mid_tag += (uint32_t)(epochs + 2);
-    *xb = (uint4 *)G.d_mid;
+    *tag0 = (unsigned)tag;
+    tag += (uint32_t)(epochs + 2);
+    *xb = (uint4 *)G.d_mid[slot];
     return PARAEXP_OK;
 }
 
@@ -689,7 +692,7 @@ int k_leapfrog_mid(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc, 
     Grid &g = *const_cast<Grid *>(ka.g);
     if (nsrc > 16) return fail(PARAEXP_EINVAL, "mid leapfrog: at most 16 sources");
     MidGeo mg;
-    if (!mid_geo(g, mg)) return fail(PARAEXP_EINVAL, "mid leapfrog: grid does not fit");
+    if (!mid_geo(g, mg, ka.mid_max_cta)) return fail(PARAEXP_EINVAL, "mid leapfrog: grid does not fit");
     MidSrc sl;
     sl.n = nsrc;
     for (int r = 0; r < nsrc; ++r) {
@@ -700,7 +703,7 @@ int k_leapfrog_mid(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc, 
     }
     uint4 *xb = nullptr;
     unsigned tag0 = 0;
-    int rc = mid_buffers(g, mg, 2 * nsteps + 1, ka.stream, &xb, &tag0);
+    int rc = mid_buffers(g, ka.mid_slot, mg, 2 * nsteps + 1, ka.stream, &xb, &tag0);
     if (rc) return rc;
     return with_types(g, 1.0, [&](auto tT, auto tEM, auto tHA) {
         using T = decltype(tT);
