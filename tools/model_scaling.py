@@ -1,7 +1,8 @@
 """ParaExp wall time at G = 1, 2, 4, 8 GPUs as a MODEL from measured per-rank block times
 (one B200; no multi-GPU box was available): for each G, every rank's paraexp_solve_block
 (its cost-balanced contiguous block: particular sweeps + Horner tails to T_p) is run on cuda:0
-and timed with CUDA events on the launching stream; the modelled wall time is
+and timed with CUDA events on the launching stream (after one warm-up call of the same block);
+the modelled wall time is
 
     T_G = max_rank T_block(rank) + T_reduce + T_finish
 
@@ -62,6 +63,10 @@ def main():
             v = (z(), z())
             We, Wh = z(), z()
             for r in range(G):
+                wv = (z(), z())
+                # warm-up of this rank's block first (first-use allocations of its concurrent-
+                # sweep buffers, exchange slots and streams are not part of a rank's time)
+                pe.solve_block(g, r, G, w.nsteps, p, wv, rho=rho, v=(z(), z()), tail_mode=tm, **kw)
                 wv = (z(), z())
                 st = pe.solve_block(g, r, G, w.nsteps, p, wv, rho=rho, v=v, tail_mode=tm, **kw)
                 blocks.append({"rank": r, "first": st["first_interval"], "last": st["last_interval"],
