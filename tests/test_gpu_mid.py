@@ -156,3 +156,25 @@ def test_mid_two_grids_concurrently():
         assert np.array_equal(out[q][0], seq[q][0]) and np.array_equal(out[q][1], seq[q][1]), q
     for g in grids:
         g.close()
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_mid_concurrent_sweeps_solve(dtype):
+    """ParaExp on a mid-size refined grid (C3r 32^3, k = 10): the particular sweeps run as
+    resident mid-kernel launches on SM partitions (one launch per sweep, not one per step),
+    against Algorithm 1 in the oracle, with random u0 beside the source."""
+    from synth import config_c3r
+    w = config_c3r(k=10.0, n=32, dtype=dtype)
+    og = fit.Grid.from_workload(w, dtype=dtype)
+    lg = pe.Grid.from_workload(w, dtype=dtype)
+    nsteps, p, m, s = 1600, 8, 32, 4
+    rho = og.rho_cfl
+    u0 = og.clean(*random_fields(w.nx, w.ny, w.nz, seed=12))
+    got = lib_solve(lg, nsteps, p, w.sources, u0=u0, m=m, s=s, rho=rho)
+    st = got[2]
+    # 8 sweeps of 200 steps: far fewer launches than the 1600 steps (+ the pair launches)
+    assert st["kernel_launches"] < nsteps, st
+    ref = fit.paraexp(og, w.sources, 0.0, nsteps, p, lambda tau: fit.make_plan("leja", m, s, tau, rho),
+                      u0=u0, rho=rho, dtype=dtype)
+    assert_parity(got[:2], ref, dtype, f"C3r 32^3 {dtype} concurrent resident sweeps")
+    lg.close()
