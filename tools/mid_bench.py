@@ -42,7 +42,7 @@ def main():
     ns = [int(a) for a in sys.argv[1:]] or [32, 48, 64]
     for n in ns:
         for dtype in ("f64", "f32"):
-            for k in ("auto", "tma"):
+            for k in os.environ.get("MID_KERNELS", "auto,tma").split(","):
                 run(n, dtype, k)
 
 
