@@ -67,6 +67,10 @@ enum { PARAEXP_TAIL_EXP = 0, PARAEXP_TAIL_LEAPFROG = 1, PARAEXP_TAIL_EXP_LPT = 2
 enum { PARAEXP_MAT_SCALAR = 0, PARAEXP_MAT_ZTABLE = 1, PARAEXP_MAT_ARRAY = 2 };
 enum { PARAEXP_KERNELS_AUTO = 0, PARAEXP_KERNELS_UNFUSED = 1, PARAEXP_KERNELS_FUSED = 2,
        PARAEXP_KERNELS_TMA = 3 };
+/* leapfrog kernel path of a grid (paraexp_grid_info_t.leapfrog_path): one kernel per curl half,
+ * the TMA z-marching kernels (one launch per step), the single-CTA small-grid kernel or the
+ * cooperative mid-size resident kernel (one launch per sequence) */
+enum { PARAEXP_PATH_UNFUSED = 0, PARAEXP_PATH_TMA = 1, PARAEXP_PATH_SMALL = 2, PARAEXP_PATH_MID = 3 };
 
 #define PARAEXP_MAX_DEGREE 150
 #define PARAEXP_MAX_SOURCES 64
@@ -121,6 +125,8 @@ typedef struct {
     int64_t device_bytes;  /* bytes of device memory currently owned by the grid         */
     int32_t device;
     int32_t warnings;      /* PARAEXP_WCFL if dt > dt_cfl                                */
+    int32_t leapfrog_path; /* PARAEXP_PATH_*: the kernels a leapfrog call on this grid    *
+                            * runs (no trace, <= 16 sources); -1 for a host-only grid     */
 } paraexp_grid_info_t;
 
 /* Create a grid: validates, assembles fp64 FIT coefficients on the host (standard FIT

@@ -28,6 +28,7 @@ TAYLOR, LEJA, KRYLOV = 0, 1, 2
 TAIL_EXP, TAIL_LEAPFROG, TAIL_EXP_LPT = 0, 1, 2
 MAT_SCALAR, MAT_ZTABLE, MAT_ARRAY = 0, 1, 2
 KERNELS_AUTO, KERNELS_UNFUSED, KERNELS_FUSED, KERNELS_TMA = 0, 1, 2, 3
+PATH_UNFUSED, PATH_TMA, PATH_SMALL, PATH_MID = 0, 1, 2, 3   # paraexp_grid_info_t.leapfrog_path
 MAX_DEGREE = 150
 MAX_PROBES = 16
 
@@ -48,7 +49,7 @@ class paraexp_grid_info_t(C.Structure):
                 ("dt", C.c_double), ("dt_cfl", C.c_double), ("rho_cfl", C.c_double),
                 ("rho_pow", C.c_double), ("material_mode", C.c_int32), ("kernels", C.c_int32),
                 ("pitch_x", C.c_int64), ("device_bytes", C.c_int64), ("device", C.c_int32),
-                ("warnings", C.c_int32)]
+                ("warnings", C.c_int32), ("leapfrog_path", C.c_int32)]
 
 
 class paraexp_source(C.Structure):

@@ -859,6 +859,15 @@ int paraexp_grid_info(paraexp_grid *grid, int32_t compute_rho_pow, void *stream,
     o->device_bytes = G.device_bytes;
     o->device = G.device;
     o->warnings = G.warnings;
+    o->leapfrog_path = -1;
+    if (G.device >= 0) {
+        pe::dev_set_device(G.device);
+        o->leapfrog_path = G.kernels == PARAEXP_KERNELS_UNFUSED                      ? PARAEXP_PATH_UNFUSED
+                           : G.kernels == PARAEXP_KERNELS_FUSED && pe::small_supported(G) ? PARAEXP_PATH_SMALL
+                           : G.kernels == PARAEXP_KERNELS_FUSED && pe::mid_supported(G)   ? PARAEXP_PATH_MID
+                           : pe::fused_supported(G)                                     ? PARAEXP_PATH_TMA
+                                                                                        : PARAEXP_PATH_UNFUSED;
+    }
     return PARAEXP_OK;
 }
 

@@ -178,3 +178,16 @@ def test_mid_concurrent_sweeps_solve(dtype):
                       u0=u0, rho=rho, dtype=dtype)
     assert_parity(got[:2], ref, dtype, f"C3r 32^3 {dtype} concurrent resident sweeps")
     lg.close()
+
+
+def test_leapfrog_path_reported():
+    """paraexp_grid_info_t.leapfrog_path names the kernels a leapfrog call runs: single-CTA
+    (<= 2048 cells fp64), the mid-size resident kernel, the TMA kernels (large grids or
+    kernels="tma"), unfused"""
+    cases = [((16, 16, 8), "auto", pe.abi.PATH_SMALL), ((24, 20, 18), "auto", pe.abi.PATH_MID),
+             ((24, 20, 18), "tma", pe.abi.PATH_TMA), ((24, 20, 18), "unfused", pe.abi.PATH_UNFUSED),
+             ((128, 128, 64), "auto", pe.abi.PATH_TMA)]
+    for n, kern, path in cases:
+        g = pe.Grid(*n, d0=1e-3, dt_frac=0.95, kernels=kern)
+        assert g.info()["leapfrog_path"] == path, (n, kern)
+        g.close()

@@ -237,3 +237,11 @@ def test_c_example_compiles_and_links(tmp_path):
                            os.path.join(root, "examples", "cavity_solve.c"), "-L", libdir,
                            "-l:libparaexp.so", f"-Wl,-rpath,{libdir}", "-lm", "-o", str(exe)])
     assert exe.exists()
+
+
+def test_leapfrog_path_host_only_grid():
+    """paraexp_grid_info_t.leapfrog_path is -1 on a host-only grid (no device to decide on)"""
+    g = pe.Grid(8, 8, 8, d0=1e-3, dt_frac=0.9, device=-1)
+    info = g.info()
+    assert info["leapfrog_path"] == -1 and info["kernels"] == pe.abi.KERNELS_FUSED
+    g.close()
