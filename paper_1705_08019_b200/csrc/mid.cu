@@ -279,7 +279,7 @@ struct Halo {
 };
 
 // Stage the neighbours' faces of epoch `tag` (slot `sidx`) into the halos: every thread issues
-// up to 8 line loads, then re-polls those whose tags are not there yet.  lo: the j-1 / k-1
+// up to 4 line loads at a time, then re-polls those whose tags are not there yet.  lo: the j-1 / k-1
 // neighbours' faces, hi: the j+1 / k+1 neighbours'.  A poll that never completes traps.
 template <typename T>
 __device__ __forceinline__ void mid_stage(const uint4 *xb, const MidGeo &mg, const MidBox &b, int nx, unsigned sidx,
