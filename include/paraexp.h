@@ -126,7 +126,8 @@ typedef struct {
     int32_t device;
     int32_t warnings;      /* PARAEXP_WCFL if dt > dt_cfl                                */
     int32_t leapfrog_path; /* PARAEXP_PATH_*: the kernels a leapfrog call on this grid    *
-                            * runs (no trace, <= 16 sources); -1 for a host-only grid     */
+                            * runs (<= 16 sources; a traced call on a single-CTA grid     *
+                            * runs the TMA kernels); -1 for a host-only grid              */
 } paraexp_grid_info_t;
 
 /* Create a grid: validates, assembles fp64 FIT coefficients on the host (standard FIT

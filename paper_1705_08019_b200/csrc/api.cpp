@@ -313,9 +313,9 @@ int k_leapfrog(const KernelArgs &ka, void *bufs[2], int64_t nsteps, const SrcDev
         return k_leapfrog_small(ka, bufs[0], nsteps, nsrc, q_dev);
     // mid-size grids: one cooperative launch per sequence (mid.cu) -- over all SMs, or, for a
     // concurrently swept sub-interval, over its CTA budget with its own exchange-buffer slot
-    if (ka.g->kernels == PARAEXP_KERNELS_FUSED && !tracing && nsrc <= 16 && (!ka.static_sched || ka.mid_slot > 0) &&
+    if (ka.g->kernels == PARAEXP_KERNELS_FUSED && nsrc <= 16 && (!ka.static_sched || ka.mid_slot > 0) &&
         mid_supported(*ka.g, ka.mid_max_cta))
-        return k_leapfrog_mid(ka, bufs[0], nsteps, nsrc, q_dev);
+        return k_leapfrog_mid(ka, bufs[0], nsteps, nsrc, q_dev, tracing ? tr : nullptr);
     if (zmarch_kernels(*ka.g) && fused_supported(*ka.g))
         return k_leapfrog_fused(ka, bufs, nsteps, src_dev, nsrc, q_dev, tr);
     return k_leapfrog_unfused(ka, bufs[0], nsteps, src_dev, nsrc, q_dev, tr);

@@ -187,7 +187,8 @@ int k_poly_small(const KernelArgs &ka, const Plan &plan, void *state);
 // the shared memory of up to one CTA per SM, neighbour-only face exchange through L2
 bool mid_supported(const Grid &g, int max_cta = 0);
 int device_sm_count();
-int k_leapfrog_mid(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc, const void *q_dev);
+int k_leapfrog_mid(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc, const void *q_dev,
+                   const TraceDev *tr = nullptr);
 // the TMA z-marching kernels serve this grid (kernels FUSED = auto choice, or TMA only)
 inline bool zmarch_kernels(const Grid &g) {
     return g.kernels == PARAEXP_KERNELS_FUSED || g.kernels == PARAEXP_KERNELS_TMA;

@@ -454,10 +454,13 @@ struct MidCoef {
 // 2m+2: stage the upper neighbours' e faces, h <- h - bH C e, publish the h faces.  Epoch 0
 // publishes the initial h faces.  Epoch t's faces go to slot t & 1 with tag tag0 + t.
 // ---------------------------------------------------------------------------------------
-template <typename T, int EM, bool HA, int R>
+// TR: also the f1 trace per step (paraexp.h): energy E_{m+1} = dt [sum e'^2 / cE + sum h h' / cH]
+// over the live DOFs (per-thread fp64 partials, one block reduction and one atomicAdd per CTA
+// per step, as K1r-TR) and the probe values e^(m+1) written by the owning thread.
+template <typename T, int EM, bool HA, int R, bool TR>
 __global__ void __launch_bounds__(kMidThreads, 1)
     leapfrog_mid_kernel(Dev<T> D, Coef<T, EM, HA> cf, MidGeo mg, T *__restrict__ st, int64_t nsteps, MidSrc src,
-                        const T *__restrict__ q, uint4 *xb, unsigned tag0) {
+                        const T *__restrict__ q, uint4 *xb, unsigned tag0, TraceDev tr) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *S = reinterpret_cast<T *>(smem_raw);
     const MidBox b = mid_box(mg, D);
@@ -469,6 +472,8 @@ __global__ void __launch_bounds__(kMidThreads, 1)
     MidCell cl[R];
     MidCoef<T, EM, HA, R> co;
     unsigned smask[R];
+    unsigned pmask[TR ? R : 1];   // probes at the cell (TR)
+    double eacc = 0.0;            // this step's energy partial (TR)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int sl = threadIdx.x + r * kMidThreads;
@@ -477,10 +482,14 @@ __global__ void __launch_bounds__(kMidThreads, 1)
         if (sl >= NL) cl[r].x = NL;   // no cell
         const int x = cl[r].x;
         smask[r] = 0;
+        if (TR) pmask[TR ? r : 0] = 0;
         if (x < NL) {
             const int i = x % nx, j = b.j0 + (x / nx) % b.byc, k = b.k0 + x / pl;
             for (int s = 0; s < src.n; ++s)
                 if (src.i[s] == i && src.j[s] == j && src.k[s] == k) smask[r] |= 1u << s;
+            if (TR)
+                for (int s = 0; s < tr.np; ++s)
+                    if (tr.i[s] == i && tr.j[s] == j && tr.k[s] == k) pmask[TR ? r : 0] |= 1u << s;
         }
         if (EM == 2)
             for (int c = 0; c < 3; ++c) co.e[EM == 2 ? r : 0][c] = cf.bE(c, 0, g);
@@ -515,6 +524,17 @@ __global__ void __launch_bounds__(kMidThreads, 1)
         ey[x] = e[1];
         ez[x] = e[2];
         if (sl) put_e_faces(sl, mg, c, e[0], e[1], e[2], tag);
+        if (TR) {
+#pragma unroll
+            for (int q3 = 0; q3 < 3; ++q3) {
+                const T be = EM == 2 ? co.e[EM == 2 ? r : 0][q3] : cf.bE(q3, (int)(f >> kKShift), 0);
+                if (be != T(0)) eacc += (double)e[q3] * (double)e[q3] / (double)be;
+            }
+            for (unsigned pm = pmask[TR ? r : 0]; pm; pm &= pm - 1) {
+                const int s = __ffs(pm) - 1;
+                tr.probe[m * tr.np + s] = (double)e[tr.c[s]];
+            }
+        }
     };
     auto h_cell = [&](int r, uint4 *sl, unsigned tag, auto remote) {
         const MidCell c = opaque(cl[r]);
@@ -527,7 +547,11 @@ __global__ void __launch_bounds__(kMidThreads, 1)
 #pragma unroll
         for (int q3 = 0; q3 < 3; ++q3) {
             const T bh = HA ? co.h[HA ? r : 0][q3] : T(1) * cf.bH(q3, 0);
-            if (f & (512u << q3)) h[q3] = h[q3] - bh * cc[q3];
+            if (f & (512u << q3)) {
+                const T hn = h[q3] - bh * cc[q3];
+                if (TR && bh != T(0)) eacc += (double)h[q3] * (double)hn / (double)bh;
+                h[q3] = hn;
+            }
         }
         hx[x] = h[0];
         hy[x] = h[1];
@@ -562,6 +586,11 @@ __global__ void __launch_bounds__(kMidThreads, 1)
 #pragma unroll
             for (int r = 0; r < R; ++r)
                 if (cl[r].x < NL && !(cl[r].f & F_FACE)) h_cell(r, nullptr, 0u, std::false_type{});
+        }
+        if (TR && tr.energy) {   // this step's energy: one block reduction, one atomic per CTA
+            const double sum = block_sum(eacc);
+            if (threadIdx.x == 0 && sum != 0.0) atomicAdd(tr.energy + m, sum * tr.dt);
+            eacc = 0.0;
         }
         __syncthreads();
     }
@@ -687,7 +716,8 @@ static int mid_buffers(Grid &G, int slot, const MidGeo &mg, int64_t epochs, void
     return PARAEXP_OK;
 }
 
-int k_leapfrog_mid(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc, const void *q_dev) {
+int k_leapfrog_mid(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc, const void *q_dev,
+                   const TraceDev *tr) {
     if (nsteps <= 0) return PARAEXP_OK;
     Grid &g = *const_cast<Grid *>(ka.g);
     if (nsrc > 16) return fail(PARAEXP_EINVAL, "mid leapfrog: at most 16 sources");
@@ -711,13 +741,19 @@ int k_leapfrog_mid(const KernelArgs &ka, void *state, int64_t nsteps, int nsrc, 
         constexpr bool HA = decltype(tHA)::value;
         constexpr int R = mid_R<T>();
         const size_t smem = mid_smem(mg, sizeof(T));
-        auto kern = leapfrog_mid_kernel<T, EM, HA, R>;
+        const bool trace = tr && (tr->energy || (tr->probe && tr->np > 0));
+        auto kern = trace ? leapfrog_mid_kernel<T, EM, HA, R, true> : leapfrog_mid_kernel<T, EM, HA, R, false>;
+        TraceDev trm;
+        if (trace) {
+            trm = *tr;
+            if (!trm.probe) trm.np = 0;
+        }
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         Dev<T> D = make_dev<T>(g);
         Coef<T, EM, HA> cf = make_coef<T, EM, HA>(g, 1.0);
         T *st = (T *)state;
         const T *q = (const T *)q_dev;
-        void *args[] = {&D, &cf, &mg, &st, &nsteps, &sl, &q, &xb, &tag0};
+        void *args[] = {&D, &cf, &mg, &st, &nsteps, &sl, &q, &xb, &tag0, &trm};
         if (cudaLaunchCooperativeKernel((const void *)kern, dim3(mg.ncta), dim3(kMidThreads), args, smem,
                                         (cudaStream_t)ka.stream) != cudaSuccess)
             return check_cuda("leapfrog mid (cooperative launch)");

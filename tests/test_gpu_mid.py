@@ -191,3 +191,31 @@ def test_leapfrog_path_reported():
         g = pe.Grid(*n, d0=1e-3, dt_frac=0.95, kernels=kern)
         assert g.info()["leapfrog_path"] == path, (n, kern)
         g.close()
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_mid_leapfrog_trace(dtype):
+    """f1 on a mid-size grid: the resident kernel's per-step energy (block reductions + one atomic
+    per CTA per step) and probe values (owner threads) against the oracle's step-by-step trace,
+    in ONE launch (per-edge eps with PEC cells)."""
+    import torch
+    from gpu_util import TOL, rel_l2, to_dev, to_host
+    n = (33, 27, 21)
+    kw = _grid_kw("edge", n)
+    og = fit.Grid(*n, dt_frac=0.95, dtype=dtype, **kw)
+    lg = pe.Grid(*n, dt_frac=0.95, dtype=dtype, **kw)
+    assert lg.info()["leapfrog_path"] == pe.abi.PATH_MID
+    e, h = inputs(og, *random_fields(*n, seed=31))
+    src = [gauss_sine(2, 16, 13, 10, f0=40e9, bw=40e9)]
+    src = [s for s in src if og.cE[og.edge_dof(s.comp, s.i, s.j, s.k)] != 0]
+    probes = [(2, 16, 13, 10), (0, 5, 7, 3), (1, 30, 0, 20), (2, 1, 26, 0)]
+    probes = [q for q in probes if og.cE[og.edge_dof(*q)] != 0]
+    ref_e, ref_h, ref_en, ref_pr = fit.leapfrog_trace(og, e, h, 150, src, t0=1e-12, probes=probes)
+    te, th = to_dev(e, lg), to_dev(h, lg)
+    st, en, pr = pe.leapfrog_trace(lg, te, th, 150, src, 1e-12, probes=probes)
+    torch.cuda.synchronize()
+    assert st["kernel_launches"] < 10, st
+    assert_parity((to_host(te), to_host(th)), (ref_e, ref_h), dtype, "mid trace fields")
+    assert rel_l2(en.cpu().numpy(), ref_en) <= TOL[dtype]
+    assert rel_l2(pr.cpu().numpy(), ref_pr) <= TOL[dtype]
+    lg.close()
