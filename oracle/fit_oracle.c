@@ -17,12 +17,17 @@
  * Out-of-range neighbours (index > n or < 0) read as 0 (virtual entries).
  *
  * All arithmetic is fp64.  Loops are plain; OpenMP only splits the outer k loop
- * (no blocking, no fusion, no reordering of the per-entry arithmetic).
+ * (no blocking, no fusion, no reordering of the per-entry arithmetic).  Every entry is
+ * computed independently, so the thread count never changes a result; grids below
+ * OR_OMP_MIN points per component run on one thread (a fork/join per half-step costs more
+ * than the loop there, and oversubscribes the host when tests run in parallel).
  */
 #include <math.h>
 #include <stdlib.h>
 #include <stdint.h>
 #include <string.h>
+
+#define OR_OMP_MIN 32768L
 
 typedef struct {
     int nx, ny, nz;
@@ -153,7 +158,7 @@ void or_curl(int nx, int ny, int nz, const double *e, double *out) {
     dims_t D = {nx, ny, nz};
     long Np = (long)(nx + 1) * (ny + 1) * (nz + 1);
     const double *ex = e, *ey = e + Np, *ez = e + 2 * Np;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if(Np >= OR_OMP_MIN)
     for (long k = 0; k <= nz; ++k)
         for (long j = 0; j <= ny; ++j)
             for (long i = 0; i <= nx; ++i) {
@@ -168,7 +173,7 @@ void or_curlT(int nx, int ny, int nz, const double *h, double *out) {
     dims_t D = {nx, ny, nz};
     long Np = (long)(nx + 1) * (ny + 1) * (nz + 1);
     const double *hx = h, *hy = h + Np, *hz = h + 2 * Np;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if(Np >= OR_OMP_MIN)
     for (long k = 0; k <= nz; ++k)
         for (long j = 0; j <= ny; ++j)
             for (long i = 0; i <= nx; ++i) {
@@ -195,7 +200,7 @@ void or_leapfrog(int nx, int ny, int nz, const double *cE, const double *cH, lon
     double *hx = h, *hy = h + Np, *hz = h + 2 * Np;
     for (long m = 0; m < nsteps; ++m) {
         /* e-half-step: reads h only, so the update may be done in place */
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if(Np >= OR_OMP_MIN)
         for (long k = 0; k <= nz; ++k)
             for (long j = 0; j <= ny; ++j)
                 for (long i = 0; i <= nx; ++i) {
@@ -206,7 +211,7 @@ void or_leapfrog(int nx, int ny, int nz, const double *cE, const double *cH, lon
                 }
         for (int s = 0; s < nsrc; ++s) e[src_dof[s]] = e[src_dof[s]] - q[m * nsrc + s];
         /* h-half-step: reads e only */
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if(Np >= OR_OMP_MIN)
         for (long k = 0; k <= nz; ++k)
             for (long j = 0; j <= ny; ++j)
                 for (long i = 0; i <= nx; ++i) {
@@ -229,7 +234,7 @@ void or_apply_A(int nx, int ny, int nz, const double *sE, const double *sH,
     long Np = (long)(nx + 1) * (ny + 1) * (nz + 1);
     const double *ex = xe, *ey = xe + Np, *ez = xe + 2 * Np;
     const double *hx = xh, *hy = xh + Np, *hz = xh + 2 * Np;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if(Np >= OR_OMP_MIN)
     for (long k = 0; k <= nz; ++k)
         for (long j = 0; j <= ny; ++j)
             for (long i = 0; i <= nx; ++i) {
@@ -265,15 +270,15 @@ int or_num_threads(void) {
  * 2 last.  Elementwise updates are plain loops (OpenMP splits the index range only); the
  * association of each update is the one written above.                                  */
 static void axpy2(long n, double *y, double a, const double *w, double b, const double *u) {
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if(n >= OR_OMP_MIN)
     for (long i = 0; i < n; ++i) y[i] = (y[i] + a * w[i]) + b * u[i];
 }
 static void xpay(long n, double *out, const double *x, double e2, const double *w) {
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if(n >= OR_OMP_MIN)
     for (long i = 0; i < n; ++i) out[i] = x[i] + e2 * w[i];
 }
 static void axpy1(long n, double *y, double c, const double *x) {
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if(n >= OR_OMP_MIN)
     for (long i = 0; i < n; ++i) y[i] = y[i] + c * x[i];
 }
 
