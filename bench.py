@@ -349,7 +349,7 @@ def main():
         # ---- e2e: the same C-ABI call with HOST buffers (pinned): the library copies u0 in and
         # (e_out, h_out) out inside the call, inside the timed region ----
         e_host = torch.empty(3 * grid.npts, dtype=tdt, pin_memory=True)
-        h_host = torch.empty_like(e_host)
+        h_host = torch.empty(3 * grid.npts, dtype=tdt, pin_memory=True)   # empty_like would not pin
         u0_host = None
         if u0 is not None:
             u0_host = (u0[0].cpu().pin_memory(), u0[1].cpu().pin_memory())

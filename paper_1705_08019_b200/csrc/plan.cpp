@@ -157,7 +157,7 @@ static void taylor_coefficients(int m, std::vector<double> &dre, std::vector<dou
     }
 }
 
-// ---- theta_m (reading 16; parity unpinned) --------------------------------------------
+// ---- theta_m (reading 16; the oracle side is pinned in tests/test_oracle_theta.py) -----------
 // max over x = j*theta/800, j = 0..800, of |p(ix) - e^{ix}|; p interpolates exp on
 // i[-a, a], a = 1.05 theta (Leja), or is the degree-m Taylor polynomial.
 static double poly_error(int method, int m, double theta) {

@@ -141,7 +141,8 @@ def test_theta_matches_oracle(method, m, tol):
 
 
 def test_theta_reference_table():
-    """Regression against the theta table of SURVEY 8(c) (parity unpinned, ~1%)."""
+    """Regression against the theta table of SURVEY 8(c) (~1%; the oracle's theta_m is pinned in
+    tests/test_oracle_theta.py and compared with the library above)."""
     ref = {(16, 1e-2): 11.9, (64, 1e-8): 41.3, (100, 1e-13): 61.1, (48, 1e-8): 27.9}
     for (m, tol), v in ref.items():
         assert abs(pe.theta("leja", m, tol) / v - 1) < 0.01

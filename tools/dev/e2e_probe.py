@@ -17,7 +17,7 @@ td = g.torch_dtype()
 ed = torch.zeros(3 * g.npts, dtype=td, device="cuda:0")
 hd = torch.zeros_like(ed)
 eh = torch.empty(3 * g.npts, dtype=td, pin_memory=True)
-hh = torch.empty_like(eh)
+hh = torch.empty(3 * g.npts, dtype=td, pin_memory=True)
 kw = dict(sources=w.sources, method=w.method, m=w.m, s=w.s, eps_A=w.eps_A)
 for outs, name in (((ed, hd), "device"), ((eh, hh), "host"), ((ed, hd), "device"), ((eh, hh), "host")):
     torch.cuda.synchronize()
