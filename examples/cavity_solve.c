@@ -9,6 +9,7 @@
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "paraexp.h"
 
@@ -38,7 +39,13 @@ int main(void) {
     const double pi = 3.14159265358979323846, bw = 50e9, tau = 2.0 / (pi * bw);
     paraexp_source src = {2, 3, 5, 4, PARAEXP_SRC_GAUSS_SINE, 1.0, 1.0, tau, 100e9, 4.0 * tau};
     const int64_t n = 3 * info.npts, nsteps = 2000;
-    double *e = calloc(n, sizeof(double)), *h = calloc(n, sizeof(double));
+    /* ParaExp outputs in pinned host memory from the library (fast copy-out), the leapfrog
+     * state in ordinary pageable memory: both are valid host field arguments */
+    double *e = NULL, *h = NULL;
+    CHECK(paraexp_host_alloc(n * sizeof(double), (void **)&e));
+    CHECK(paraexp_host_alloc(n * sizeof(double), (void **)&h));
+    memset(e, 0, n * sizeof(double));
+    memset(h, 0, n * sizeof(double));
     double *el = calloc(n, sizeof(double)), *hl = calloc(n, sizeof(double));
 
     paraexp_expmv_opts o = {PARAEXP_LEJA, 0, 0, 1e-12, 0.0, 0, 0.0};
@@ -56,8 +63,8 @@ int main(void) {
            paraexp_version(), info.nx, info.ny, info.nz, info.dt, (long long)nsteps,
            (long long)st.a_applications, st.m, st.s_first, (long long)st.kernel_launches,
            sqrt(num / den));
-    free(e);
-    free(h);
+    paraexp_host_free(e);
+    paraexp_host_free(h);
     free(el);
     free(hl);
     paraexp_grid_destroy(g);

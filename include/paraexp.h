@@ -408,6 +408,16 @@ double paraexp_optimal_tolerance(double dt, double beta, double norm_A, int32_t 
  * (reading 16), method TAYLOR or LEJA.  Cached. */
 double paraexp_theta(int32_t method, int32_t m, double eps_A);
 
+/* Page-locked (pinned) host memory for field arguments passed as HOST pointers: the library
+ * copies host fields with cudaMemcpyAsync, which reaches the link's bandwidth only from pinned
+ * memory (pageable buffers go through the driver's staging path, several times slower for the
+ * 815 MB of a C3 fp64 output).  *out is owned by the caller until paraexp_host_free; usable
+ * from any device (portable).  The memory is not initialised.
+ * Errors: EINVAL (bytes == 0, out == NULL), ENOMEM / ECUDA (no driver, pinning failed). */
+int paraexp_host_alloc(size_t bytes, void **out);
+/* Release memory from paraexp_host_alloc (NULL is a no-op). */
+void paraexp_host_free(void *p);
+
 const char *paraexp_strerror(int code);
 const char *paraexp_last_error(void);
 /* library version string, e.g. "paraexp-b200 0.1 (sm_100a)" */

@@ -138,6 +138,34 @@ def _field(t, grid, name, writable=True):
     return C.c_void_p(t.data_ptr())
 
 
+class HostField:
+    """paraexp_host_alloc / paraexp_host_free: one canonical-layout field (3*npts values of the
+    grid's dtype) in page-locked host memory, viewed as a torch CPU tensor (``.tensor``, no
+    copy) that solve / leapfrog / expmv accept as a host buffer."""
+
+    def __init__(self, grid: "Grid"):
+        import numpy as np
+        import torch
+        dt = np.float64 if grid.dtype == "f64" else np.float32
+        self.nbytes = 3 * grid.npts * np.dtype(dt).itemsize
+        h = C.c_void_p()
+        check(abi.lib.paraexp_host_alloc(self.nbytes, C.byref(h)), "paraexp_host_alloc")
+        self._p = h
+        buf = (C.c_uint8 * self.nbytes).from_address(h.value)
+        self.tensor = torch.from_numpy(np.frombuffer(buf, dtype=dt))
+
+    @property
+    def ptr(self) -> int:
+        return self._p.value
+
+    def close(self):
+        """Free the pinned memory; ``tensor`` must not be used afterwards."""
+        if getattr(self, "_p", None):
+            self.tensor = None
+            abi.lib.paraexp_host_free(self._p)
+            self._p = None
+
+
 def make_sources(sources: Optional[Iterable]) -> tuple:
     """Sources as any objects with comp, i, j, k, kind, weight, amp, t_param, f0, t_delay."""
     srcs = list(sources or [])

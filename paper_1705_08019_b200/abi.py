@@ -136,6 +136,8 @@ _sigs = {
                                     C.c_double, C.c_double, C.POINTER(paraexp_plan_info)]),
     "paraexp_theta": (C.c_double, [C.c_int32, C.c_int32, C.c_double]),
     "paraexp_optimal_tolerance": (C.c_double, [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_int32)]),
+    "paraexp_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "paraexp_host_free": (None, [_vp]),
     "paraexp_strerror": (C.c_char_p, [C.c_int]),
     "paraexp_last_error": (C.c_char_p, []),
     "paraexp_version": (C.c_char_p, []),

@@ -799,6 +799,21 @@ const char *paraexp_strerror(int code) {
 
 const char *paraexp_last_error(void) { return pe::t_last_error.c_str(); }
 
+int paraexp_host_alloc(size_t bytes, void **out) {
+    if (!out || bytes == 0) return pe::fail(PARAEXP_EINVAL, "paraexp_host_alloc: need bytes > 0 and out != NULL");
+    *out = nullptr;
+    const cudaError_t e = cudaHostAlloc(out, bytes, cudaHostAllocPortable);
+    if (e == cudaSuccess) return PARAEXP_OK;
+    *out = nullptr;
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation) return pe::fail(PARAEXP_ENOMEM, "paraexp_host_alloc: cannot pin that much host memory");
+    return pe::fail(PARAEXP_ECUDA, std::string("paraexp_host_alloc: ") + cudaGetErrorString(e));
+}
+
+void paraexp_host_free(void *p) {
+    if (p && cudaFreeHost(p) != cudaSuccess) cudaGetLastError();
+}
+
 int paraexp_partition(int64_t nsteps, int32_t p, int64_t *bounds) {
     if (p < 1 || nsteps < p || !bounds) return pe::fail(PARAEXP_EINVAL, "need p >= 1 and nsteps >= p");
     const int64_t M = nsteps / p;

@@ -157,6 +157,39 @@ def test_host_pointer_fields(pinned):
     assert eo_h.abs().max() > 0
 
 
+def test_host_alloc_pinned_fields():
+    """paraexp_host_alloc: page-locked memory (cudaPointerGetAttributes says host-registered via
+    torch's is_pinned), usable as e_out / h_out of a solve with the bits of the device-buffer
+    solve, against the oracle too; free is idempotent."""
+    import torch
+    n = (20, 12, 7)
+    og = fit.Grid(*n, d0=1e-3, dt_frac=0.9)
+    lg = pe.Grid(*n, d0=1e-3, dt_frac=0.9)
+    src = [gauss_sine(2, 5, 5, 3, f0=60e9, bw=60e9)]
+    he, hh = pe.HostField(lg), pe.HostField(lg)
+    assert he.nbytes == 3 * lg.npts * 8 and he.ptr % 4096 == 0
+    assert he.tensor.is_pinned() and hh.tensor.is_pinned()
+    he.tensor.fill_(7.0)
+    hh.tensor.fill_(7.0)
+    de = torch.zeros(3 * lg.npts, dtype=torch.float64, device="cuda:0")
+    dh = torch.zeros_like(de)
+    pe.solve(lg, 24, 3, src, m=12, s=2, rho=og.rho_cfl, e_out=de, h_out=dh)
+    pe.solve(lg, 24, 3, src, m=12, s=2, rho=og.rho_cfl, e_out=he.tensor, h_out=hh.tensor)
+    torch.cuda.synchronize()
+    assert torch.equal(de.cpu(), he.tensor) and torch.equal(dh.cpu(), hh.tensor)
+    rho = og.rho_cfl
+    ref = fit.paraexp(og, src, 0.0, 24, 3, lambda tau: fit.make_plan("leja", 12, 2, tau, rho))
+    for got, want in ((he.tensor.numpy(), ref[0]), (hh.tensor.numpy(), ref[1])):
+        assert np.linalg.norm(got - want) <= 1e-10 * np.linalg.norm(want)
+    he.close()
+    he.close()
+    hh.close()
+    with pytest.raises(pe.ParaexpError) as ei:
+        import ctypes
+        pe.check(pe.abi.lib.paraexp_host_alloc(0, ctypes.byref(ctypes.c_void_p())), "paraexp_host_alloc")
+    assert ei.value.code == pe.EINVAL
+
+
 def test_c_example_runs(tmp_path):
     """examples/cavity_solve.c through the C ABI from plain C with host buffers: runs and prints
     a finite, nonzero ParaExp (exact-exponential tails) vs serial leapfrog gap on C1 -- large

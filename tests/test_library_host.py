@@ -29,6 +29,24 @@ def test_exports_every_declared_symbol():
     assert declared == set(abi.EXPORTED)
 
 
+def test_host_alloc_argument_checks():
+    """paraexp_host_alloc validates its arguments before touching the driver; without a GPU
+    the allocation itself fails loudly (ECUDA / ENOMEM) and leaves *out NULL; free(NULL) is a
+    no-op."""
+    import ctypes as C
+    h = C.c_void_p(1234)
+    assert abi.lib.paraexp_host_alloc(0, C.byref(h)) == pe.EINVAL
+    assert abi.lib.paraexp_host_alloc(64, None) == pe.EINVAL
+    rc = abi.lib.paraexp_host_alloc(4096, C.byref(h))
+    if rc == 0:                       # a driver is present
+        assert h.value
+        abi.lib.paraexp_host_free(h)
+    else:
+        assert rc in (abi.ECUDA, abi.ENOMEM) and not h.value
+        assert b"paraexp_host_alloc" in abi.lib.paraexp_last_error()
+    abi.lib.paraexp_host_free(None)
+
+
 def test_partition_and_schedule():
     ex = GOLD["partition_example"]
     b = pe.partition(ex["nsteps"], ex["p"])
