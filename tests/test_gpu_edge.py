@@ -167,7 +167,7 @@ def test_host_alloc_pinned_fields():
     lg = pe.Grid(*n, d0=1e-3, dt_frac=0.9)
     src = [gauss_sine(2, 5, 5, 3, f0=60e9, bw=60e9)]
     he, hh = pe.HostField(lg), pe.HostField(lg)
-    assert he.nbytes == 3 * lg.npts * 8 and he.ptr % 4096 == 0
+    assert he.nbytes == 3 * lg.npts * 8 and he.ptr % 256 == 0
     assert he.tensor.is_pinned() and hh.tensor.is_pinned()
     he.tensor.fill_(7.0)
     hh.tensor.fill_(7.0)
