@@ -140,7 +140,7 @@ def _run_leapfrog_expmv(w, dtype, nlf, m, centers, half=6, seed=11, t0=0.0):
     torch.cuda.empty_cache()
 
 
-def _run_solve(w, dtype, nsteps, p, m, centers, half=5, seed=13, t0=0.0):
+def _run_solve(w, dtype, nsteps, p, m, centers, half=5, seed=13, t0=0.0, host_io=False):
     """full-grid CUDA paraexp_solve (random u0 + the workload's sources, fixed Leja plan
     (m, s = 1) per sub-interval) vs the oracle's sequential Algorithm 1 on sub-grids"""
     import torch
@@ -153,6 +153,19 @@ def _run_solve(w, dtype, nsteps, p, m, centers, half=5, seed=13, t0=0.0):
                   e_out=eo, h_out=ho)
     torch.cuda.synchronize()
     assert st["leapfrog_steps"] == nsteps
+    if host_io:
+        # bench.py's e2e path at full size: u0 and the outputs as pinned HOST fields from
+        # paraexp_host_alloc, staged by the library -- the bits of the device-buffer solve
+        hf = [pe.HostField(lg) for _ in range(4)]
+        hf[0].tensor.copy_(e0)
+        hf[1].tensor.copy_(h0)
+        hf[2].tensor.fill_(float("nan"))
+        hf[3].tensor.fill_(float("nan"))
+        pe.solve(lg, nsteps, p, w.sources, t0=t0, u0=(hf[0].tensor, hf[1].tensor), method="leja", m=m,
+                 s=1, rho=rho, e_out=hf[2].tensor, h_out=hf[3].tensor)
+        assert torch.equal(hf[2].tensor, eo.cpu()) and torch.equal(hf[3].tensor, ho.cpu())
+        for f in hf:
+            f.close()
     # domain of dependence: all leapfrog steps + p propagators of m + the dt/2 Taylor (24 s)
     half_plan = fit.half_step_plan(fit.Grid(1, 1, 1, d0=w.d0, dt=dt), rho)
     R = nsteps + p * m + half_plan.m * half_plan.s + 2
@@ -181,7 +194,7 @@ def test_c3_fullsize_leapfrog_expmv_m150(dtype):
 def test_c3_fullsize_solve(dtype):
     """C3 256^3: paraexp_solve with p = 8 sub-intervals at full size (random u0 + source)."""
     w = config_c3(dtype)
-    _run_solve(w, dtype, 16, 8, 4, [(128, 128, 32), (250, 3, 190)])
+    _run_solve(w, dtype, 16, 8, 4, [(128, 128, 32), (250, 3, 190)], host_io=dtype == "f64")
 
 
 def test_c4_fullsize_spiral():
