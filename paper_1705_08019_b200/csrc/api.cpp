@@ -1750,7 +1750,7 @@ static int solve_impl(paraexp_grid *grid, paraexp_comm *comm, const paraexp_sour
     const bool coll = comm && (world > 1 || getenv("PARAEXP_FORCE_COLLECTIVES"));
     CommCtx cctx{comm, &G};
     paraexp_comm_view view;
-    if (comm && world > 1 && !(opts && opts->rho > 0)) {
+    if (coll && !(opts && opts->rho > 0)) {      // also for a forced one-rank communicator (tests)
         view.ctx = &cctx;
         view.bcast_rho = bcast_rho_nccl;
     }

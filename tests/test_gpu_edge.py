@@ -120,6 +120,17 @@ def test_nccl_path_one_rank(monkeypatch, window):
     # energy rows: block partial sums are combined with atomics (order not reproducible)
     np.testing.assert_allclose(outs[1][2], outs[0][2], rtol=1e-13, atol=0)
     assert outs[1][4]["ms_reduce"] > 0          # the collective ran
+    # auto rho (K5) goes through ncclBroadcast(rho) when the collectives are on: same plan, same bits
+    auto = []
+    for c in (None, comm):
+        eo = torch.zeros(3 * lg.npts, dtype=torch.float64, device="cuda:0")
+        ho = torch.zeros_like(eo)
+        st = pe.solve(lg, 40, 4, src, eps_A=1e-10, e_out=eo, h_out=ho, comm=c)
+        torch.cuda.synchronize()
+        auto.append((eo.cpu().numpy(), ho.cpu().numpy(), st))
+    assert auto[0][2]["rho"] == auto[1][2]["rho"] and 0 < auto[1][2]["rho"] <= og.rho_cfl * (1 + 1e-12)
+    assert (auto[0][2]["m"], auto[0][2]["s_first"]) == (auto[1][2]["m"], auto[1][2]["s_first"])
+    assert np.array_equal(auto[0][0], auto[1][0]) and np.array_equal(auto[0][1], auto[1][1])
     comm.close()
 
 
